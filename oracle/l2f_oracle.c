@@ -151,8 +151,9 @@ static void draw_block(const or_config* cfg, uint64_t env_id, uint64_t t, uint32
     or_philox4x32_10(ctr, key, out);
 }
 
-/* 24-bit uniform in (0,1): u = ((x >> 8) + 1/2) 2^-24 (Q20). */
-double or_uniform(uint32_t x) { return ((double)(x >> 8) + 0.5) * (1.0 / 16777216.0); }
+/* 23-bit uniform in (0,1): u = ((x >> 9) + 1/2) 2^-23 (Q20).  Every value is exactly
+ * representable in fp32 (2k+1 < 2^24), so both sides of the parity test draw the same u. */
+double or_uniform(uint32_t x) { return ((double)(x >> 9) + 0.5) * (1.0 / 8388608.0); }
 
 /* Box-Muller (Q20): (x_a, x_b) -> (r cos 2 pi u2, r sin 2 pi u2), r = sqrt(-2 ln u1). */
 void or_box_muller(uint32_t xa, uint32_t xb, double z[2])

@@ -47,8 +47,12 @@ def test_philox_kat_random123():
 
 
 def test_uniform_range_and_resolution():
-    assert oracle.uniform(0) == 0.5 / 2 ** 24
-    assert oracle.uniform(0xFFFFFFFF) == 1 - 0.5 / 2 ** 24
+    assert oracle.uniform(0) == 0.5 / 2 ** 23
+    assert oracle.uniform(0xFFFFFFFF) == 1 - 0.5 / 2 ** 23
+    # every uniform is exactly representable in fp32 (Q20)
+    for x in (0, 511, 512, 0x80000000, 0xFFFFFE00, 0xFFFFFFFF, 123456789):
+        u = oracle.uniform(x)
+        assert float(np.float32(u)) == u
     assert 0 < oracle.uniform(12345678) < 1
 
 
