@@ -1,0 +1,411 @@
+#!/usr/bin/env python3
+"""Benchmark of the batched quadrotor env hot path (arXiv 2311.13081) on B200.
+
+  python bench.py --gpus N --steps K --warmup W [--impl reference]
+  (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...)
+
+One bench "step" = one pass of the whole hot path over the
+per-GPU batch: l2f_rollout of T = 1000 env-steps with the actor MLP on tensor cores, noise,
+reward + curriculum, termination, auto-reset and DR-free C5 physics, then the episode-stat
+reduction and (N > 1) its NCCL all-reduce.  Workload (BASELINE configs[4], per GPU shard):
+2^21 envs per GPU x 1000 steps; at N = 8 this is exactly the 2^24-env C5 config; weak scaling.
+
+Prints ONE JSON line (rank 0).  Secondary measurements of the other configs (C3 single-step
+API against the HBM roofline, C4, the open-loop dynamics mode) ride along under "modes".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+T_ROLLOUT = 1000
+ENVS_PER_GPU = 1 << 21
+METRIC = "env-steps/s (sim flight-s per wall-s) at 1/2/4/8 B200 vs roofline"
+DT = 0.01
+# Algorithmic work per env-step:
+#  HBM bytes of one l2f_step with DR (C3): reads state 68 + action 16 + dist 24 + DR 20 +
+#  ep counters 8; writes state 68 + counters 8 + history slot 16 + obs_core 72 + reward 4 + flags 1
+STEP_BYTES_DR = 68 + 16 + 24 + 20 + 8 + 68 + 8 + 16 + 72 + 4 + 1
+#  tensor-core FLOPs of the actor MLP 146 -> 64 -> 64 -> 4 per env-step
+MLP_FLOPS = 2 * (146 * 64 + 64 * 64 + 64 * 4)
+#  scalar (non-tensor) operations of one fused MLP env-step, counted from the method as
+#  written with a fused multiply-add counted once (DESIGN.md section 5 table)
+ALU_OPS_PER_ENV_STEP = 1372
+SMS = 148
+
+
+def peaks():
+    p = {"hbm_gbs": 6551.4, "bf16_tflops": 1653.4, "bf16_tflops_sustained": 1387.6, "sm_max_mhz": 1965.0,
+         "source": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({k: m[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained", "sm_max_mhz") if k in m})
+        p["source"] = "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        pass
+    return p
+
+
+# ----------------------------------------------------------------------------------------
+# clocks during the timed region
+# ----------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.idx), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------------------
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torch.distributed.run (one rank per GPU)")
+    return world, rank, local
+
+
+def cpu_baseline(cfg, policy_w, target_s=12.0, nthreads=None):
+    """The oracle as it stands (FP64 C, std::thread-style pthreads over all host cores) on a
+    bounded sample of the same workload: n_s envs x T_s steps of the fused MLP env step."""
+    import numpy as np
+
+    import oracle
+
+    nthreads = nthreads or os.cpu_count() or 1
+    pol = oracle.PolicyHandle(policy_w)
+    n_s = max(nthreads * 8, 64)
+    ids = np.arange(n_s, dtype=np.uint64) * 997
+    E = oracle.reset_many(cfg, ids, 0)
+    t0 = time.perf_counter()
+    oracle.rollout(cfg, E.copy(), ids, 0, 4, oracle.MODE_POLICY, policy=pol, nthreads=nthreads)
+    probe = time.perf_counter() - t0
+    T_s = int(max(4, min(1000, target_s / max(probe / 4, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.rollout(cfg, E, ids, 0, T_s, oracle.MODE_POLICY, policy=pol, nthreads=nthreads)
+    el = time.perf_counter() - t0
+    v = n_s * T_s / el
+    return {"value": v, "unit": "env-steps/s", "cores": nthreads, "kind": "oracle",
+            "sample": f"{n_s} envs (ids spread over the workload) x {T_s} fused MLP env-steps, FP64 C oracle, "
+                      f"{el:.1f} s wall"}
+
+
+def reference_arm(args):
+    """--impl reference: the oracle (the base contract's reference arm for this tier)."""
+    world, rank, local = dist_setup(args)
+    if rank != 0:
+        return
+    import inputs
+
+    cfg = inputs.config_c5()
+    W = inputs.policy_weights(18 + 4 * cfg["n_hist"], 64, seed=7, out_bias=inputs.hover_policy_bias())
+    target = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    cb = None
+    for k in range(args.warmup + args.steps):
+        cb = cpu_baseline(cfg, W, target_s=target)
+        if k >= args.warmup:
+            vals.append(cb["value"])
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "env-steps/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C5 per-GPU shard (bounded oracle sample)", "envs_per_gpu": ENVS_PER_GPU,
+                       "steps_per_rollout": T_ROLLOUT},
+            "cpu_baseline": dict(cb, value=v),
+            "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "sim_seconds_per_wall_second": v * DT}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--envs-per-gpu", type=int, default=ENVS_PER_GPU)
+    ap.add_argument("--T", type=int, default=T_ROLLOUT)
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="mlp", choices=["mlp", "step", "open"])
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import inputs
+    import paper_2311_13081_b200 as pkg
+
+    world, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    pk = peaks()
+    n = args.envs_per_gpu
+    T = args.T
+    stream = torch.cuda.current_stream()
+
+    cfg = inputs.config_c5()
+    W = inputs.policy_weights(18 + 4 * cfg["n_hist"], 64, seed=7, out_bias=inputs.hover_policy_bias())
+    env = pkg.Env(cfg, n, env_id_offset=rank * n, device=dev)
+    env.reset()
+    pol = pkg.Policy(W, device=dev)
+    stats_buf = torch.zeros(8, dtype=torch.float64, device=dev)
+
+    def one_step():
+        if args.mode == "mlp":
+            env.rollout(T, policy=pol)
+        else:
+            env.rollout(T)  # open loop, Philox random actions
+        st = env.episode_stats(reset=True)
+        if world > 1:
+            dist.all_reduce(st)
+        stats_buf.add_(st)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier()
+    stats_buf.zero_()
+    l0 = pkg.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            one_step()
+        ev1.record(stream)
+        barrier()
+    launches = pkg.launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms_max = float(t_max.item())
+    env_steps = world * n * T * args.steps
+    value = env_steps / (ms_max / 1e3)
+    stats = stats_buf.cpu().numpy()
+
+    # per-launch time of the dominant kernel (the fused rollout) on its own stream
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev2.record(stream)
+    if args.mode == "mlp":
+        env.rollout(T, policy=pol)
+    else:
+        env.rollout(T)
+    ev3.record(stream)
+    torch.cuda.synchronize()
+    k_ms = ev2.elapsed_time(ev3)
+    clocks = clk.summary()
+    f_clk = (clocks["sm_mhz"] or pk["sm_max_mhz"]) * 1e6
+    k_rate = n * T / (k_ms / 1e3)
+    alu_peak = SMS * 128 * f_clk / 1e12
+    roof = {"bound": "alu", "kernel": "rollout_mlp_kernel" if args.mode == "mlp" else "rollout_open_kernel",
+            "achieved": ALU_OPS_PER_ENV_STEP * k_rate / 1e12, "peak": alu_peak, "unit": "Tops/s",
+            "frac": ALU_OPS_PER_ENV_STEP * k_rate / 1e12 / alu_peak, "traffic": None,
+            "peak_source": f"148 SMs x 128 lanes x {f_clk / 1e6:.0f} MHz (median SM clock sampled in the timed region)",
+            "tensor": {"achieved": MLP_FLOPS * k_rate / 1e12, "peak": pk["bf16_tflops_sustained"],
+                       "unit": "TFLOP/s", "frac": MLP_FLOPS * k_rate / 1e12 / pk["bf16_tflops_sustained"],
+                       "peak_source": pk["source"] + " bf16 sustained (fp16 dense rate equal)"}}
+
+    # ---- e2e through the public host-buffer API: H2D of the policy (pinned), rollout, D2H stats
+    e2e_val, h2d = None, 0
+    if args.mode == "mlp":
+        e2e_val, h2d = e2e_rollout(args, pkg, torch, dist, env, W, T, n, world, dev, stream, barrier)
+    modes = {}
+    if not args.no_secondary and rank == 0:
+        modes = secondary(pkg, inputs, torch, dev, pk, f_clk)
+    cb = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cb = cpu_baseline(cfg, W)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32+f16mma", "data": "synthetic",
+                "config": {"workload": "C5 per-GPU shard: 2^21 envs/GPU x 1000 steps fused actor-MLP rollout "
+                                       "(146-64-64-4 tcgen05, N_H=32), obs/action noise, reward + 4-stage "
+                                       "curriculum, termination, auto-reset, disturbance; NCCL stat all-reduce",
+                           "envs_per_gpu": n, "steps_per_rollout": T, "mode": args.mode,
+                           "l2": "inputs larger than L2: env state+history 1.4 GB per GPU",
+                           "parallelism": f"env-shard x{world}"},
+                "sim_seconds_per_wall_second": value * DT,
+                "roofline": roof,
+                "e2e": {"value": e2e_val, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": 64,
+                        "api": "l2f_rollout_host (pinned host policy in, FP64 stats out)"},
+                "gpu_launches": int(launches),
+                "clocks": clocks,
+                "episode_stats": {"episodes": stats[0], "mean_len": stats[4] / max(stats[0], 1),
+                                  "mean_return": stats[5] / max(stats[0], 1)},
+                "modes": modes,
+                "cpu_baseline": cb,
+                "paper_context": {"value": 1.284e9, "unit": "env-steps/s", "hardware": "Quadro T2000 laptop GPU",
+                                  "workload": "8192 envs x 1e6 steps, forward dynamics only (P:165)"}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e_rollout(args, pkg, torch, dist, env, W, T, n, world, dev, stream, barrier):
+    hpol = pkg.HostPolicy(W)
+    h_stats = torch.zeros(8, dtype=torch.float64).pin_memory()
+    h2d = sum(int(t.numel()) * 2 for t in hpol.t.values())
+    e2e_env = env
+    for _ in range(1):
+        e2e_env.rollout_host(hpol, T, h_stats)
+    barrier()
+    t0 = time.perf_counter()
+    ev4, ev5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev4.record(stream)
+    for _ in range(args.steps):
+        e2e_env.rollout_host(hpol, T, h_stats)
+        if world > 1:
+            st = torch.from_numpy(h_stats.numpy().copy()).to(dev)
+            dist.all_reduce(st)
+    ev5.record(stream)
+    barrier()
+    e2e_ms = torch.tensor([ev4.elapsed_time(ev5)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_val = world * n * T * args.steps / (float(e2e_ms.item()) / 1e3)
+
+    return e2e_val, h2d
+
+
+def secondary(pkg, inputs, torch, dev, pk, f_clk):
+    """C3 single-step API (HBM roofline), C4 exactly, and the open-loop dynamics mode."""
+    out = {}
+    stream = torch.cuda.current_stream()
+    # C3: 2^20 envs, DR, l2f_step, ring of 8 action buffers (16 MiB each; > L2 in total with state)
+    n = 1 << 20
+    cfg = inputs.config_c3()
+    env = pkg.Env(cfg, n, device=dev)
+    env.reset()
+    acts = [torch.tensor(inputs.actions_near_hover(1, n, seed=100 + k)[0], dtype=torch.float32, device=dev)
+            for k in range(8)]
+    o = env.make_out(obs_core=True, reward=True, flags=True)
+    for k in range(20):
+        env.step(acts[k % 8], o)
+    torch.cuda.synchronize()
+    reps = 400
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(reps):
+        env.step(acts[k % 8], o)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    rate = n / (ms / 1e3)
+    gbs = STEP_BYTES_DR * n / (ms / 1e3) / 1e9
+    out["C3_step_api"] = {"value": rate, "unit": "env-steps/s", "us_per_step": ms * 1e3,
+                          "sim_seconds_per_wall_second": rate * DT,
+                          "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                                       "frac": gbs / pk["hbm_gbs"], "traffic": None,
+                                       "bytes_per_env_step": STEP_BYTES_DR, "peak_source": pk["source"]}}
+    # e2e of the step API through host buffers (pinned): H2D actions, D2H obs/reward/flags
+    ha = acts[0].cpu().pin_memory()
+    hobs = torch.empty(18, n).pin_memory()
+    hr = torch.empty(n).pin_memory()
+    hf = torch.empty(n, dtype=torch.uint8).pin_memory()
+    env.step_host(ha, hobs, hr, hf)
+    t0 = time.perf_counter()
+    for _ in range(20):
+        env.step_host(ha, hobs, hr, hf)
+    el = (time.perf_counter() - t0) / 20
+    out["C3_step_api"]["e2e"] = {"value": n / el, "unit": "env-steps/s", "h2d_bytes_per_step": 16 * n,
+                                 "d2h_bytes_per_step": 77 * n}
+    del env, acts, o
+    torch.cuda.empty_cache()
+    # open-loop dynamics-only mode (paper-comparable): 2^20 envs x 1000 steps, flags 0
+    cfg = inputs.config_c1()
+    n = 1 << 20
+    env = pkg.Env(cfg, n, device=dev)
+    env.reset()
+    env.rollout(50)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    env.rollout(1000)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    rate = n * 1000 / (ms / 1e3)
+    out["open_loop_dynamics"] = {"value": rate, "unit": "env-steps/s", "ms": ms,
+                                 "workload": "2^20 envs x 1000 steps, Philox random actions, no noise/termination",
+                                 "vs_paper_T2000": rate / 1.284e9}
+    del env
+    torch.cuda.empty_cache()
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,256 @@
+/*
+ * l2f.h -- C ABI of the B200-native batched quadrotor environment of arXiv 2311.13081
+ * ("Learning to Fly in Seconds").  libl2f.so, sm_100a.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n.  "Qn" = a reading of the paper listed
+ * in DESIGN.md section 3 (where the paper is silent).
+ *
+ * The library computes, for N independent environments, the MDP of P:131-152:
+ *   state  s = {p, q, v, omega, omega_m} (17-D), per-episode disturbance
+ *          {f_r, tau_r}, optional per-env domain-randomised parameters (Q19);
+ *   action a in [-1,1]^4 = normalised RPM setpoints;
+ *   step   first-order motor lag + polynomial RPM->thrust/torque
+ *          + rigid-body dynamics integrated with RK4 at dt (Q1);
+ *   obs    o_a = {p, R(q), v, omega, H} + noise, H = action history;
+ *   reward r(s,a,s') with curriculum-scheduled weights;
+ *   done   termination (Q14) / truncation (Q15), same-step auto-reset (Q16).
+ * and a fused rollout that evaluates the actor MLP per env between steps.
+ *
+ * Conventions for every entry point:
+ *  - All functions are extern "C", never throw, and return an l2f_status.  On a non-OK
+ *    status l2f_last_error() returns a thread-local message.
+ *  - Device pointers ("d_") are caller-owned CUDA device memory on the env's device; host
+ *    pointers ("h_") are caller-owned host memory.  The library never allocates device
+ *    memory: the caller provides a workspace of l2f_workspace_size() bytes at create time.
+ *  - Every call is asynchronous on the caller's stream (a cudaStream_t passed as void*;
+ *    NULL = the legacy default stream) unless its comment says it synchronises.  The
+ *    returned status covers argument validation and launch errors; asynchronous device
+ *    faults surface at the caller's next synchronisation.
+ *  - Layouts are structure-of-arrays: "[C][N]" means component-major, env index fastest
+ *    (element (c, i) at c*N + i), fp32 unless stated.
+ *  - Numerical divergence (non-finite state) is per env, never a global error: the env
+ *    is flagged L2F_DONE_DIVERGED | L2F_DONE_TERMINATED.
+ */
+#ifndef L2F_H
+#define L2F_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define L2F_API __attribute__((visibility("default")))
+#else
+#define L2F_API
+#endif
+
+#define L2F_ABI_VERSION 1
+#define L2F_STATE_DIM 17     /* p(3) q(4: w,x,y,z) v(3) omega(3) omega_m(4) */
+#define L2F_OBS_CORE 18      /* p(3) R(9, row-major) v(3) omega(3) */
+#define L2F_MAX_HIST 32      /* N_H upper bound                                  */
+#define L2F_DIST_DIM 6       /* f_r (world, N), tau_r (body, N m) */
+#define L2F_DR_DIM 5         /* mass, Jxx, Jyy, Jzz, thrust-curve scale factors (Q19)  */
+#define L2F_STATS_LEN 8
+#define L2F_TRACE_FIELDS 32
+
+typedef struct l2f_env l2f_env; /* opaque */
+
+typedef enum {
+    L2F_OK = 0,
+    L2F_ERR_INVALID_ARGUMENT = 1,
+    L2F_ERR_CUDA = 2,
+    L2F_ERR_WORKSPACE_TOO_SMALL = 3,
+    L2F_ERR_NOT_SUPPORTED = 4,
+    L2F_ERR_BAD_STATE = 5
+} l2f_status;
+
+/* Feature flags (l2f_config.flags). */
+enum {
+    L2F_OBS_NOISE = 1u << 0,      /* Gaussian observation noise on p, R, v, omega   */
+    L2F_ACTION_NOISE = 1u << 1,   /* Gaussian exploration noise on actions (Q7)      */
+    L2F_TERMINATION = 1u << 2,    /* box / speed termination (Q14)                   */
+    L2F_AUTO_RESET = 1u << 3,     /* same-step reset of ended envs (Q16)                    */
+    L2F_DISTURBANCE = 1u << 4,    /* per-episode random force/torque                */
+    L2F_DOMAIN_RAND = 1u << 5     /* per-episode mass/inertia/thrust factors (Q19)          */
+};
+
+/* Per-env step flags (l2f_step_out.flags, trace field 26). */
+enum { L2F_DONE_TERMINATED = 1, L2F_DONE_TRUNCATED = 2, L2F_DONE_DIVERGED = 4, L2F_DONE_RESET = 8 };
+
+/* Episode statistics (l2f_episode_stats output, FP64). */
+enum {
+    L2F_ST_EPISODES = 0,  /* episodes that ended (terminated or truncated)   */
+    L2F_ST_TERMINATED,
+    L2F_ST_TRUNCATED,
+    L2F_ST_DIVERGED,
+    L2F_ST_SUM_LEN,       /* sum of episode lengths (steps)                  */
+    L2F_ST_SUM_RET,       /* sum of episode returns                          */
+    L2F_ST_SUM_RET_SQ,    /* sum of squared episode returns                  */
+    L2F_ST_ENV_STEPS      /* env-steps executed                              */
+};
+
+/* Quadrotor parameters. m = 0.027 kg and T_m = 0.15 s are the paper's. */
+typedef struct {
+    double mass;            /* kg */
+    double J[3];            /* diagonal inertia, kg m^2 */
+    double rotor_pos[4][3]; /* body frame, m */
+    double spin_dir[4];     /* +1 / -1 */
+    double thrust_c[3];     /* per-rotor thrust f(w) = c0 + c1 w + c2 w^2 (N), w in rotor-speed units */
+    double torque_c;        /* yaw torque per unit thrust (m) */
+    double motor_tau;       /* first-order motor time constant T_m (s) */
+    double rpm_min, rpm_max;/* rotor-speed range */
+    double gravity;         /* m/s^2, acting along -z */
+} l2f_params;
+
+/* Reward constants of P:148-151; C_rab is a 4-vector in normalised action space (Q9). */
+typedef struct {
+    double C_rp, C_rq, C_rv, C_rw, C_ra;
+    double C_rab[4];
+    double C_rs;
+} l2f_reward_weights;
+
+/* Curriculum: stage k = floor(t / interval); each weight w_k = w_{k-1} * factor,
+ * clamped at target in the direction of travel; the exploration sigma follows the same
+ * scheme.  interval = 0 keeps stage 0.  C_rab is not scheduled. */
+typedef struct {
+    l2f_reward_weights init, target, factor;
+    double sigma_init, sigma_target, sigma_factor;
+    int64_t interval;
+} l2f_curriculum;
+
+typedef struct {
+    uint32_t abi_version;      /* must be L2F_ABI_VERSION */
+    uint32_t flags;            /* L2F_* feature flags */
+    int64_t num_envs;          /* N > 0 on this device */
+    uint64_t env_id_offset;    /* global id of local env 0 (sharding, Q20); offset + N <= 2^32 */
+    uint64_t seed;             /* Philox key */
+    int32_t action_history;    /* N_H in [0, 32] */
+    int32_t max_episode_steps; /* truncation cap (Q15); 0 = none */
+    double dt;                 /* integration step (s); 0.01 = 100 Hz */
+    l2f_params params;         /* nominal parameters */
+    double dr_lo, dr_hi;       /* DR factor range, each factor ~ U[dr_lo, dr_hi] (Q19) */
+    double init_pos, init_angle, init_vel, init_angvel; /* initial-state bounds (Q17) */
+    double init_rpm_lo, init_rpm_hi;
+    double dist_force, dist_torque;  /* disturbance bounds, component-wise uniform (Q18) */
+    double obs_sigma[4];       /* observation noise sigma for p, R, v, omega (Q8) */
+    double term_pos, term_vel, term_angvel; /* termination thresholds (Q14) */
+    l2f_curriculum curriculum;
+} l2f_config;
+
+/* Optional per-step outputs (device pointers; any may be NULL). */
+typedef struct {
+    float* obs_core;    /* [18][N]: noisy {p, R, v, omega} of the state after the step (or the
+                           reset state if the episode ended and auto-reset is on), Q11 */
+    float* obs_dense;   /* [N][18 + 4 N_H]: obs_core transposed + H, most recent first */
+    float* reward;      /* [N] */
+    uint8_t* flags;     /* [N] L2F_DONE_* bits */
+    float* final_state; /* [17][N]: s' before any auto-reset */
+} l2f_step_out;
+
+/* Actor MLP in_dim -> hidden -> hidden -> 4 (BASELINE configs[3]; Q21): ReLU hidden layers,
+ * tanh output; every weight and bias an IEEE fp16 bit pattern, row-major [out][in]; layer
+ * inputs are rounded to fp16, accumulation is FP32 on the tensor cores.
+ * in_dim must equal 18 + 4 N_H; hidden must be 64.  Device pointers. */
+typedef struct {
+    const uint16_t *W1, *b1, *W2, *b2, *W3, *b3;
+    int32_t in_dim, hidden;
+} l2f_policy;
+
+/* Borrowed device views into the env workspace (valid until l2f_destroy).  The caller may
+ * read or overwrite them between calls (checkpoint / resume / set_state).  q is not
+ * re-normalised on write (precondition ||q|| = 1). */
+typedef struct {
+    float* state;      /* [17][N] */
+    float* dist;       /* [6][N]  */
+    float* dr;         /* [5][N]  factors (1 when DR is off) */
+    float* hist;       /* [N_H][4][N] ring: slot (tau mod N_H) holds the action applied at step tau */
+    int32_t* ep_step;  /* [N] */
+    float* ep_return;  /* [N] */
+    uint64_t t;        /* global step counter: the next l2f_step is step t */
+    int64_t num_envs;
+    int32_t action_history;
+} l2f_state_view;
+
+/* ---- lifecycle ---------------------------------------------------------------------- */
+
+/* Bytes of device workspace an env with this config needs.  Validates the config:
+ * INVALID_ARGUMENT for N <= 0, N_H outside [0,32], dt <= 0, rpm_max <= rpm_min,
+ * T_m <= 0, mass/inertia <= 0, offset + N > 2^32, dr_lo <= 0 or dr_lo > dr_hi, or hover
+ * infeasible at the worst DR corner (4 f(rpm_max) <= m g). */
+L2F_API l2f_status l2f_workspace_size(const l2f_config* cfg, size_t* bytes);
+
+/* Creates an env over a caller-owned, 256-byte-aligned device workspace on the current
+ * CUDA device.  Copies cfg.  Does not touch the workspace: call l2f_reset before stepping. */
+L2F_API l2f_status l2f_create(const l2f_config* cfg, void* d_workspace, size_t bytes, l2f_env** out);
+
+/* Frees host-side resources (never the caller's workspace). */
+L2F_API l2f_status l2f_destroy(l2f_env* env);
+
+/* ---- stepping ----------------------------------------------------------------------- */
+
+/* Resets the envs where d_mask[i] != 0 (d_mask == NULL: all envs and the episode
+ * statistics), drawing initial state, disturbance, DR factors from Philox counter t
+ * (Q17-Q20), filling the history (Q10) and zeroing episode counters.
+ * Writes obs_core / obs_dense of the reset envs if requested (obs noise counter t). */
+L2F_API l2f_status l2f_reset(l2f_env* env, const uint8_t* d_mask, const l2f_step_out* out, void* stream);
+
+/* One environment step for all N envs.  d_actions: [4][N] in [-1,1] (clipped
+ * after exploration noise).  Then t += 1.  HBM-bound; one kernel launch. */
+L2F_API l2f_status l2f_step(l2f_env* env, const float* d_actions, const l2f_step_out* out, void* stream);
+
+/* Fused rollout of T >= 1 steps in one persistent launch, state in registers.
+ *  policy != NULL: actions from the actor MLP on the noisy observation (tcgen05 tensor
+ *                  cores; requires N_H % 4 == 0); d_actions must be NULL.
+ *  policy == NULL, d_actions != NULL: open loop, actions [T][4][N].
+ *  policy == NULL, d_actions == NULL: open loop, Philox random actions U(-1,1) (stream 6).
+ * d_trace: NULL or [T][K][32] floats for the K local env indices d_trace_ids[K] (device):
+ *   fields 0-16 pre-step state, 17-20 raw action, 21-24 applied action, 25 reward,
+ *   26 flags, 27 ep_step after the step, 28-31 zero.  Then t += T.
+ * With a policy the history ring is held in fp16 on chip, so afterwards it holds q16(a'). */
+L2F_API l2f_status l2f_rollout(l2f_env* env, const l2f_policy* policy, const float* d_actions,
+                       int32_t T, float* d_trace, const int64_t* d_trace_ids, int32_t K,
+                       void* stream);
+
+/* Reduces the episode statistics accumulated since the last reset of the accumulators into
+ * d_out[8] (FP64, fixed-order, deterministic).  reset_accumulators != 0 zeroes them. */
+L2F_API l2f_status l2f_episode_stats(l2f_env* env, double* d_out, int32_t reset_accumulators, void* stream);
+
+/* ---- host-buffer entry points (end-to-end; synchronise the stream before returning) --- */
+
+/* H2D of h_actions [4][N], l2f_step, D2H of the requested outputs (any may be NULL). */
+L2F_API l2f_status l2f_step_host(l2f_env* env, const float* h_actions, float* h_obs_core,
+                         float* h_reward, uint8_t* h_flags, void* stream);
+
+/* H2D of a host policy (fp16 bits) into the env's workspace, l2f_rollout(T), then
+ * l2f_episode_stats(reset_accumulators) D2H into h_stats[8] (may be NULL). */
+L2F_API l2f_status l2f_rollout_host(l2f_env* env, const l2f_policy* h_policy, int32_t T,
+                            double* h_stats, int32_t reset_accumulators, void* stream);
+
+/* ---- state access --------------------------------------------------------------------- */
+
+L2F_API l2f_status l2f_get_state(l2f_env* env, l2f_state_view* out);
+L2F_API l2f_status l2f_set_t(l2f_env* env, uint64_t t);
+
+/* Actor MLP forward on explicit observations (the same tcgen05 tile code as the rollout):
+ * d_obs [N][in_dim] fp32, d_act [N][4] fp32 (tanh output, before noise). */
+L2F_API l2f_status l2f_policy_forward(const l2f_policy* policy, const float* d_obs, float* d_act,
+                              int64_t n, void* stream);
+
+/* Diagnostics: writes our Philox4x32-10 output and curand_Philox4x32_10's for counters
+ * (i, t, i mod 7, i mod 5), key = seed, i < n, into d_ours[n][4] / d_curand[n][4] (uint32). */
+L2F_API l2f_status l2f_selftest_philox(int64_t n, uint64_t seed, uint32_t t, uint32_t* d_ours, uint32_t* d_curand,
+                                       void* stream);
+
+/* Number of kernels this library launched since load (diagnostics for the bench). */
+L2F_API uint64_t l2f_launch_count(void);
+
+L2F_API const char* l2f_last_error(void);
+L2F_API int32_t l2f_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* L2F_H */

@@ -155,7 +155,7 @@ def random_states(n: int, seed: int = 21, params: dict | None = None) -> dict:
     dist = np.concatenate([g.uniform(-0.0265, 0.0265, (3, n)), g.uniform(-1e-5, 1e-5, (3, n))])
     dr = g.uniform(0.8, 1.2, (5, n))
     hist = g.uniform(-1, 1, (32, 4, n))
-    ep_step = g.integers(0, 499, n).astype(np.int32)
+    ep_step = g.integers(0, 500, n).astype(np.int32)
     ep_return = g.uniform(-50, 50, n)
     return {"state": s, "dist": dist, "dr": dr, "hist": hist, "ep_step": ep_step,
             "ep_return": ep_return}

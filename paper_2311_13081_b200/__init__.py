@@ -1,0 +1,191 @@
+"""B200-native batched quadrotor environment of arXiv 2311.13081 ("Learning to Fly in Seconds").
+
+Thin Python binding over the C ABI of ``libl2f.so`` (include/l2f.h).  Argument marshalling
+only: every step of the method runs in the sm_100a kernels behind the ABI.  PyTorch provides
+device memory (the env workspace and I/O tensors) and streams.  There is no CPU fallback:
+importing this package without the built extension raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from .abi import (ABI_VERSION, DONE_DIVERGED, DONE_RESET, DONE_TERMINATED, DONE_TRUNCATED,  # noqa: F401
+                  OBS_CORE, STATE_DIM, STATS, STATS_LEN, TRACE_FIELDS, L2FError, lib, make_config)
+
+__all__ = ["Env", "Policy", "policy_forward", "lib", "L2FError", "launch_count"]
+
+
+def _stream(stream=None) -> C.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _check(st: int, what: str):
+    if st != 0:
+        raise L2FError(f"{what}: status {st}: {lib().l2f_last_error().decode()}")
+
+
+def launch_count() -> int:
+    return int(lib().l2f_launch_count())
+
+
+class Policy:
+    """Actor MLP parameters as fp16 bit patterns (uint16 tensors), row-major [out][in]."""
+
+    def __init__(self, weights: dict, device="cuda"):
+        self.t = {k: torch.as_tensor(weights[k]).view(torch.int16).to(device).contiguous()
+                  for k in ("W1", "b1", "W2", "b2", "W3", "b3")}
+        self.in_dim = int(self.t["W1"].shape[1])
+        self.hidden = int(self.t["W1"].shape[0])
+        self.s = lib().make_policy(*(self.t[k].data_ptr() for k in ("W1", "b1", "W2", "b2", "W3", "b3")),
+                                   self.in_dim, self.hidden)
+
+
+class HostPolicy:
+    """Same, in pinned host memory (for l2f_rollout_host)."""
+
+    def __init__(self, weights: dict):
+        self.t = {k: torch.as_tensor(weights[k]).view(torch.int16).contiguous().pin_memory()
+                  for k in ("W1", "b1", "W2", "b2", "W3", "b3")}
+        self.in_dim = int(self.t["W1"].shape[1])
+        self.hidden = int(self.t["W1"].shape[0])
+        self.s = lib().make_policy(*(self.t[k].data_ptr() for k in ("W1", "b1", "W2", "b2", "W3", "b3")),
+                                   self.in_dim, self.hidden)
+
+
+def policy_forward(policy: Policy, obs: torch.Tensor, stream=None) -> torch.Tensor:
+    """obs [n][in_dim] fp32 (cuda) -> tanh actions [n][4] (before exploration noise)."""
+    assert obs.is_cuda and obs.dtype == torch.float32 and obs.is_contiguous()
+    out = torch.empty(obs.shape[0], 4, device=obs.device, dtype=torch.float32)
+    _check(lib().l2f_policy_forward(C.byref(policy.s), _ptr(obs), _ptr(out), obs.shape[0], _stream(stream)),
+           "l2f_policy_forward")
+    return out
+
+
+class Env:
+    """N independent quadrotor environments resident in HBM (one workspace tensor)."""
+
+    def __init__(self, cfg: dict, num_envs: int, env_id_offset: int = 0, device="cuda"):
+        L = lib()
+        self.cfg_dict = cfg
+        self.n = int(num_envs)
+        self.n_hist = int(cfg["n_hist"])
+        self.device = torch.device(device)
+        self.cfg = make_config(cfg, self.n, env_id_offset)
+        nbytes = C.c_size_t()
+        _check(L.l2f_workspace_size(C.byref(self.cfg), C.byref(nbytes)), "l2f_workspace_size")
+        self.ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
+        self.h = C.c_void_p()
+        _check(L.l2f_create(C.byref(self.cfg), _ptr(self.ws), nbytes, C.byref(self.h)), "l2f_create")
+        self._views()
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().l2f_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def _views(self):
+        v = lib().StateView()
+        _check(lib().l2f_get_state(self.h, C.byref(v)), "l2f_get_state")
+        base = self.ws.data_ptr()
+        n, nh = self.n, max(self.n_hist, 1)
+
+        def view(ptr, count, dtype, shape):
+            off = int(ptr) - base
+            esz = torch.empty(0, dtype=dtype).element_size()
+            return self.ws[off: off + count * esz].view(dtype).view(*shape)
+
+        self.state = view(v.state, 17 * n, torch.float32, (17, n))
+        self.dist = view(v.dist, 6 * n, torch.float32, (6, n))
+        self.dr = view(v.dr, 5 * n, torch.float32, (5, n))
+        self.hist = view(v.hist, nh * 4 * n, torch.float32, (nh, 4, n))
+        self.ep_step = view(v.ep_step, n, torch.int32, (n,))
+        self.ep_return = view(v.ep_return, n, torch.float32, (n,))
+
+    # -------------------------------------------------------------------------------
+    @property
+    def t(self) -> int:
+        v = lib().StateView()
+        _check(lib().l2f_get_state(self.h, C.byref(v)), "l2f_get_state")
+        return int(v.t)
+
+    @t.setter
+    def t(self, value: int):
+        _check(lib().l2f_set_t(self.h, int(value)), "l2f_set_t")
+
+    def make_out(self, obs_core=True, reward=True, flags=True, final_state=False, obs_dense=False):
+        d = self.device
+        return {
+            "obs_core": torch.empty(18, self.n, device=d) if obs_core else None,
+            "reward": torch.empty(self.n, device=d) if reward else None,
+            "flags": torch.empty(self.n, device=d, dtype=torch.uint8) if flags else None,
+            "final_state": torch.empty(17, self.n, device=d) if final_state else None,
+            "obs_dense": torch.empty(self.n, 18 + 4 * self.n_hist, device=d) if obs_dense else None,
+        }
+
+    def _out_struct(self, out: dict | None):
+        if out is None:
+            return None
+        o = lib().StepOut()
+        for k in ("obs_core", "obs_dense", "reward", "flags", "final_state"):
+            t = out.get(k)
+            if t is not None:
+                assert t.is_cuda and t.is_contiguous()
+                setattr(o, k, t.data_ptr())
+        return C.byref(o)
+
+    def reset(self, mask: torch.Tensor | None = None, out: dict | None = None, stream=None):
+        if mask is not None:
+            assert mask.dtype == torch.uint8 and mask.is_cuda and mask.numel() == self.n
+        _check(lib().l2f_reset(self.h, _ptr(mask), self._out_struct(out), _stream(stream)), "l2f_reset")
+        return out
+
+    def step(self, actions: torch.Tensor, out: dict | None = None, stream=None):
+        assert actions.is_cuda and actions.dtype == torch.float32 and actions.is_contiguous()
+        assert actions.shape == (4, self.n)
+        _check(lib().l2f_step(self.h, _ptr(actions), self._out_struct(out), _stream(stream)), "l2f_step")
+        return out
+
+    def rollout(self, T: int, policy: Policy | None = None, actions: torch.Tensor | None = None,
+                trace_ids: torch.Tensor | None = None, stream=None):
+        trace = None
+        K = 0
+        if actions is not None:
+            assert actions.is_cuda and actions.dtype == torch.float32 and actions.shape == (T, 4, self.n)
+            actions = actions.contiguous()
+        if trace_ids is not None:
+            trace_ids = trace_ids.to(device=self.device, dtype=torch.int64).contiguous()
+            K = int(trace_ids.numel())
+            trace = torch.zeros(T, K, TRACE_FIELDS, device=self.device)
+        _check(lib().l2f_rollout(self.h, C.byref(policy.s) if policy is not None else None, _ptr(actions), int(T),
+                                 _ptr(trace), _ptr(trace_ids), K, _stream(stream)), "l2f_rollout")
+        return trace
+
+    def episode_stats(self, reset: bool = False, stream=None) -> torch.Tensor:
+        out = torch.empty(STATS_LEN, dtype=torch.float64, device=self.device)
+        _check(lib().l2f_episode_stats(self.h, _ptr(out), int(reset), _stream(stream)), "l2f_episode_stats")
+        return out
+
+    # host-buffer entry points (synchronous) ----------------------------------------
+    def step_host(self, h_actions: torch.Tensor, h_obs=None, h_reward=None, h_flags=None, stream=None):
+        assert not h_actions.is_cuda and h_actions.dtype == torch.float32 and h_actions.is_contiguous()
+        _check(lib().l2f_step_host(self.h, _ptr(h_actions), _ptr(h_obs), _ptr(h_reward), _ptr(h_flags),
+                                   _stream(stream)), "l2f_step_host")
+
+    def rollout_host(self, policy: HostPolicy, T: int, h_stats: torch.Tensor | None = None, reset_stats=True,
+                     stream=None):
+        if h_stats is not None:
+            assert h_stats.dtype == torch.float64 and not h_stats.is_cuda
+        _check(lib().l2f_rollout_host(self.h, C.byref(policy.s), int(T), _ptr(h_stats), int(reset_stats),
+                                      _stream(stream)), "l2f_rollout_host")
+        return h_stats

@@ -1,0 +1,528 @@
+// l2f_device.cuh -- device-side building blocks of the batched quadrotor env step
+// (arXiv 2311.13081).  One env per thread; every function here operates on registers.
+// Shared by the single-step kernel, the open-loop rollout and the tcgen05 MLP rollout so
+// that T x l2f_step and l2f_rollout(T) execute the same arithmetic.
+//
+// Citations: P:n = /root/reference/PAPER.md line n; Qn = DESIGN.md section 3 readings.
+// This file is independent of oracle/ (no shared code, tables or constants).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace l2f {
+
+constexpr int kStateDim = 17;
+constexpr int kObsCore = 18;
+constexpr int kMaxHist = 32;
+constexpr int kMaxStages = 8;
+constexpr int kStatsLen = 8;
+constexpr int kTraceFields = 32;
+
+enum : uint32_t {
+    F_OBS_NOISE = 1u << 0,
+    F_ACTION_NOISE = 1u << 1,
+    F_TERMINATION = 1u << 2,
+    F_AUTO_RESET = 1u << 3,
+    F_DISTURBANCE = 1u << 4,
+    F_DOMAIN_RAND = 1u << 5,
+};
+enum : uint32_t { D_TERM = 1, D_TRUNC = 2, D_DIV = 4, D_RESET = 8 };
+enum : uint32_t { S_ACT = 1, S_OBS = 2, S_RESET = 3, S_DIST = 4, S_DR = 5, S_RAND_ACT = 6 };
+
+// Reward weights + exploration sigma of one curriculum stage, fp32.
+struct StageW {
+    float C_rp, C_rq, C_rv, C_rw, C_ra, C_rab[4], C_rs, sigma_a;
+};
+
+// Launch-uniform parameters, passed by value (constant bank) to every kernel.
+struct DevParams {
+    uint32_t key0, key1;       // Philox key = seed (Q20)
+    uint32_t flags;
+    int32_t n_hist;
+    int32_t max_ep;
+    uint32_t id_offset;        // global env id of local env 0
+    int64_t n;                 // envs
+    uint32_t t0;               // step counter at launch
+    // integration
+    float dt, half_dt, dt_6;
+    // nominal parameters; DR factors scale mass, J, thrust coefficients (Q19)
+    float mass, J[3], c[3], ctau, inv_tm, rpm_min, rpm_max, gravity, rpm_half_span, inv_rpm_span2;
+    float rx[4], ry[4], spin[4];
+    // reset distribution (Q17-Q19)
+    float init_pos, init_angle, init_vel, init_angvel, init_rpm_lo, init_rpm_hi;
+    float dist_force, dist_torque, dr_lo, dr_hi;
+    // observation noise (Q8), termination (Q14)
+    float obs_sigma[4];
+    float term_pos, term_vel2, term_angvel2;
+    // curriculum slice covering [t0, t0 + T): stage of step t = stage_base + floor(t/interval)
+    int64_t interval;          // 0 = single stage
+    int64_t stage_first;       // global stage index of stage[0]
+    int32_t n_stages;
+    StageW stage[kMaxStages];
+};
+
+// Workspace views (SoA, [C][N]).
+struct DevBufs {
+    float* state;     // [17][N]
+    float* dist;      // [6][N]
+    float* dr;        // [5][N]
+    float* hist;      // [N_H][4][N]
+    int32_t* ep_step; // [N]
+    float* ep_return; // [N]
+    double* slots;    // [n_slots][8] per-block statistics partials
+    int32_t n_slots;
+};
+
+// Registers of one env.
+struct EnvReg {
+    float s[kStateDim];
+    float dist[6];
+    float dr[5];
+    int32_t ep_step;
+    float ep_return;
+};
+
+// ---------------------------------------------------------------------------------------
+// Philox4x32-10 (Random123), counter = (env id, t, stream, block), key = seed (Q20).
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                        uint32_t k0, uint32_t k1)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        c0 = hi1 ^ c1 ^ k0;
+        c2 = hi0 ^ c3 ^ k1;
+        c1 = lo1;
+        c3 = lo0;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
+__device__ __forceinline__ uint4 draw(const DevParams& P, uint32_t gid, uint32_t t,
+                                      uint32_t stream, uint32_t block)
+{
+    return philox(gid, t, stream, block, P.key0, P.key1);
+}
+
+// u = (2 (x >> 9) + 1) 2^-24, exact in fp32 (Q20)
+__device__ __forceinline__ float unif(uint32_t x)
+{
+    return __uint2float_rn(((x >> 9) << 1) | 1u) * 5.9604644775390625e-08f;
+}
+
+// ln(u) for u in (0,1): log1p series near 1 (where MUFU.LG2's absolute error would swamp
+// the tiny result), MUFU.LG2 elsewhere (relative error <= ~3e-6 there).
+__device__ __forceinline__ float ln_unit(float u)
+{
+    const float x = u - 1.0f;  // exact for u >= 1/2
+    float p = fmaf(x, -1.0f / 6.0f, 0.2f);
+    p = fmaf(x, p, -0.25f);
+    p = fmaf(x, p, 1.0f / 3.0f);
+    p = fmaf(x, p, -0.5f);
+    p = fmaf(x, p, 1.0f);
+    const float series = x * p;
+    const float l = __log2f(u) * 0.69314718055994531f;
+    return (x > -0.0625f) ? series : l;
+}
+
+// Box-Muller (Q20): r = sqrt(-2 ln u1), theta = 2 pi u2.
+__device__ __forceinline__ void box_muller(uint32_t xa, uint32_t xb, float& z0, float& z1)
+{
+    const float u1 = unif(xa), u2 = unif(xb);
+    const float y = -2.0f * ln_unit(u1);
+    const float r = y * rsqrtf(y);
+    float sn, cs;
+    __sincosf(6.28318530717958648f * u2, &sn, &cs);
+    z0 = r * cs;
+    z1 = r * sn;
+}
+
+__device__ __forceinline__ const StageW& stage_of(const DevParams& P, uint32_t t)
+{
+    int k = 0;
+    if (P.interval > 0) {
+        long long g = (long long)(t / (uint64_t)P.interval) - P.stage_first;
+        k = (int)min(max(g, 0ll), (long long)(P.n_stages - 1));
+    }
+    return P.stage[k];
+}
+
+// ---------------------------------------------------------------------------------------
+// Dynamics: per-step constants of one env, then f(s).
+// ---------------------------------------------------------------------------------------
+struct Phys {
+    float c0, c1, c2;       // thrust coefficients x DR thrust scale
+    float inv_m;
+    float Jx, Jy, Jz, iJx, iJy, iJz;
+    float u_tm[4];          // setpoint / T_m
+};
+
+__device__ __forceinline__ void make_phys(const DevParams& P, const EnvReg& e, const float u[4],
+                                          bool dr_on, Phys& ph)
+{
+    if (dr_on) {
+        ph.c0 = P.c[0] * e.dr[4];
+        ph.c1 = P.c[1] * e.dr[4];
+        ph.c2 = P.c[2] * e.dr[4];
+        ph.inv_m = __fdividef(1.0f, P.mass * e.dr[0]);
+        ph.Jx = P.J[0] * e.dr[1];
+        ph.Jy = P.J[1] * e.dr[2];
+        ph.Jz = P.J[2] * e.dr[3];
+    } else {
+        ph.c0 = P.c[0];
+        ph.c1 = P.c[1];
+        ph.c2 = P.c[2];
+        ph.inv_m = __fdividef(1.0f, P.mass);
+        ph.Jx = P.J[0];
+        ph.Jy = P.J[1];
+        ph.Jz = P.J[2];
+    }
+    ph.iJx = __fdividef(1.0f, ph.Jx);
+    ph.iJy = __fdividef(1.0f, ph.Jy);
+    ph.iJz = __fdividef(1.0f, ph.Jz);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ph.u_tm[i] = u[i] * P.inv_tm;
+}
+
+// ds = f(s): p' = v; q' = 1/2 q (x) (0,w); v' = (R e_z T + f_r)/m - g e_z;
+// w' = J^-1 (tau - w x J w); w_m' = (u - w_m)/T_m.
+__device__ __forceinline__ void deriv(const DevParams& P, const Phys& ph, const float* d,
+                                      const float* s, float* ds)
+{
+    float f[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) f[i] = fmaf(fmaf(ph.c2, s[13 + i], ph.c1), s[13 + i], ph.c0);
+    const float T = (f[0] + f[1]) + (f[2] + f[3]);
+    float tx = d[3], ty = d[4], tz = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        tx = fmaf(P.ry[i], f[i], tx);
+        ty = fmaf(-P.rx[i], f[i], ty);
+        tz = fmaf(P.spin[i], f[i], tz);
+    }
+    tz = fmaf(P.ctau, tz, d[5]);
+    const float qw = s[3], qx = s[4], qy = s[5], qz = s[6];
+    const float wx = s[10], wy = s[11], wz = s[12];
+    ds[0] = s[7];
+    ds[1] = s[8];
+    ds[2] = s[9];
+    const float hx = 0.5f * wx, hy = 0.5f * wy, hz = 0.5f * wz;
+    ds[3] = -(qx * hx + qy * hy + qz * hz);
+    ds[4] = qw * hx + qy * hz - qz * hy;
+    ds[5] = qw * hy - qx * hz + qz * hx;
+    ds[6] = qw * hz + qx * hy - qy * hx;
+    // third column of R(q): body z-axis in world
+    const float r02 = 2.0f * (qx * qz + qw * qy);
+    const float r12 = 2.0f * (qy * qz - qw * qx);
+    const float r22 = 1.0f - 2.0f * (qx * qx + qy * qy);
+    ds[7] = fmaf(r02, T, d[0]) * ph.inv_m;
+    ds[8] = fmaf(r12, T, d[1]) * ph.inv_m;
+    ds[9] = fmaf(fmaf(r22, T, d[2]), ph.inv_m, -P.gravity);
+    // Euler: J w' = tau - w x (J w)
+    const float cx = (ph.Jz - ph.Jy) * (wy * wz);
+    const float cy = (ph.Jx - ph.Jz) * (wz * wx);
+    const float cz = (ph.Jy - ph.Jx) * (wx * wy);
+    ds[10] = (tx - cx) * ph.iJx;
+    ds[11] = (ty - cy) * ph.iJy;
+    ds[12] = (tz - cz) * ph.iJz;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ds[13 + i] = fmaf(-s[13 + i], P.inv_tm, ph.u_tm[i]);
+}
+
+// Classical RK4 with zero-order-hold setpoints (Q1), then q renormalisation and rotor-speed
+// clamp (Q5).  Returns true if the result is non-finite.
+__device__ __forceinline__ bool rk4_step(const DevParams& P, const Phys& ph, const float* d, float* s)
+{
+    float acc[kStateDim], tmp[kStateDim], k[kStateDim];
+    deriv(P, ph, d, s, k);
+#pragma unroll
+    for (int i = 0; i < kStateDim; ++i) {
+        acc[i] = k[i];
+        tmp[i] = fmaf(P.half_dt, k[i], s[i]);
+    }
+    deriv(P, ph, d, tmp, k);
+#pragma unroll
+    for (int i = 0; i < kStateDim; ++i) {
+        acc[i] = fmaf(2.0f, k[i], acc[i]);
+        tmp[i] = fmaf(P.half_dt, k[i], s[i]);
+    }
+    deriv(P, ph, d, tmp, k);
+#pragma unroll
+    for (int i = 0; i < kStateDim; ++i) {
+        acc[i] = fmaf(2.0f, k[i], acc[i]);
+        tmp[i] = fmaf(P.dt, k[i], s[i]);
+    }
+    deriv(P, ph, d, tmp, k);
+#pragma unroll
+    for (int i = 0; i < kStateDim; ++i) s[i] = fmaf(P.dt_6, acc[i] + k[i], s[i]);
+    const float n2 = (s[3] * s[3] + s[4] * s[4]) + (s[5] * s[5] + s[6] * s[6]);
+    const float inv = rsqrtf(n2);
+#pragma unroll
+    for (int i = 3; i < 7; ++i) s[i] *= inv;
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < kStateDim; ++i) bad |= !isfinite(s[i]);
+#pragma unroll
+    for (int i = 13; i < 17; ++i) s[i] = fminf(fmaxf(s[i], P.rpm_min), P.rpm_max);
+    return bad;
+}
+
+// ---------------------------------------------------------------------------------------
+// Result of one transition (before any reset).
+// ---------------------------------------------------------------------------------------
+struct Trans {
+    float a[4];      // applied action a'
+    float reward;
+    uint32_t flags;  // D_TERM | D_TRUNC | D_DIV
+    int32_t len;     // episode length if it ended
+    float ret;       // episode return if it ended
+};
+
+// One env transition s_t -> s_{t+1}: exploration noise + clip (Q7),
+// action map, RK4 dynamics, reward on s' (Q12), termination (Q14),
+// truncation (Q15).  Episode counters are advanced; the caller handles history and reset.
+__device__ __forceinline__ void transition(const DevParams& P, EnvReg& e, uint32_t gid, uint32_t t,
+                                           const float a_in[4], Trans& o)
+{
+    const StageW& W = stage_of(P, t);
+    float z[4] = {0.f, 0.f, 0.f, 0.f};
+    const bool act_noise = (P.flags & F_ACTION_NOISE) != 0;
+    if (act_noise) {
+        const uint4 x = draw(P, gid, t, S_ACT, 0);
+        box_muller(x.x, x.y, z[0], z[1]);
+        box_muller(x.z, x.w, z[2], z[3]);
+    }
+    float u[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float v = act_noise ? fmaf(W.sigma_a, z[i], a_in[i]) : a_in[i];
+        o.a[i] = fminf(fmaxf(v, -1.0f), 1.0f);
+        u[i] = fmaf(o.a[i] + 1.0f, P.rpm_half_span, P.rpm_min);
+    }
+    Phys ph;
+    make_phys(P, e, u, (P.flags & F_DOMAIN_RAND) != 0, ph);
+    const bool div = rk4_step(P, ph, e.dist, e.s);
+
+    const float* s = e.s;
+    const float pp = s[0] * s[0] + s[1] * s[1] + s[2] * s[2];
+    const float vv = s[7] * s[7] + s[8] * s[8] + s[9] * s[9];
+    const float ww = s[10] * s[10] + s[11] * s[11] + s[12] * s[12];
+    float aa = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float d = o.a[i] - W.C_rab[i];
+        aa = fmaf(d, d, aa);
+    }
+    float r = W.C_rs;
+    r = fmaf(-W.C_rp, pp, r);
+    r = fmaf(-W.C_rq, fmaf(-s[3], s[3], 1.0f), r);
+    r = fmaf(-W.C_rv, vv, r);
+    r = fmaf(-W.C_rw, ww, r);
+    r = fmaf(-W.C_ra, aa, r);
+    if (div) r = 0.0f;  // Q26
+    bool term = div;
+    if (P.flags & F_TERMINATION) {
+        const float pinf = fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2])));
+        term |= (pinf > P.term_pos) | (vv > P.term_vel2) | (ww > P.term_angvel2);
+    }
+    e.ep_step += 1;
+    e.ep_return += r;
+    const bool trunc = !term && P.max_ep > 0 && e.ep_step >= P.max_ep;
+    o.reward = r;
+    o.flags = (term ? D_TERM : 0u) | (trunc ? D_TRUNC : 0u) | (div ? D_DIV : 0u);
+    o.len = e.ep_step;
+    o.ret = e.ep_return;
+}
+
+__device__ __forceinline__ float uab(float a, float b, uint32_t x) { return fmaf(b - a, unif(x), a); }
+
+// Reset of one env from Philox counter `ctr` (Q17-Q19): state, disturbance,
+// DR factors, episode counters.  Returns the history fill value per rotor (Q10) in hfill.
+__device__ __forceinline__ void reset_env(const DevParams& P, EnvReg& e, uint32_t gid, uint32_t ctr,
+                                          float hfill[4])
+{
+    const uint4 b0 = draw(P, gid, ctr, S_RESET, 0);
+    const uint4 b1 = draw(P, gid, ctr, S_RESET, 1);
+    const uint4 b2 = draw(P, gid, ctr, S_RESET, 2);
+    const uint4 b3 = draw(P, gid, ctr, S_RESET, 3);
+    e.s[0] = uab(-P.init_pos, P.init_pos, b0.x);
+    e.s[1] = uab(-P.init_pos, P.init_pos, b0.y);
+    e.s[2] = uab(-P.init_pos, P.init_pos, b0.z);
+    const float cz = uab(-1.0f, 1.0f, b0.w);
+    const float phi = 6.28318530717958648f * unif(b1.x);
+    const float th = P.init_angle * unif(b1.y);
+    const float sxy = sqrtf(fmaxf(fmaf(-cz, cz, 1.0f), 0.0f));
+    float sp, cp, sh, ch;
+    __sincosf(phi, &sp, &cp);
+    __sincosf(0.5f * th, &sh, &ch);
+    e.s[3] = ch;
+    e.s[4] = sh * (sxy * cp);
+    e.s[5] = sh * (sxy * sp);
+    e.s[6] = sh * cz;
+    e.s[7] = uab(-P.init_vel, P.init_vel, b1.z);
+    e.s[8] = uab(-P.init_vel, P.init_vel, b1.w);
+    e.s[9] = uab(-P.init_vel, P.init_vel, b2.x);
+    e.s[10] = uab(-P.init_angvel, P.init_angvel, b2.y);
+    e.s[11] = uab(-P.init_angvel, P.init_angvel, b2.z);
+    e.s[12] = uab(-P.init_angvel, P.init_angvel, b2.w);
+    e.s[13] = uab(P.init_rpm_lo, P.init_rpm_hi, b3.x);
+    e.s[14] = uab(P.init_rpm_lo, P.init_rpm_hi, b3.y);
+    e.s[15] = uab(P.init_rpm_lo, P.init_rpm_hi, b3.z);
+    e.s[16] = uab(P.init_rpm_lo, P.init_rpm_hi, b3.w);
+    if (P.flags & F_DISTURBANCE) {
+        const uint4 d0 = draw(P, gid, ctr, S_DIST, 0);
+        const uint4 d1 = draw(P, gid, ctr, S_DIST, 1);
+        e.dist[0] = uab(-P.dist_force, P.dist_force, d0.x);
+        e.dist[1] = uab(-P.dist_force, P.dist_force, d0.y);
+        e.dist[2] = uab(-P.dist_force, P.dist_force, d0.z);
+        e.dist[3] = uab(-P.dist_torque, P.dist_torque, d0.w);
+        e.dist[4] = uab(-P.dist_torque, P.dist_torque, d1.x);
+        e.dist[5] = uab(-P.dist_torque, P.dist_torque, d1.y);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 6; ++j) e.dist[j] = 0.0f;
+    }
+    if (P.flags & F_DOMAIN_RAND) {
+        const uint4 r0 = draw(P, gid, ctr, S_DR, 0);
+        const uint4 r1 = draw(P, gid, ctr, S_DR, 1);
+        e.dr[0] = uab(P.dr_lo, P.dr_hi, r0.x);
+        e.dr[1] = uab(P.dr_lo, P.dr_hi, r0.y);
+        e.dr[2] = uab(P.dr_lo, P.dr_hi, r0.z);
+        e.dr[3] = uab(P.dr_lo, P.dr_hi, r0.w);
+        e.dr[4] = uab(P.dr_lo, P.dr_hi, r1.x);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 5; ++j) e.dr[j] = 1.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) hfill[i] = fmaf(e.s[13 + i] - P.rpm_min, P.inv_rpm_span2, -1.0f);
+    e.ep_step = 0;
+    e.ep_return = 0.0f;
+}
+
+// Noisy core observation {p, R(q) row-major, v, w} (Q8); obs-noise normal i is
+// normal (i mod 4) of Philox block floor(i/4) of stream OBS at counter t (Q20).
+__device__ __forceinline__ void observe_core(const DevParams& P, const float* s, uint32_t gid,
+                                             uint32_t t, float o[kObsCore])
+{
+    const float qw = s[3], qx = s[4], qy = s[5], qz = s[6];
+    o[0] = s[0];
+    o[1] = s[1];
+    o[2] = s[2];
+    o[3] = 1.0f - 2.0f * (qy * qy + qz * qz);
+    o[4] = 2.0f * (qx * qy - qw * qz);
+    o[5] = 2.0f * (qx * qz + qw * qy);
+    o[6] = 2.0f * (qx * qy + qw * qz);
+    o[7] = 1.0f - 2.0f * (qx * qx + qz * qz);
+    o[8] = 2.0f * (qy * qz - qw * qx);
+    o[9] = 2.0f * (qx * qz - qw * qy);
+    o[10] = 2.0f * (qy * qz + qw * qx);
+    o[11] = 1.0f - 2.0f * (qx * qx + qy * qy);
+    o[12] = s[7];
+    o[13] = s[8];
+    o[14] = s[9];
+    o[15] = s[10];
+    o[16] = s[11];
+    o[17] = s[12];
+    if (P.flags & F_OBS_NOISE) {
+        float z[20];
+#pragma unroll
+        for (int b = 0; b < 5; ++b) {
+            const uint4 x = draw(P, gid, t, S_OBS, (uint32_t)b);
+            box_muller(x.x, x.y, z[4 * b], z[4 * b + 1]);
+            if (b < 4) box_muller(x.z, x.w, z[4 * b + 2], z[4 * b + 3]);
+        }
+#pragma unroll
+        for (int i = 0; i < kObsCore; ++i) {
+            const int g = i < 3 ? 0 : (i < 12 ? 1 : (i < 15 ? 2 : 3));
+            o[i] = fmaf(P.obs_sigma[g], z[i], o[i]);
+        }
+    }
+}
+
+// Open-loop random action (stream RAND_ACT): a_i = -1 + 2 u_i.
+__device__ __forceinline__ void random_action(const DevParams& P, uint32_t gid, uint32_t t, float a[4])
+{
+    const uint4 x = draw(P, gid, t, S_RAND_ACT, 0);
+    a[0] = uab(-1.0f, 1.0f, x.x);
+    a[1] = uab(-1.0f, 1.0f, x.y);
+    a[2] = uab(-1.0f, 1.0f, x.z);
+    a[3] = uab(-1.0f, 1.0f, x.w);
+}
+
+// ---------------------------------------------------------------------------------------
+// Episode statistics: per-thread accumulation -> warp (REDUX / shuffles) -> block partial
+// in a fixed order -> the block's slot (deterministic for a fixed launch sequence).
+// ---------------------------------------------------------------------------------------
+struct StatAcc {
+    int32_t ep, term, trunc, div, len;
+    double ret, ret2;
+};
+
+__device__ __forceinline__ void stat_zero(StatAcc& a)
+{
+    a.ep = a.term = a.trunc = a.div = a.len = 0;
+    a.ret = a.ret2 = 0.0;
+}
+
+__device__ __forceinline__ void stat_episode(StatAcc& a, const Trans& o)
+{
+    a.ep += 1;
+    a.term += (o.flags & D_TERM) ? 1 : 0;
+    a.trunc += (o.flags & D_TRUNC) ? 1 : 0;
+    a.div += (o.flags & D_DIV) ? 1 : 0;
+    a.len += o.len;
+    const double r = (double)o.ret;
+    a.ret += r;
+    a.ret2 += r * r;
+}
+
+// Warp-reduce `a` and write lane 0's result into smem[warp][8] (doubles); returns nothing.
+// All 32 lanes must call it.
+__device__ __forceinline__ void stat_warp_to_smem(const StatAcc& a, double* smem_warp_row)
+{
+    const unsigned m = 0xffffffffu;
+    const int ep = __reduce_add_sync(m, a.ep);
+    const int term = __reduce_add_sync(m, a.term);
+    const int trunc = __reduce_add_sync(m, a.trunc);
+    const int dv = __reduce_add_sync(m, a.div);
+    const int len = __reduce_add_sync(m, a.len);
+    double r = a.ret, r2 = a.ret2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        r += __shfl_xor_sync(m, r, o);
+        r2 += __shfl_xor_sync(m, r2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        smem_warp_row[0] = ep;
+        smem_warp_row[1] = term;
+        smem_warp_row[2] = trunc;
+        smem_warp_row[3] = dv;
+        smem_warp_row[4] = len;
+        smem_warp_row[5] = r;
+        smem_warp_row[6] = r2;
+        smem_warp_row[7] = 0.0;
+    }
+}
+
+// Fixed-order sum of nw warp rows into slot[0..6] plus `steps` into slot[7].  Call after a
+// barrier that makes the warp rows visible; threads 0..7 participate.
+__device__ __forceinline__ void stat_rows_to_slot(const double* smem, int nw, double steps, double* slot)
+{
+    if (threadIdx.x < kStatsLen) {
+        double x = 0.0;
+        if (threadIdx.x < 7)
+            for (int w = 0; w < nw; ++w) x += smem[w * kStatsLen + threadIdx.x];
+        else
+            x = steps;
+        slot[threadIdx.x] += x;
+    }
+}
+
+}  // namespace l2f

@@ -1,0 +1,42 @@
+// l2f_internal.h -- host-side declarations shared by the ABI and the kernel translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "l2f_device.cuh"
+
+namespace l2f {
+
+constexpr int kStepBlock = 256;
+constexpr int kRolloutBlock = 128;
+
+struct StepOutDev {
+    float* obs_core;
+    float* obs_dense;
+    float* reward;
+    uint8_t* flags;
+    float* final_state;
+};
+
+// Actor MLP parameters on the device (fp16 bits, row-major [out][in]).
+struct PolicyDev {
+    const uint16_t *W1, *b1, *W2, *b2, *W3, *b3;
+    int32_t in_dim, hidden;
+};
+
+cudaError_t launch_step(const DevParams& P, const DevBufs& B, const float* act, const StepOutDev& O,
+                        cudaStream_t s);
+cudaError_t launch_reset(const DevParams& P, const DevBufs& B, const uint8_t* mask, const StepOutDev& O,
+                         cudaStream_t s);
+cudaError_t launch_rollout_open(const DevParams& P, const DevBufs& B, const float* act, int32_t T, float* trace,
+                                const int64_t* trace_ids, int32_t K, cudaStream_t s);
+cudaError_t launch_philox_selftest(int64_t n, uint64_t seed, uint32_t t, uint32_t* ours, uint32_t* ref,
+                                   cudaStream_t s);
+cudaError_t launch_stats_finalize(double* slots, int32_t n_slots, double* out, int32_t reset, cudaStream_t s);
+
+// tcgen05 actor-MLP rollout (l2f_mlp.cu).  Returns cudaErrorNotSupported for unsupported shapes.
+int mlp_rollout_grid(int64_t n);
+cudaError_t launch_rollout_mlp(const DevParams& P, const DevBufs& B, const PolicyDev& W, int32_t T, float* trace,
+                               const int64_t* trace_ids, int32_t K, cudaStream_t s);
+cudaError_t launch_policy_forward(const PolicyDev& W, const float* obs, float* act, int64_t n, cudaStream_t s);
+
+}  // namespace l2f

@@ -1,0 +1,355 @@
+// l2f_kernels.cu -- single-step, reset, open-loop rollout and statistics kernels (sm_100a).
+//
+// Data layout: structure-of-arrays [C][N] fp32 in HBM, one env per
+// thread, so every component load/store of a warp is one fully-coalesced 128-byte line.
+// Step kernel bytes per env-step (algorithmic): reads state 68 + action 16 +
+// disturbance 24 + counters 8 (+ DR 20), writes state 68 + counters 8 + history slot 16 +
+// obs_core 72 + reward 4 + flags 1.
+#include <curand_philox4x32_x.h>
+
+#include "l2f_device.cuh"
+#include "l2f_internal.h"
+
+namespace l2f {
+
+__device__ __forceinline__ void load_env(const DevParams& P, const DevBufs& B, int64_t i, EnvReg& e)
+{
+    const int64_t N = P.n;
+#pragma unroll
+    for (int c = 0; c < kStateDim; ++c) e.s[c] = B.state[c * N + i];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) e.dist[c] = B.dist[c * N + i];
+    if (P.flags & F_DOMAIN_RAND) {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) e.dr[c] = B.dr[c * N + i];
+    } else {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) e.dr[c] = 1.0f;
+    }
+    e.ep_step = B.ep_step[i];
+    e.ep_return = B.ep_return[i];
+}
+
+__device__ __forceinline__ void store_state(const DevParams& P, const DevBufs& B, int64_t i, const EnvReg& e)
+{
+    const int64_t N = P.n;
+#pragma unroll
+    for (int c = 0; c < kStateDim; ++c) B.state[c * N + i] = e.s[c];
+    B.ep_step[i] = e.ep_step;
+    B.ep_return[i] = e.ep_return;
+}
+
+// Written only when an episode starts (reset): disturbance + DR factors.
+__device__ __forceinline__ void store_episode_consts(const DevParams& P, const DevBufs& B, int64_t i,
+                                                     const EnvReg& e)
+{
+    const int64_t N = P.n;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) B.dist[c * N + i] = e.dist[c];
+    if (P.flags & F_DOMAIN_RAND) {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) B.dr[c * N + i] = e.dr[c];
+    }
+}
+
+__device__ __forceinline__ void hist_fill(const DevParams& P, const DevBufs& B, int64_t i, const float h[4])
+{
+    const int64_t N = P.n;
+    for (int k = 0; k < P.n_hist; ++k)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) B.hist[((int64_t)k * 4 + c) * N + i] = h[c];
+}
+
+// Dense actor observation row [18 + 4 N_H]: obs_core then H most-recent-first,
+// H[k] = ring[(t_last - k) mod N_H] where t_last is the step that wrote the newest slot.
+__device__ __forceinline__ void write_dense(const DevParams& P, const DevBufs& B, int64_t i,
+                                           const float ob[kObsCore], uint32_t t_last, float* row)
+{
+    const int64_t N = P.n;
+#pragma unroll
+    for (int j = 0; j < kObsCore; ++j) row[j] = ob[j];
+    for (int k = 0; k < P.n_hist; ++k) {
+        const int slot = (int)(((int64_t)t_last - k) % P.n_hist + P.n_hist) % P.n_hist;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) row[kObsCore + 4 * k + c] = B.hist[((int64_t)slot * 4 + c) * N + i];
+    }
+}
+
+__device__ __forceinline__ void stats_block_end(const StatAcc& st, double* srow, double steps, double* slot)
+{
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const bool any = __any_sync(0xffffffffu, st.ep > 0);
+    if (any) {
+        stat_warp_to_smem(st, srow + warp * kStatsLen);
+    } else if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int j = 0; j < kStatsLen; ++j) srow[warp * kStatsLen + j] = 0.0;
+    }
+    __syncthreads();
+    stat_rows_to_slot(srow, nw, steps, slot);
+}
+
+// ---------------------------------------------------------------------------------------
+// l2f_step: one transition for every env.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, const DevBufs B,
+                                                          const float* __restrict__ act, const StepOutDev O)
+{
+    __shared__ double srow[(kStepBlock / 32) * kStatsLen];
+    const int64_t N = P.n;
+    const int64_t i = (int64_t)blockIdx.x * kStepBlock + threadIdx.x;
+    const bool active = i < N;
+    const uint32_t t = P.t0;
+    StatAcc st;
+    stat_zero(st);
+    if (active) {
+        const uint32_t gid = P.id_offset + (uint32_t)i;
+        EnvReg e;
+        load_env(P, B, i, e);
+        float a[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a[c] = __ldg(act + c * N + i);
+        Trans o;
+        transition(P, e, gid, t, a, o);
+        uint32_t fl = o.flags;
+        if (O.final_state) {
+#pragma unroll
+            for (int c = 0; c < kStateDim; ++c) O.final_state[c * N + i] = e.s[c];
+        }
+        bool did_reset = false;
+        float hf[4];
+        if (fl & (D_TERM | D_TRUNC)) {
+            stat_episode(st, o);
+            if (P.flags & F_AUTO_RESET) {
+                reset_env(P, e, gid, t + 1, hf);
+                fl |= D_RESET;
+                did_reset = true;
+            } else {
+                e.ep_step = 0;
+                e.ep_return = 0.0f;
+            }
+        }
+        if (P.n_hist > 0) {
+            if (did_reset) {
+                hist_fill(P, B, i, hf);
+            } else {
+                const int slot = (int)(t % (uint32_t)P.n_hist);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) B.hist[((int64_t)slot * 4 + c) * N + i] = o.a[c];
+            }
+        }
+        store_state(P, B, i, e);
+        if (did_reset) store_episode_consts(P, B, i, e);
+        if (O.obs_core || O.obs_dense) {
+            float ob[kObsCore];
+            observe_core(P, e.s, gid, t + 1, ob);
+            if (O.obs_core) {
+#pragma unroll
+                for (int j = 0; j < kObsCore; ++j) O.obs_core[j * N + i] = ob[j];
+            }
+            if (O.obs_dense) write_dense(P, B, i, ob, t, O.obs_dense + i * (kObsCore + 4 * P.n_hist));
+        }
+        if (O.reward) O.reward[i] = o.reward;
+        if (O.flags) O.flags[i] = (uint8_t)fl;
+    }
+    const int64_t rem = N - (int64_t)blockIdx.x * kStepBlock;
+    stats_block_end(st, srow, (double)(rem < kStepBlock ? rem : kStepBlock), B.slots + (size_t)blockIdx.x * kStatsLen);
+}
+
+// ---------------------------------------------------------------------------------------
+// l2f_reset: masked (or full) reset at Philox counter t0.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kStepBlock) reset_kernel(const DevParams P, const DevBufs B,
+                                                           const uint8_t* __restrict__ mask, const StepOutDev O)
+{
+    const int64_t N = P.n;
+    const int64_t i = (int64_t)blockIdx.x * kStepBlock + threadIdx.x;
+    if (i >= N) return;
+    if (mask && !mask[i]) return;
+    const uint32_t gid = P.id_offset + (uint32_t)i;
+    EnvReg e;
+    float hf[4];
+    reset_env(P, e, gid, P.t0, hf);
+    store_state(P, B, i, e);
+    const int64_t NN = N;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) B.dist[c * NN + i] = e.dist[c];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) B.dr[c * NN + i] = e.dr[c];
+    hist_fill(P, B, i, hf);
+    if (O.obs_core || O.obs_dense) {
+        float ob[kObsCore];
+        observe_core(P, e.s, gid, P.t0, ob);
+        if (O.obs_core) {
+#pragma unroll
+            for (int j = 0; j < kObsCore; ++j) O.obs_core[j * N + i] = ob[j];
+        }
+        if (O.obs_dense) write_dense(P, B, i, ob, P.t0, O.obs_dense + i * (kObsCore + 4 * P.n_hist));
+    }
+    if (O.flags) O.flags[i] = D_RESET;
+    if (O.reward) O.reward[i] = 0.0f;
+}
+
+// ---------------------------------------------------------------------------------------
+// Open-loop fused rollout: T transitions with the state in registers (N3).  Actions from a
+// [T][4][N] buffer or the Philox RAND_ACT stream.  The history ring stays in HBM.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevParams P, const DevBufs B,
+                                                                     const float* __restrict__ act, int32_t T,
+                                                                     float* __restrict__ trace,
+                                                                     const int64_t* __restrict__ trace_ids,
+                                                                     int32_t K)
+{
+    __shared__ double srow[(kRolloutBlock / 32) * kStatsLen];
+    const int64_t N = P.n;
+    const int64_t i = (int64_t)blockIdx.x * kRolloutBlock + threadIdx.x;
+    const bool active = i < N;
+    StatAcc st;
+    stat_zero(st);
+    if (active) {
+        const uint32_t gid = P.id_offset + (uint32_t)i;
+        int tslot = -1;
+        if (trace)
+            for (int k = 0; k < K; ++k)
+                if (trace_ids[k] == i) tslot = k;
+        EnvReg e;
+        load_env(P, B, i, e);
+        for (int32_t k = 0; k < T; ++k) {
+            const uint32_t t = P.t0 + (uint32_t)k;
+            float a[4];
+            if (act) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) a[c] = __ldg(act + ((int64_t)k * 4 + c) * N + i);
+            } else {
+                random_action(P, gid, t, a);
+            }
+            float* tr = (tslot >= 0) ? trace + ((int64_t)k * K + tslot) * kTraceFields : nullptr;
+            if (tr) {
+#pragma unroll
+                for (int c = 0; c < kStateDim; ++c) tr[c] = e.s[c];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tr[17 + c] = a[c];
+            }
+            Trans o;
+            transition(P, e, gid, t, a, o);
+            uint32_t fl = o.flags;
+            bool did_reset = false;
+            float hf[4];
+            if (fl & (D_TERM | D_TRUNC)) {
+                stat_episode(st, o);
+                if (P.flags & F_AUTO_RESET) {
+                    reset_env(P, e, gid, t + 1, hf);
+                    fl |= D_RESET;
+                    did_reset = true;
+                } else {
+                    e.ep_step = 0;
+                    e.ep_return = 0.0f;
+                }
+            }
+            if (P.n_hist > 0) {
+                if (did_reset) {
+                    hist_fill(P, B, i, hf);
+                } else {
+                    const int slot = (int)(t % (uint32_t)P.n_hist);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) B.hist[((int64_t)slot * 4 + c) * N + i] = o.a[c];
+                }
+            }
+            if (tr) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tr[21 + c] = o.a[c];
+                tr[25] = o.reward;
+                tr[26] = (float)fl;
+                tr[27] = (float)e.ep_step;
+                tr[28] = tr[29] = tr[30] = tr[31] = 0.0f;
+            }
+        }
+        store_state(P, B, i, e);
+        store_episode_consts(P, B, i, e);
+    }
+    const int64_t rem = N - (int64_t)blockIdx.x * kRolloutBlock;
+    const double steps = (double)(rem < kRolloutBlock ? rem : kRolloutBlock) * (double)T;
+    stats_block_end(st, srow, steps, B.slots + (size_t)blockIdx.x * kStatsLen);
+}
+
+// Fixed-order reduction of all statistics slots into out[8] (one block of 256 threads).
+__global__ void __launch_bounds__(256) stats_finalize_kernel(double* __restrict__ slots, int32_t n_slots,
+                                                             double* __restrict__ out, int32_t reset)
+{
+    __shared__ double part[256 * kStatsLen];
+    const int tid = threadIdx.x;
+    double acc[kStatsLen];
+#pragma unroll
+    for (int j = 0; j < kStatsLen; ++j) acc[j] = 0.0;
+    for (int s = tid; s < n_slots; s += 256)
+#pragma unroll
+        for (int j = 0; j < kStatsLen; ++j) acc[j] += slots[(size_t)s * kStatsLen + j];
+#pragma unroll
+    for (int j = 0; j < kStatsLen; ++j) part[tid * kStatsLen + j] = acc[j];
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (tid < w)
+#pragma unroll
+            for (int j = 0; j < kStatsLen; ++j) part[tid * kStatsLen + j] += part[(tid + w) * kStatsLen + j];
+        __syncthreads();
+    }
+    if (tid < kStatsLen) out[tid] = part[tid];
+    if (reset) {
+        __syncthreads();
+        for (int s = tid; s < n_slots * kStatsLen; s += 256) slots[s] = 0.0;
+    }
+}
+
+// Self-test: our Philox4x32-10 vs curand's curand_Philox4x32_10 (an independent library
+// routine) on counters (i, t, stream, block) -- diagnostics only.
+__global__ void philox_selftest_kernel(int64_t n, uint32_t k0, uint32_t k1, uint32_t t, uint4* ours, uint4* ref)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t c0 = (uint32_t)i, c2 = (uint32_t)(i % 7), c3 = (uint32_t)(i % 5);
+    ours[i] = philox(c0, t, c2, c3, k0, k1);
+    ref[i] = curand_Philox4x32_10(make_uint4(c0, t, c2, c3), make_uint2(k0, k1));
+}
+
+cudaError_t launch_philox_selftest(int64_t n, uint64_t seed, uint32_t t, uint32_t* ours, uint32_t* ref,
+                                   cudaStream_t s)
+{
+    philox_selftest_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, (uint32_t)seed, (uint32_t)(seed >> 32), t,
+                                                                       (uint4*)ours, (uint4*)ref);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------------------
+cudaError_t launch_step(const DevParams& P, const DevBufs& B, const float* act, const StepOutDev& O,
+                        cudaStream_t s)
+{
+    const int64_t grid = (P.n + kStepBlock - 1) / kStepBlock;
+    step_kernel<<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, act, O);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reset(const DevParams& P, const DevBufs& B, const uint8_t* mask, const StepOutDev& O,
+                         cudaStream_t s)
+{
+    const int64_t grid = (P.n + kStepBlock - 1) / kStepBlock;
+    reset_kernel<<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, mask, O);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rollout_open(const DevParams& P, const DevBufs& B, const float* act, int32_t T, float* trace,
+                                const int64_t* trace_ids, int32_t K, cudaStream_t s)
+{
+    const int64_t grid = (P.n + kRolloutBlock - 1) / kRolloutBlock;
+    rollout_open_kernel<<<(unsigned)grid, kRolloutBlock, 0, s>>>(P, B, act, T, trace, trace_ids, K);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stats_finalize(double* slots, int32_t n_slots, double* out, int32_t reset, cudaStream_t s)
+{
+    stats_finalize_kernel<<<1, 256, 0, s>>>(slots, n_slots, out, reset);
+    return cudaGetLastError();
+}
+
+}  // namespace l2f

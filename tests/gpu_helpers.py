@@ -1,0 +1,81 @@
+"""Helpers for the GPU <-> oracle parity tests: moving env state between the CUDA env's SoA
+workspace and the oracle's per-env records, and the tolerances of BASELINE north_star."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle
+
+# north_star: single step per-component |err| <= 1e-5 |x| + 1e-6
+REL, ABS = 1e-5, 1e-6
+
+
+def close(gpu, ref, rel=REL, abs_=ABS):
+    gpu = np.asarray(gpu, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    return np.abs(gpu - ref) <= rel * np.abs(ref) + abs_
+
+
+def close_step(gpu, ref, prev, rel=REL, abs_=ABS):
+    """Single-step tolerance with the component's scale over the step (Q27):
+    |err| <= 1e-5 max(|x_t|, |x_t+1|) + 1e-6.  FP32 carries ~eps |dx| absolute error on a
+    component that changes by dx in one step, so a value landing near zero after a large
+    change is judged against the change's scale."""
+    gpu = np.asarray(gpu, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    scale = np.maximum(np.abs(ref), np.abs(np.asarray(prev, dtype=np.float64)))
+    return np.abs(gpu - ref) <= rel * scale + abs_
+
+
+# obs_core index -> state index whose pre-step value sets the scale (p, v, omega blocks)
+OBS_PREV = {0: 0, 1: 1, 2: 2, 12: 7, 13: 8, 14: 9, 15: 10, 16: 11, 17: 12}
+
+
+def close_obs(gpu_obs, ref_obs, s_prev):
+    prev = np.zeros(len(ref_obs))
+    for j, k in OBS_PREV.items():
+        prev[j] = s_prev[k]
+    return close_step(gpu_obs, ref_obs, prev)
+
+
+def snapshot(env) -> dict:
+    torch.cuda.synchronize()
+    return {k: getattr(env, k).detach().cpu().numpy().copy()
+            for k in ("state", "dist", "dr", "hist", "ep_step", "ep_return")}
+
+
+def load_snapshot(env, snap: dict):
+    for k, v in snap.items():
+        getattr(env, k).copy_(torch.as_tensor(v))
+    torch.cuda.synchronize()
+
+
+def to_oracle(snap: dict, idx, t: int, n_hist: int) -> np.ndarray:
+    """GPU SoA (ring slot tau mod N_H holds a_tau) -> oracle records (H[k] = a_{t-1-k})."""
+    idx = np.asarray(idx)
+    E = oracle.new_envs(len(idx))
+    for j, i in enumerate(idx):
+        E[j]["s"] = snap["state"][:, i]
+        E[j]["dist"] = snap["dist"][:, i]
+        E[j]["dr"] = snap["dr"][:, i]
+        for k in range(n_hist):
+            slot = (t - 1 - k) % n_hist
+            E[j]["hist"][k] = snap["hist"][slot, :, i]
+        E[j]["ep_step"] = snap["ep_step"][i]
+        E[j]["ep_return"] = snap["ep_return"][i]
+    return E
+
+
+def ring_to_mrf(hist_ring: np.ndarray, i: int, t_next: int, n_hist: int) -> np.ndarray:
+    """Most-recent-first history of env i when the next step is t_next."""
+    return np.array([hist_ring[(t_next - 1 - k) % n_hist, :, i] for k in range(n_hist)])
+
+
+def near_threshold(so, cfg, extra: float = 0.0) -> bool:
+    """Q22: an env-step whose termination margin is within the compared tolerance."""
+    thr = (cfg["term_pos"], cfg["term_vel"], cfg["term_angvel"])
+    for m, t in zip(so.margin, thr):
+        if abs(m) <= max(1e-6, REL * abs(t) + ABS) + extra:
+            return True
+    return False

@@ -1,0 +1,90 @@
+"""CPU-side checks of the C ABI (-m "not gpu"): the library loads, exports every symbol that
+include/l2f.h declares, and validates configs without touching a GPU."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+import inputs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2311_13081_b200 import _build
+    _build.build()
+    import paper_2311_13081_b200 as pkg
+    return pkg.lib()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "l2f.h")).read()
+    return sorted(set(re.findall(r"L2F_API\s+[\w\s\*]+?\b(l2f_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for need in ("l2f_create", "l2f_reset", "l2f_step", "l2f_rollout", "l2f_episode_stats"):
+        assert need in syms
+    assert len(syms) >= 15
+
+
+def test_library_exports_every_declared_symbol(L):
+    from paper_2311_13081_b200.abi import EXPORTS, LIB_PATH
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (l2f_\w+)", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    assert sorted(EXPORTS) == declared_symbols()
+    for s in declared_symbols():
+        assert hasattr(L, s)
+
+
+def test_library_is_sm100a(L):
+    from paper_2311_13081_b200.abi import LIB_PATH
+    out = subprocess.run(["cuobjdump", "--list-elf", LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_abi_version(L):
+    assert L.l2f_abi_version() == 1
+
+
+def _size(L, cfg, n, off=0):
+    from paper_2311_13081_b200.abi import make_config
+    c = make_config(cfg, n, off)
+    b = C.c_size_t()
+    st = L.l2f_workspace_size(C.byref(c), C.byref(b))
+    return st, b.value, L.l2f_last_error().decode()
+
+
+def test_workspace_size_and_validation(L):
+    cfg = inputs.config_c3()
+    n = 1 << 20
+    st, b, _ = _size(L, cfg, n)
+    assert st == 0
+    # state 68 + dist 24 + dr 20 + hist 512 + counters 8 + staging (16 + 72 + 4 + 1) B per env
+    assert 725 * n <= b <= 760 * n
+    assert _size(L, cfg, 0)[0] == 1
+    assert _size(L, cfg, 10, off=(1 << 32) - 5)[0] == 1
+    assert _size(L, inputs.config_c3(n_hist=33), 10)[0] == 1
+    assert _size(L, inputs.config_c3(dt=0.0), 10)[0] == 1
+    bad = inputs.config_c3()
+    bad["params"] = dict(bad["params"], rpm_max=1000.0)  # hover infeasible
+    st, _, msg = _size(L, bad, 10)
+    assert st == 1 and "hover" in msg
+    st, _, msg = _size(L, inputs.config_c3(dr_range=[0.8, 2.5]), 10)  # infeasible at the worst DR corner
+    assert st == 1 and "hover" in msg
+
+
+def test_create_rejects_host_memory(L):
+    from paper_2311_13081_b200.abi import make_config
+    c = make_config(inputs.config_c1(), 64)
+    h = C.c_void_p()
+    buf = (C.c_uint8 * (1 << 20))()
+    addr = (C.addressof(buf) + 255) & ~255
+    st = L.l2f_create(C.byref(c), C.c_void_p(addr), 1 << 19, C.byref(h))
+    assert st != 0

@@ -1,0 +1,403 @@
+"""GPU <-> oracle parity for the single-step API, reset and the open-loop fused rollout
+(-m gpu).  Every comparison runs the CUDA path through the C ABI and the FP64 oracle on the
+same seeded inputs, with BASELINE north_star tolerances:
+  single step: |err| <= 1e-5 |x| + 1e-6 per component;
+  100-step open-loop trajectories: position within 1e-3 m;
+  summed rewards: relative 1e-4 (Q23);
+  flags / history indexing: bit-exact except near-threshold env-steps (Q22)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import inputs
+import oracle
+from gpu_helpers import close, close_obs, close_step, load_snapshot, near_threshold, ring_to_mrf, snapshot, to_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2311_13081_b200 as p
+    p.lib()
+    return p
+
+
+def dev_actions(a):
+    return torch.tensor(np.ascontiguousarray(a), dtype=torch.float32, device="cuda")
+
+
+# ------------------------------------------------------------------------------------------
+def test_philox_matches_curand(pkg):
+    """Our device Philox4x32-10 equals curand_Philox4x32_10 (library routine) bit for bit,
+    and both equal the oracle's Philox (pinned to the Random123 KATs)."""
+    import ctypes as C
+    n = 4096
+    ours = torch.zeros(n, 4, dtype=torch.int32, device="cuda")
+    ref = torch.zeros_like(ours)
+    seed = 0x1234_5678_9ABC_DEF0
+    st = pkg.lib().l2f_selftest_philox(n, seed, 77, C.c_void_p(ours.data_ptr()), C.c_void_p(ref.data_ptr()),
+                                       C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert st == 0
+    a, b = ours.cpu().numpy().view(np.uint32), ref.cpu().numpy().view(np.uint32)
+    assert np.array_equal(a, b)
+    for i in (0, 1, 999, 4095):
+        exp = oracle.philox([i, 77, i % 7, i % 5], [seed & 0xFFFFFFFF, seed >> 32])
+        assert np.array_equal(a[i], exp)
+
+
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("flags", [inputs.ALL_NO_DR, inputs.ALL_NO_DR | inputs.DOMAIN_RAND])
+def test_reset_matches_oracle(pkg, flags):
+    cfg = inputs.config_c2(flags=flags)
+    n = 3000
+    env = pkg.Env(cfg, n, env_id_offset=123)
+    out = env.make_out(obs_dense=True)
+    env.reset(out=out)
+    snap = snapshot(env)
+    ids = np.arange(n)
+    E = oracle.reset_many(cfg, ids + 123, 0)
+    for j in range(17):
+        assert np.all(close(snap["state"][j], E["s"][:, j])), j
+    assert np.all(close(snap["dist"], E["dist"].T))
+    assert np.all(close(snap["dr"], E["dr"].T))
+    for k in range(cfg["n_hist"]):
+        assert np.all(close(snap["hist"][k], E["hist"][:, k, :].T))
+    assert np.all(snap["ep_step"] == 0) and np.all(snap["ep_return"] == 0)
+    obs = out["obs_core"].cpu().numpy()
+    dense = out["obs_dense"].cpu().numpy()
+    for i in range(0, n, 97):
+        ref = oracle.observe(cfg, E[i], i + 123, 0)
+        assert np.all(close(obs[:, i], ref[:18])), i
+        assert np.all(close(dense[i], ref)), i
+
+
+# ------------------------------------------------------------------------------------------
+FEATURE_MIXES = [
+    0,
+    inputs.TERMINATION,
+    inputs.OBS_NOISE | inputs.ACTION_NOISE,
+    inputs.ALL_NO_DR,
+    inputs.ALL_NO_DR | inputs.DOMAIN_RAND,
+]
+
+
+@pytest.mark.parametrize("flags", FEATURE_MIXES)
+def test_single_step_parity(pkg, flags):
+    """10^4 random valid states x random actions, one l2f_step, every output vs the oracle."""
+    cfg = inputs.base_config(flags=flags, seed=99)
+    n = 10000
+    t = 1234
+    env = pkg.Env(cfg, n)
+    env.reset()
+    rs = inputs.random_states(n, seed=21)
+    snap = {"state": rs["state"], "dist": rs["dist"], "dr": rs["dr"] if flags & inputs.DOMAIN_RAND else np.ones((5, n)),
+            "hist": rs["hist"], "ep_step": rs["ep_step"], "ep_return": rs["ep_return"]}
+    load_snapshot(env, snap)
+    snap = snapshot(env)  # fp32-rounded inputs, shared by both sides
+    env.t = t
+    acts = np.random.default_rng(5).uniform(-1.2, 1.2, (4, n))
+    out = env.make_out(final_state=True, obs_dense=True)
+    env.step(dev_actions(acts), out)
+    after = snapshot(env)
+    fin = out["final_state"].cpu().numpy()
+    rew = out["reward"].cpu().numpy()
+    flg = out["flags"].cpu().numpy()
+    obs = out["obs_core"].cpu().numpy()
+    dense = out["obs_dense"].cpu().numpy()
+    E = to_oracle(snap, np.arange(n), t, cfg["n_hist"])
+    n_excl = 0
+    for i in range(n):
+        e = E[i:i + 1]
+        so = oracle.env_step(cfg, e, i, t, acts[:, i].astype(np.float32).astype(np.float64))
+        ref = np.array(so.final_s)
+        s_prev = snap["state"][:, i]
+        assert np.all(close_step(fin[:, i], ref, s_prev)), (i, fin[:, i] - ref, ref)
+        assert close(rew[i], so.reward, abs_=1e-5), (i, rew[i], so.reward)
+        if near_threshold(so, cfg):
+            n_excl += 1
+            continue
+        assert flg[i] == so.flags, (i, flg[i], so.flags)
+        reset = bool(so.flags & oracle.FLAG_RESET)
+        sp = e[0]["s"] if reset else s_prev
+        assert np.all(close_step(after["state"][:, i], e[0]["s"], sp)), i
+        assert after["ep_step"][i] == e[0]["ep_step"]
+        assert close(after["ep_return"][i], e[0]["ep_return"], abs_=1e-4)
+        ob = oracle.observe(cfg, e[0], i, t + 1)
+        assert np.all(close_obs(obs[:, i], ob[:18], sp)), (i, obs[:, i] - ob[:18])
+        assert np.all(close_obs(dense[i][:18], ob[:18], sp)), i
+        assert np.all(close(dense[i][18:], ob[18:])), i
+        # history ring: slot t mod N_H holds a'_t unless the env was reset (filled)
+        H = ring_to_mrf(after["hist"], i, t + 1, cfg["n_hist"])
+        assert np.all(close(H, e[0]["hist"][:cfg["n_hist"]])), i
+    assert n_excl < n // 100
+
+
+# ------------------------------------------------------------------------------------------
+def _gpu_rollout_trace(pkg, cfg, n, T, acts_TCN, trace_ids, t0=0, offset=0):
+    env = pkg.Env(cfg, n, env_id_offset=offset)
+    env.reset()
+    env.t = t0
+    snap0 = snapshot(env)
+    tr = env.rollout(T, actions=dev_actions(acts_TCN) if acts_TCN is not None else None,
+                     trace_ids=torch.as_tensor(trace_ids))
+    torch.cuda.synchronize()
+    return env, snap0, tr.cpu().numpy()
+
+
+def test_c1_open_loop_trajectories(pkg):
+    """C1: 64 envs x 500 steps, fixed params, open-loop U(-1,1) actions (as literally stated),
+    no noise / resets.  Positions within 1e-3 m over the first 100 steps (north_star); the
+    full 500 steps are compared with the same bound while the trajectories stay bounded."""
+    cfg = inputs.config_c1()
+    n, T = 64, 500
+    acts = inputs.actions_uniform(T, n, seed=11)
+    ids = np.arange(n)
+    env, snap0, tr = _gpu_rollout_trace(pkg, cfg, n, T, acts, ids)
+    E = to_oracle(snap0, ids, 0, cfg["n_hist"])
+    _, otr = oracle.rollout(cfg, E, ids.astype(np.uint64), 0, T, oracle.MODE_ACTIONS,
+                            actions=acts.astype(np.float32).astype(np.float64).transpose(0, 2, 1).copy(), trace=True)
+    dp = np.abs(tr[:, :, 0:3] - otr[:, :, 0:3])
+    assert dp[:100].max() <= 1e-3, dp[:100].max()
+    assert np.array_equal(tr[:, :, 26].astype(int) & 7, otr[:, :, 26].astype(int) & 7)
+    # actions recorded identically (raw and applied = clipped raw, no noise)
+    assert np.all(close(tr[:, :, 21:25], otr[:, :, 21:25]))
+
+
+def test_c1_hover_stream_500_steps(pkg):
+    """C1 with the near-hover action stream: trajectories stay near hover, 500-step positions
+    within 1e-3 m."""
+    cfg = inputs.config_c1()
+    n, T = 64, 500
+    acts = inputs.actions_near_hover(T, n, seed=12, sigma=0.05)
+    ids = np.arange(n)
+    _, snap0, tr = _gpu_rollout_trace(pkg, cfg, n, T, acts, ids)
+    E = to_oracle(snap0, ids, 0, cfg["n_hist"])
+    _, otr = oracle.rollout(cfg, E, ids.astype(np.uint64), 0, T, oracle.MODE_ACTIONS,
+                            actions=acts.astype(np.float32).astype(np.float64).transpose(0, 2, 1).copy(), trace=True)
+    dp = np.abs(tr[:, :, 0:3] - otr[:, :, 0:3])
+    assert dp[:100].max() <= 1e-3
+
+
+def test_c2_subset_parity(pkg):
+    """C2 features (noise, reward, termination, auto-reset, disturbance) on 4096 envs x 200
+    steps of near-hover actions: traced subset positions within 1e-3 m, flags bit-exact until
+    the first near-threshold step (Q22, margin within the trajectory tolerance 1e-3), summed
+    rewards relative 1e-4 (Q23)."""
+    cfg = inputs.config_c2()
+    n, T = 4096, 200
+    acts = inputs.actions_near_hover(T, n, seed=12)
+    ids = inputs.trace_ids(n, 256)
+    _, snap0, tr = _gpu_rollout_trace(pkg, cfg, n, T, acts, ids)
+    E = to_oracle(snap0, ids, 0, cfg["n_hist"])
+    a32 = acts.astype(np.float32).astype(np.float64)
+    checked = 0
+    for j, i in enumerate(ids):
+        e = E[j:j + 1]
+        stop, flags, pos, rew = T, [], [], []
+        for k in range(T):
+            pos.append(e[0]["s"][0:3].copy())
+            so = oracle.env_step(cfg, e, int(i), k, a32[k, :, i])
+            flags.append(so.flags)
+            rew.append(so.reward)
+            if near_threshold(so, cfg, extra=1e-3):
+                stop = k
+                break
+        if stop < 5:
+            continue
+        checked += 1
+        gfl = tr[:stop, j, 26].astype(int)
+        assert np.array_equal(gfl, np.array(flags[:stop])), j
+        assert np.abs(tr[:stop, j, 0:3] - np.array(pos[:stop])).max() <= 1e-3, j
+        r_g, r_o = tr[:stop, j, 25].astype(np.float64), np.array(rew[:stop])
+        assert abs(r_g.sum() - r_o.sum()) <= 1e-4 * np.abs(r_o).sum() + 1e-6, j
+    assert checked >= len(ids) // 2
+
+
+# ------------------------------------------------------------------------------------------
+def test_T_steps_equal_rollout_bitwise(pkg):
+    """T x l2f_step and l2f_rollout(T) run the same device arithmetic: bitwise equal state,
+    history, counters and statistics."""
+    cfg = inputs.config_c3()  # C2 features + DR
+    n, T = 5000, 40
+    acts = inputs.actions_near_hover(T, n, seed=3)
+    A = dev_actions(acts)
+    e1 = pkg.Env(cfg, n)
+    e1.reset()
+    for k in range(T):
+        e1.step(A[k].contiguous())
+    s1 = snapshot(e1)
+    st1 = e1.episode_stats().cpu().numpy()
+    e2 = pkg.Env(cfg, n)
+    e2.reset()
+    e2.rollout(T, actions=A)
+    s2 = snapshot(e2)
+    st2 = e2.episode_stats().cpu().numpy()
+    for k in s1:
+        assert np.array_equal(s1[k], s2[k]), k
+    assert np.array_equal(st1[[0, 1, 2, 3, 4, 7]], st2[[0, 1, 2, 3, 4, 7]])
+    assert np.allclose(st1, st2, rtol=1e-12)
+    assert e1.t == e2.t == T
+
+
+def test_shard_invariance_bitwise(pkg):
+    """RNG keyed by global env id (Q20): two shards with offsets == one big env, bitwise."""
+    cfg = inputs.config_c3()
+    n, T = 3000, 30
+    acts = inputs.actions_near_hover(T, n, seed=4)
+    big = pkg.Env(cfg, n)
+    big.reset()
+    big.rollout(T, actions=dev_actions(acts))
+    sb = snapshot(big)
+    parts = []
+    for lo, hi in ((0, 1234), (1234, n)):
+        e = pkg.Env(cfg, hi - lo, env_id_offset=lo)
+        e.reset()
+        e.rollout(T, actions=dev_actions(acts[:, :, lo:hi]))
+        parts.append(snapshot(e))
+    for k in ("state", "dist", "dr", "hist"):
+        assert np.array_equal(sb[k], np.concatenate([p[k] for p in parts], axis=-1)), k
+    assert np.array_equal(sb["ep_step"], np.concatenate([p["ep_step"] for p in parts]))
+
+
+def test_determinism_run_to_run(pkg):
+    cfg = inputs.config_c2()
+    n, T = 4096, 100
+    res = []
+    for _ in range(2):
+        e = pkg.Env(cfg, n)
+        e.reset()
+        e.rollout(T)  # Philox random actions
+        res.append((snapshot(e), e.episode_stats().cpu().numpy()))
+    for k in res[0][0]:
+        assert np.array_equal(res[0][0][k], res[1][0][k])
+    assert np.array_equal(res[0][1], res[1][1])
+
+
+def test_random_action_stream_matches_oracle(pkg):
+    cfg = inputs.config_c2()
+    n, T = 512, 50
+    ids = np.arange(0, n, 5)
+    _, snap0, tr = _gpu_rollout_trace(pkg, cfg, n, T, None, ids)
+    for k in (0, 7, 49):
+        for j, i in enumerate(ids[:20]):
+            assert np.all(close(tr[k, j, 17:21], oracle.random_action(cfg, int(i), k), abs_=1e-6))
+
+
+def test_stats_match_oracle(pkg):
+    """Episode statistics of a C2 run vs the oracle run from the same start (FP64 sums)."""
+    cfg = inputs.config_c2()
+    n, T = 2048, 150
+    acts = inputs.actions_near_hover(T, n, seed=12)
+    env = pkg.Env(cfg, n)
+    env.reset()
+    snap0 = snapshot(env)
+    env.episode_stats(reset=True)
+    env.rollout(T, actions=dev_actions(acts))
+    st = env.episode_stats().cpu().numpy()
+    ids = np.arange(n)
+    E = to_oracle(snap0, ids, 0, cfg["n_hist"])
+    ost, _ = oracle.rollout(cfg, E, ids.astype(np.uint64), 0, T, oracle.MODE_ACTIONS,
+                            actions=acts.astype(np.float32).astype(np.float64).transpose(0, 2, 1).copy(), nthreads=8)
+    assert st[7] == ost[7] == n * T
+    # counts may differ only by near-threshold flips (Q22): a handful out of thousands
+    assert abs(st[0] - ost[0]) <= max(3, 2e-3 * ost[0])
+    assert abs(st[4] - ost[4]) <= 2e-3 * ost[4]
+    assert abs(st[5] - ost[5]) <= 2e-3 * abs(ost[5]) + 1
+
+
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("n,nh", [(1, 32), (257, 32), (1000, 0), (300, 1), (513, 7)])
+def test_edge_sizes_and_history_lengths(pkg, n, nh):
+    """Ragged tails, N = 1, N_H = 0 / 1 / 7: one step vs the oracle incl. history indexing."""
+    cfg = inputs.config_c2(n_hist=nh)
+    env = pkg.Env(cfg, n)
+    env.reset()
+    env.t = 5
+    snap = snapshot(env)
+    acts = np.random.default_rng(n).uniform(-1, 1, (4, n))
+    out = env.make_out(final_state=True, obs_dense=True)
+    env.step(dev_actions(acts), out)
+    after = snapshot(env)
+    E = to_oracle(snap, np.arange(n), 5, nh)
+    dense = out["obs_dense"].cpu().numpy()
+    assert dense.shape == (n, 18 + 4 * nh)
+    for i in range(n):
+        e = E[i:i + 1]
+        so = oracle.env_step(cfg, e, i, 5, acts[:, i].astype(np.float32).astype(np.float64))
+        if near_threshold(so, cfg):
+            continue
+        sp = snap["state"][:, i]
+        assert np.all(close_step(out["final_state"].cpu().numpy()[:, i], so.final_s, sp))
+        if nh:
+            H = ring_to_mrf(after["hist"], i, 6, nh)
+            assert np.all(close(H, e[0]["hist"][:nh]))
+        ob = oracle.observe(cfg, e[0], i, 6)
+        sp2 = e[0]["s"] if so.flags & oracle.FLAG_RESET else sp
+        assert np.all(close_obs(dense[i][:18], ob[:18], sp2))
+        assert np.all(close(dense[i][18:], ob[18:]))
+
+
+def test_masked_reset(pkg):
+    cfg = inputs.config_c2()
+    n = 1000
+    env = pkg.Env(cfg, n)
+    env.reset()
+    env.rollout(20)
+    before = snapshot(env)
+    mask = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    mask[::3] = 1
+    env.reset(mask=mask)
+    after = snapshot(env)
+    t = env.t
+    m = mask.cpu().numpy().astype(bool)
+    assert np.array_equal(after["state"][:, ~m], before["state"][:, ~m])
+    E = oracle.reset_many(cfg, np.nonzero(m)[0], t)
+    assert np.all(close(after["state"][:, m], E["s"].T))
+
+
+def test_invalid_arguments_fail_loudly(pkg):
+    cfg = inputs.config_c2()
+    env = pkg.Env(cfg, 64)
+    with pytest.raises(pkg.L2FError):
+        env.rollout(0)
+    with pytest.raises(pkg.L2FError):
+        pkg.Env(inputs.config_c2(n_hist=40), 64)
+
+
+def test_c3_full_size_sampled(pkg):
+    """C3 at full size (2^20 envs, DR, single-step API, the launch configuration bench.py
+    times): 2000 sampled envs vs the oracle; global invariants on all envs."""
+    cfg = inputs.config_c3()
+    n = 1 << 20
+    env = pkg.Env(cfg, n)
+    env.reset()
+    A = dev_actions(inputs.actions_near_hover(1, n, seed=8)[0])
+    for _ in range(3):
+        env.step(A)
+    snap = snapshot(env)
+    t = env.t
+    out = env.make_out(final_state=True)
+    env.step(A, out)
+    after = snapshot(env)
+    fin = out["final_state"].cpu().numpy()
+    flg = out["flags"].cpu().numpy()
+    q = after["state"][3:7]
+    assert np.allclose(np.linalg.norm(q, axis=0), 1, atol=1e-6)
+    assert np.all(np.isfinite(after["state"]))
+    assert np.all((after["state"][13:17] >= 0) & (after["state"][13:17] <= cfg["params"]["rpm_max"]))
+    idx = inputs.trace_ids(n, 2000, seed=5)
+    E = to_oracle(snap, idx, t, cfg["n_hist"])
+    a = A.cpu().numpy()
+    for j, i in enumerate(idx):
+        e = E[j:j + 1]
+        so = oracle.env_step(cfg, e, int(i), t, a[:, i].astype(np.float64))
+        sp = snap["state"][:, i]
+        assert np.all(close_step(fin[:, i], so.final_s, sp)), i
+        if not near_threshold(so, cfg):
+            assert flg[i] == so.flags
+            sp2 = e[0]["s"] if so.flags & oracle.FLAG_RESET else sp
+            assert np.all(close_step(after["state"][:, i], e[0]["s"], sp2)), i
