@@ -1,7 +1,510 @@
-// placeholder, replaced by the tcgen05 MLP rollout
+// l2f_mlp.cu -- fused rollout with the actor MLP on 5th-gen tensor cores (tcgen05), sm_100a.
+//
+// Per step and env (BASELINE configs[3]):
+//   o_t = {p, R, v, omega} + noise  ++  H (last N_H applied actions, most recent first)
+//   a_t = tanh(W3 q16(relu(W2 q16(relu(W1 q16(o_t) + b1)) + b2)) + b3)        (Q21)
+//   then the same env transition as l2f_step (l2f_device.cuh).
+//
+// Design:
+//  * persistent CTA per SM, 3 tiles x 128 envs; thread r of a tile owns env row r, which is
+//    both row r of the MMA A operand and TMEM lane r of the accumulator (32x32b loads);
+//  * operands fp16 in shared memory (SWIZZLE_NONE canonical layouts), accumulators fp32 in
+//    TMEM (64 columns per tile reused by the three layers); biases enter the MMA through a
+//    constant "ones" column, so epilogues are relu + fp16 pack only;
+//  * the action history lives in the A operand as a ring: the action of step tau sits at
+//    ring position (-tau mod N_H) and never moves; each step the B descriptor of W1's
+//    history block is rotated instead (MN-major copy with duplicated K rows, so a rotation
+//    by 4 K-rows is a 64-byte start-address offset).  Zero shared-memory traffic for the
+//    history beyond the one 8-byte slot write per env-step;
+//  * one elected thread per tile issues the MMAs after a 128-thread named barrier; MMA
+//    completion is signalled through tcgen05.commit -> mbarrier.  The other two tiles' warps
+//    keep the FP32/INT pipes busy while one tile waits on the tensor core.
+#include "l2f_device.cuh"
 #include "l2f_internal.h"
+#include "l2f_tcgen05.cuh"
+
 namespace l2f {
-int mlp_rollout_grid(int64_t) { return 1; }
-cudaError_t launch_rollout_mlp(const DevParams&, const DevBufs&, const PolicyDev&, int32_t, float*, const int64_t*, int32_t, cudaStream_t) { return cudaErrorNotSupported; }
-cudaError_t launch_policy_forward(const PolicyDev&, const float*, float*, int64_t, cudaStream_t) { return cudaErrorNotSupported; }
+namespace {
+
+constexpr int kTiles = 3;
+constexpr int kM = 128;
+constexpr int kThreads = kTiles * kM;
+constexpr int kHid = 64;
+
+// shared-memory map (bytes)
+constexpr uint32_t kChunkA = kM * 16;                 // one 8-wide K chunk of a 128-row A tile
+constexpr uint32_t kA1Bytes = 20 * kChunkA;           // K = 32 (obs, ones, pad) + 128 (history)
+constexpr uint32_t kA2Bytes = 8 * kChunkA;            // K = 64
+constexpr uint32_t kW1oBytes = 4 * kHid * 16;         // K = 32 x N = 64, K-major
+constexpr uint32_t kW1hBytes = 8 * (8 * kMaxHist * 16);  // MN-major: 8 N-groups x 2*4*N_H K-rows
+constexpr uint32_t kW2Bytes = 10 * kHid * 16;         // K = 80 x N = 64, K-major
+constexpr uint32_t kW3Bytes = 10 * 16 * 16;           // K = 80 x N = 16, K-major
+constexpr uint32_t kOnesBytes = 2 * kChunkA;          // A K16 slice: column 0 = 1
+
+constexpr uint32_t OFF_A1 = 0;
+constexpr uint32_t OFF_A2 = OFF_A1 + kTiles * kA1Bytes;
+constexpr uint32_t OFF_W1O = OFF_A2 + kTiles * kA2Bytes;
+constexpr uint32_t OFF_W1H = OFF_W1O + kW1oBytes;
+constexpr uint32_t OFF_W2 = OFF_W1H + kW1hBytes;
+constexpr uint32_t OFF_W3 = OFF_W2 + kW2Bytes;
+constexpr uint32_t OFF_ONES = OFF_W3 + kW3Bytes;
+constexpr uint32_t OFF_BAR = OFF_ONES + kOnesBytes;   // kTiles mbarriers
+constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * kTiles;
+constexpr uint32_t OFF_STAT = OFF_TMEM + 8;           // (kThreads/32) x 8 doubles
+constexpr uint32_t kSmemBytes = OFF_STAT + (kThreads / 32) * kStatsLen * 8;
+static_assert(kSmemBytes <= 232448, "shared memory budget");
+constexpr uint32_t kTmemCols = 256;  // kTiles x 64, power of two
+
+constexpr uint32_t kIdescN64 = tc::make_idesc(128, 64, 0, 0);
+constexpr uint32_t kIdescN64BMN = tc::make_idesc(128, 64, 0, 1);
+constexpr uint32_t kIdescN16 = tc::make_idesc(128, 16, 0, 0);
+
+__device__ __forceinline__ uint16_t h16(const uint16_t* p, int i) { return __ldg(p + i); }
+
+__device__ __forceinline__ void st_u16(uint32_t saddr, uint16_t v)
+{
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(saddr), "h"(v) : "memory");
 }
+
+// Lay out the policy in shared memory (once per CTA): B operands with the bias as the K row
+// paired with the A operand's ones column.
+__device__ void stage_weights(const PolicyDev& W, uint32_t sbase, int n_hist)
+{
+    const int tid = threadIdx.x;
+    const int I = W.in_dim;
+    for (int idx = tid; idx < kHid * 32; idx += blockDim.x) {  // W1 obs part, K-major
+        const int n = idx / 32, k = idx % 32;
+        const uint16_t v = k < 18 ? h16(W.W1, n * I + k) : (k == 18 ? h16(W.b1, n) : (uint16_t)0);
+        st_u16(sbase + OFF_W1O + (k / 8) * (kHid * 16) + n * 16 + (k % 8) * 2, v);
+    }
+    const int hk = 4 * n_hist;  // history K
+    const uint32_t sbo_h = 2 * hk * 16;
+    for (int idx = tid; idx < kHid * 2 * hk; idx += blockDim.x) {  // W1 history, MN-major, rows duplicated
+        const int n = idx / (2 * hk), i = idx % (2 * hk);
+        const uint16_t v = h16(W.W1, n * I + 18 + (i % hk));
+        st_u16(sbase + OFF_W1H + (n / 8) * sbo_h + i * 16 + (n % 8) * 2, v);
+    }
+    for (int idx = tid; idx < kHid * 80; idx += blockDim.x) {  // W2 + b2, K-major
+        const int n = idx / 80, k = idx % 80;
+        const uint16_t v = k < 64 ? h16(W.W2, n * 64 + k) : (k == 64 ? h16(W.b2, n) : (uint16_t)0);
+        st_u16(sbase + OFF_W2 + (k / 8) * (kHid * 16) + n * 16 + (k % 8) * 2, v);
+    }
+    for (int idx = tid; idx < 16 * 80; idx += blockDim.x) {  // W3 + b3 padded to N = 16, K-major
+        const int n = idx / 80, k = idx % 80;
+        uint16_t v = 0;
+        if (n < 4) v = k < 64 ? h16(W.W3, n * 64 + k) : (k == 64 ? h16(W.b3, n) : (uint16_t)0);
+        st_u16(sbase + OFF_W3 + (k / 8) * (16 * 16) + n * 16 + (k % 8) * 2, v);
+    }
+    for (int r = tid; r < kM; r += blockDim.x) {  // ones column
+        tc::sts128(sbase + OFF_ONES + r * 16, 0x3C00u, 0u, 0u, 0u);
+        tc::sts128(sbase + OFF_ONES + kChunkA + r * 16, 0u, 0u, 0u, 0u);
+    }
+}
+
+__device__ __forceinline__ float tanh_fast(float z)
+{
+    // tanh z = 1 - 2 / (exp(2z) + 1); exact limits at +-inf, absolute error ~1e-7
+    return 1.0f - __fdividef(2.0f, __expf(2.0f * z) + 1.0f);
+}
+
+struct TileCtx {
+    uint32_t a1_row, a2_row;  // this thread's row in the A1 / A2 tiles
+    uint32_t a1, a2;          // tile bases
+    uint32_t mbar;
+    uint32_t tmem_row;        // TMEM address of (this thread's lane, tile column 0)
+    uint32_t tmem_tile;       // TMEM address of (lane 0, tile column 0)
+    uint32_t bar_id;
+    uint32_t phase;
+    bool leader;
+};
+
+// Epilogue of L1 / L2: accumulator row -> relu -> fp16 -> A2 row.
+__device__ __forceinline__ void epilogue_hidden(const TileCtx& c)
+{
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint32_t v[16];
+        tc::tmem_ld16(c.tmem_row + 16 * q, v);
+        tc::tmem_wait_ld();
+        tc::sts128(c.a2_row + (2 * q) * kChunkA, tc::relu_pack(v[0], v[1]), tc::relu_pack(v[2], v[3]),
+                   tc::relu_pack(v[4], v[5]), tc::relu_pack(v[6], v[7]));
+        tc::sts128(c.a2_row + (2 * q + 1) * kChunkA, tc::relu_pack(v[8], v[9]), tc::relu_pack(v[10], v[11]),
+                   tc::relu_pack(v[12], v[13]), tc::relu_pack(v[14], v[15]));
+    }
+}
+
+__device__ __forceinline__ void handoff_to_mma(const TileCtx& c)
+{
+    tc::fence_proxy_async();
+    tc::fence_before();
+    tc::named_sync(c.bar_id, kM);
+}
+
+__device__ __forceinline__ void wait_mma(TileCtx& c)
+{
+    tc::mbar_wait(c.mbar, c.phase);
+    c.phase ^= 1u;
+    tc::fence_after();
+}
+
+// The three layers on the tensor core for one tile.  Precondition: A1 rows written by all 128
+// threads.  `rot` = rotation of the history ring (W1 history row offset in slots).
+__device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist, uint32_t rot, float a[4])
+{
+    const uint32_t hk = 4u * (uint32_t)n_hist;
+    handoff_to_mma(c);
+    if (c.leader) {
+        tc::fence_after();
+        // L1: obs part (K = 32) then history (K = 4 N_H), D = tile columns [0, 64)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+            tc::mma_f16(c.tmem_tile, tc::make_desc(c.a1 + 2 * j * kChunkA, kChunkA, 128),
+                        tc::make_desc(sbase + OFF_W1O + 2 * j * (kHid * 16), kHid * 16, 128), kIdescN64, j);
+        for (int j = 0; j < n_hist / 4; ++j)
+            tc::mma_f16(c.tmem_tile, tc::make_desc(c.a1 + (4 + 2 * j) * kChunkA, kChunkA, 128),
+                        tc::make_desc(sbase + OFF_W1H + (16u * j + 4u * rot) * 16u, 128, 2u * hk * 16u),
+                        kIdescN64BMN, 1);
+        tc::commit(c.mbar);
+    }
+    wait_mma(c);
+    epilogue_hidden(c);
+    handoff_to_mma(c);
+    if (c.leader) {
+        tc::fence_after();
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            tc::mma_f16(c.tmem_tile, tc::make_desc(c.a2 + 2 * j * kChunkA, kChunkA, 128),
+                        tc::make_desc(sbase + OFF_W2 + 2 * j * (kHid * 16), kHid * 16, 128), kIdescN64, j);
+        tc::mma_f16(c.tmem_tile, tc::make_desc(sbase + OFF_ONES, kChunkA, 128),
+                    tc::make_desc(sbase + OFF_W2 + 8 * (kHid * 16), kHid * 16, 128), kIdescN64, 1);
+        tc::commit(c.mbar);
+    }
+    wait_mma(c);
+    epilogue_hidden(c);
+    handoff_to_mma(c);
+    if (c.leader) {
+        tc::fence_after();
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            tc::mma_f16(c.tmem_tile, tc::make_desc(c.a2 + 2 * j * kChunkA, kChunkA, 128),
+                        tc::make_desc(sbase + OFF_W3 + 2 * j * 256, 256, 128), kIdescN16, j);
+        tc::mma_f16(c.tmem_tile, tc::make_desc(sbase + OFF_ONES, kChunkA, 128),
+                    tc::make_desc(sbase + OFF_W3 + 8 * 256, 256, 128), kIdescN16, 1);
+        tc::commit(c.mbar);
+    }
+    wait_mma(c);
+    uint32_t v[4];
+    tc::tmem_ld4(c.tmem_row, v);
+    tc::tmem_wait_ld();
+    tc::fence_before();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a[j] = tanh_fast(__uint_as_float(v[j]));
+}
+
+__device__ __forceinline__ void write_obs_row(const TileCtx& c, const float o[kObsCore])
+{
+    tc::sts128(c.a1_row, tc::pack_h2(o[0], o[1]), tc::pack_h2(o[2], o[3]), tc::pack_h2(o[4], o[5]),
+               tc::pack_h2(o[6], o[7]));
+    tc::sts128(c.a1_row + kChunkA, tc::pack_h2(o[8], o[9]), tc::pack_h2(o[10], o[11]), tc::pack_h2(o[12], o[13]),
+               tc::pack_h2(o[14], o[15]));
+    tc::sts128(c.a1_row + 2 * kChunkA, tc::pack_h2(o[16], o[17]), 0x00003C00u /* (1, 0) */, 0u, 0u);
+}
+
+// history ring position p -> A1 address (8 bytes: 4 fp16)
+__device__ __forceinline__ uint32_t hist_addr(const TileCtx& c, int p)
+{
+    return c.a1_row + (4 + (p >> 1)) * kChunkA + (p & 1) * 8;
+}
+
+__device__ void setup_cta(const PolicyDev& W, uint32_t sbase, int n_hist)
+{
+    stage_weights(W, sbase, n_hist);
+    if (threadIdx.x == 0) {
+        for (int g = 0; g < kTiles; ++g) tc::mbar_init(sbase + OFF_BAR + 8 * g, 1);
+        tc::fence_mbar_init();
+    }
+    if (threadIdx.x < 32) tc::tmem_alloc(sbase + OFF_TMEM, kTmemCols);
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+}
+
+__device__ __forceinline__ TileCtx make_ctx(uint32_t sbase)
+{
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int g = threadIdx.x / kM, r = threadIdx.x % kM;
+    const uint32_t tbase = *reinterpret_cast<const uint32_t*>(smem + OFF_TMEM);
+    TileCtx c;
+    c.a1 = sbase + OFF_A1 + g * kA1Bytes;
+    c.a2 = sbase + OFF_A2 + g * kA2Bytes;
+    c.a1_row = c.a1 + r * 16;
+    c.a2_row = c.a2 + r * 16;
+    c.mbar = sbase + OFF_BAR + 8 * g;
+    c.tmem_tile = tbase + 64 * g;
+    c.tmem_row = c.tmem_tile + ((uint32_t)(32 * (r / 32)) << 16);
+    c.bar_id = 1 + g;
+    c.phase = 0;
+    c.leader = (r == 0);
+    tc::sts128(c.a1_row + 3 * kChunkA, 0u, 0u, 0u, 0u);  // K 24..31: constant zero pad
+    return c;
+}
+
+__device__ void teardown_cta()
+{
+    extern __shared__ __align__(1024) uint8_t smem[];
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (threadIdx.x < 32) tc::tmem_dealloc(*reinterpret_cast<const uint32_t*>(smem + OFF_TMEM), kTmemCols);
+}
+
+// -------------------------------------------------------------------------------------------
+// Fused rollout: T steps of {obs -> MLP (tensor cores) -> env transition} per env.
+// -------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1)
+    rollout_mlp_kernel(const DevParams P, const DevBufs B, const PolicyDev W, int32_t T, float* __restrict__ trace,
+                       const int64_t* __restrict__ trace_ids, int32_t K, int32_t n_tiles)
+{
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t sbase = tc::smem_u32(smem);
+    const int NH = P.n_hist;
+    setup_cta(W, sbase, NH);
+    TileCtx c = make_ctx(sbase);
+    const int64_t N = P.n;
+    const int r = threadIdx.x % kM;
+    StatAcc st;
+    stat_zero(st);
+    double steps_done = 0.0;
+
+    for (int tile = blockIdx.x * kTiles + (int)(threadIdx.x / kM); tile < n_tiles; tile += gridDim.x * kTiles) {
+        const int64_t i = (int64_t)tile * kM + r;
+        const bool active = i < N;
+        const uint32_t gid = P.id_offset + (uint32_t)i;
+        EnvReg e;
+        if (active) {
+#pragma unroll
+            for (int q = 0; q < kStateDim; ++q) e.s[q] = B.state[q * N + i];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) e.dist[q] = B.dist[q * N + i];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) e.dr[q] = (P.flags & F_DOMAIN_RAND) ? B.dr[q * N + i] : 1.0f;
+            e.ep_step = B.ep_step[i];
+            e.ep_return = B.ep_return[i];
+        } else {
+#pragma unroll
+            for (int q = 0; q < kStateDim; ++q) e.s[q] = 0.0f;
+            e.s[3] = 1.0f;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) e.dist[q] = 0.0f;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) e.dr[q] = 1.0f;
+            e.ep_step = 0;
+            e.ep_return = 0.0f;
+        }
+        // history ring (HBM slot s holds a_tau with tau = s mod N_H) -> A1 position (-s) mod N_H
+        for (int s = 0; s < NH; ++s) {
+            float h[4] = {0.f, 0.f, 0.f, 0.f};
+            if (active)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) h[q] = B.hist[((int64_t)s * 4 + q) * N + i];
+            const int p = (NH - s) % NH;
+            tc::sts64(hist_addr(c, p), tc::pack_h2(h[0], h[1]), tc::pack_h2(h[2], h[3]));
+        }
+        int tslot = -1;
+        if (trace && active)
+            for (int q = 0; q < K; ++q)
+                if (trace_ids[q] == i) tslot = q;
+
+        for (int32_t k = 0; k < T; ++k) {
+            const uint32_t t = P.t0 + (uint32_t)k;
+            float ob[kObsCore];
+            observe_core(P, e.s, gid, t, ob);
+            write_obs_row(c, ob);
+            float a[4];
+            const uint32_t rot = NH > 0 ? (t + (uint32_t)NH - 1u) % (uint32_t)NH : 0u;
+            mlp_tile(c, sbase, NH, rot, a);
+            float* tr = (tslot >= 0) ? trace + ((int64_t)k * K + tslot) * kTraceFields : nullptr;
+            if (tr) {
+#pragma unroll
+                for (int q = 0; q < kStateDim; ++q) tr[q] = e.s[q];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) tr[17 + q] = a[q];
+            }
+            Trans o;
+            transition(P, e, gid, t, a, o);
+            uint32_t fl = o.flags;
+            bool did_reset = false;
+            float hf[4];
+            if (fl & (D_TERM | D_TRUNC)) {
+                if (active) stat_episode(st, o);
+                if (P.flags & F_AUTO_RESET) {
+                    reset_env(P, e, gid, t + 1, hf);
+                    fl |= D_RESET;
+                    did_reset = true;
+                } else {
+                    e.ep_step = 0;
+                    e.ep_return = 0.0f;
+                }
+            }
+            if (NH > 0) {
+                if (did_reset) {
+                    const uint32_t h01 = tc::pack_h2(hf[0], hf[1]), h23 = tc::pack_h2(hf[2], hf[3]);
+                    for (int p = 0; p < NH; p += 2) {
+                        if (p + 1 < NH)
+                            tc::sts128(hist_addr(c, p), h01, h23, h01, h23);
+                        else
+                            tc::sts64(hist_addr(c, p), h01, h23);
+                    }
+                } else {
+                    const int p = (int)((uint32_t)NH - t % (uint32_t)NH) % NH;
+                    tc::sts64(hist_addr(c, p), tc::pack_h2(o.a[0], o.a[1]), tc::pack_h2(o.a[2], o.a[3]));
+                }
+            }
+            if (tr) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) tr[21 + q] = o.a[q];
+                tr[25] = o.reward;
+                tr[26] = (float)fl;
+                tr[27] = (float)e.ep_step;
+                tr[28] = tr[29] = tr[30] = tr[31] = 0.0f;
+            }
+        }
+        if (active) {
+#pragma unroll
+            for (int q = 0; q < kStateDim; ++q) B.state[q * N + i] = e.s[q];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) B.dist[q * N + i] = e.dist[q];
+            if (P.flags & F_DOMAIN_RAND)
+#pragma unroll
+                for (int q = 0; q < 5; ++q) B.dr[q * N + i] = e.dr[q];
+            B.ep_step[i] = e.ep_step;
+            B.ep_return[i] = e.ep_return;
+            for (int s = 0; s < NH; ++s) {
+                uint32_t h01, h23;
+                tc::lds64(hist_addr(c, (NH - s) % NH), h01, h23);
+                const __half2 x = *reinterpret_cast<__half2*>(&h01), y = *reinterpret_cast<__half2*>(&h23);
+                B.hist[((int64_t)s * 4 + 0) * N + i] = __low2float(x);
+                B.hist[((int64_t)s * 4 + 1) * N + i] = __high2float(x);
+                B.hist[((int64_t)s * 4 + 2) * N + i] = __low2float(y);
+                B.hist[((int64_t)s * 4 + 3) * N + i] = __high2float(y);
+            }
+            steps_done += (double)T;
+        }
+    }
+    // statistics: warp -> fixed-order block sum -> this CTA's slot
+    double* srow = reinterpret_cast<double*>(smem + OFF_STAT);
+    const int warp = threadIdx.x >> 5;
+    stat_warp_to_smem(st, srow + warp * kStatsLen);
+    double sd = steps_done;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) srow[warp * kStatsLen + 7] = sd;
+    __syncthreads();
+    if (threadIdx.x < kStatsLen) {
+        double x = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) x += srow[w * kStatsLen + threadIdx.x];
+        B.slots[(size_t)blockIdx.x * kStatsLen + threadIdx.x] += x;
+    }
+    teardown_cta();
+}
+
+// -------------------------------------------------------------------------------------------
+// Policy forward on explicit observations: obs [n][in_dim] fp32 -> act [n][4] (tanh output).
+// The history part of each observation is written in order (ring rotation 0).
+// -------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1)
+    policy_forward_kernel(const PolicyDev W, const float* __restrict__ obs, float* __restrict__ act, int64_t n,
+                          int32_t n_tiles)
+{
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t sbase = tc::smem_u32(smem);
+    const int NH = (W.in_dim - 18) / 4;
+    setup_cta(W, sbase, NH);
+    TileCtx c = make_ctx(sbase);
+    const int r = threadIdx.x % kM;
+    for (int tile = blockIdx.x * kTiles + (int)(threadIdx.x / kM); tile < n_tiles; tile += gridDim.x * kTiles) {
+        const int64_t i = (int64_t)tile * kM + r;
+        const bool active = i < n;
+        const float* row = obs + i * W.in_dim;
+        float o[kObsCore];
+#pragma unroll
+        for (int q = 0; q < kObsCore; ++q) o[q] = active ? row[q] : 0.0f;
+        write_obs_row(c, o);
+        // with rot = 0, ring position p carries H[p]
+        for (int p = 0; p < NH; ++p) {
+            float h[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) h[q] = active ? row[18 + 4 * p + q] : 0.0f;
+            tc::sts64(hist_addr(c, p), tc::pack_h2(h[0], h[1]), tc::pack_h2(h[2], h[3]));
+        }
+        float a[4];
+        mlp_tile(c, sbase, NH, 0u, a);
+        if (active)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) act[i * 4 + q] = a[q];
+    }
+    teardown_cta();
+}
+
+int sm_count()
+{
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
+}  // namespace
+
+// Upper bound of the rollout grid (statistics slots are sized with it; host-only arithmetic).
+int mlp_rollout_grid(int64_t n)
+{
+    const int64_t tiles = (n + kM - 1) / kM;
+    const int64_t g = (tiles + kTiles - 1) / kTiles;
+    return (int)(g < 1024 ? g : 1024);
+}
+
+static int grid_for(int64_t n)
+{
+    const int64_t tiles = (n + kM - 1) / kM;
+    int64_t g = (tiles + kTiles - 1) / kTiles;
+    const int sms = sm_count();
+    return (int)(g < sms ? (g < 1 ? 1 : g) : sms);
+}
+
+cudaError_t launch_rollout_mlp(const DevParams& P, const DevBufs& B, const PolicyDev& W, int32_t T, float* trace,
+                               const int64_t* trace_ids, int32_t K, cudaStream_t s)
+{
+    if (P.n_hist % 4 != 0 || W.hidden != kHid || W.in_dim != 18 + 4 * P.n_hist) return cudaErrorNotSupported;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(rollout_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int n_tiles = (int)((P.n + kM - 1) / kM);
+    rollout_mlp_kernel<<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, n_tiles);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_policy_forward(const PolicyDev& W, const float* obs, float* act, int64_t n, cudaStream_t s)
+{
+    if ((W.in_dim - 18) % 16 != 0 || W.hidden != kHid) return cudaErrorNotSupported;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e =
+            cudaFuncSetAttribute(policy_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int n_tiles = (int)((n + kM - 1) / kM);
+    policy_forward_kernel<<<grid_for(n), kThreads, kSmemBytes, s>>>(W, obs, act, n, n_tiles);
+    return cudaGetLastError();
+}
+
+}  // namespace l2f

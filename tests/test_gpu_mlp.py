@@ -1,0 +1,230 @@
+"""GPU <-> oracle parity of the tcgen05 actor MLP and the fused MLP rollout (-m gpu).
+
+Closed-loop rollouts are checked teacher-forced:
+for every traced env-step the oracle re-evaluates the policy on the GPU's own pre-step state
+and history (action agreement |da| <= 2e-3; <= 1e-4 away from fp16 rounding midpoints) and
+re-steps the env with the GPU's action (single-step state tolerance).  Free-running
+trajectories are compared only in distribution (episode length / return)."""
+import numpy as np
+import pytest
+import torch
+
+import inputs
+import oracle
+from gpu_helpers import close, close_step, snapshot
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2311_13081_b200 as p
+    p.lib()
+    return p
+
+
+def realistic_obs(n, nh, seed):
+    g = np.random.default_rng(seed)
+    cfg = inputs.config_c2(n_hist=nh)
+    E = oracle.reset_many(cfg, np.arange(n), 3)
+    obs = np.stack([oracle.observe(cfg, E[i], i, 3) for i in range(n)])
+    if nh:
+        obs[:, 18:] = g.uniform(-1, 1, (n, 4 * nh))
+    return obs
+
+
+@pytest.mark.parametrize("nh", [32, 4, 0])
+def test_policy_forward_matches_oracle(pkg, nh):
+    n = 3000
+    W = inputs.policy_weights(18 + 4 * nh, 64, seed=7)
+    obs = realistic_obs(n, nh, seed=1)
+    pol = pkg.Policy(W)
+    a = pkg.policy_forward(pol, torch.tensor(obs, dtype=torch.float32, device="cuda")).cpu().numpy()
+    ph = oracle.PolicyHandle(W)
+    o32 = obs.astype(np.float32).astype(np.float64)
+    worst_ok = 0.0
+    for i in range(n):
+        ref = oracle.mlp(ph, o32[i])
+        d = np.max(np.abs(a[i] - ref))
+        assert d <= 2e-3, (i, a[i], ref)
+        if oracle.mlp_midpoint_margin(ph, o32[i]) > 1e-5:
+            worst_ok = max(worst_ok, d)
+    assert worst_ok <= 1e-4, worst_ok
+
+
+def test_policy_forward_ragged_and_large(pkg):
+    W = inputs.policy_weights(146, 64, seed=9)
+    pol = pkg.Policy(W)
+    ph = oracle.PolicyHandle(W)
+    for n in (1, 127, 129, 100_003):
+        obs = np.random.default_rng(n).uniform(-1, 1, (n, 146))
+        a = pkg.policy_forward(pol, torch.tensor(obs, dtype=torch.float32, device="cuda")).cpu().numpy()
+        for i in np.unique(np.linspace(0, n - 1, 50).astype(int)):
+            ref = oracle.mlp(ph, obs[i].astype(np.float32).astype(np.float64))
+            assert np.max(np.abs(a[i] - ref)) <= 2e-3
+
+
+def _teacher_forced(pkg, cfg, n, T, K, t0=0, seed=7, check_every=1):
+    nh = cfg["n_hist"]
+    W = inputs.policy_weights(18 + 4 * nh, 64, seed=seed, out_bias=inputs.hover_policy_bias())
+    pol = pkg.Policy(W)
+    ph = oracle.PolicyHandle(W)
+    env = pkg.Env(cfg, n)
+    env.reset()
+    env.t = t0
+    snap0 = snapshot(env)
+    ids = inputs.trace_ids(n, K, seed=3)
+    tr = env.rollout(T, policy=pol, trace_ids=torch.as_tensor(ids)).cpu().numpy()
+    after = snapshot(env)
+    n_checked = n_excl = 0
+    worst = 0.0
+    for j, i in enumerate(ids):
+        e = oracle.new_envs(1)
+        e[0]["dist"] = snap0["dist"][:, i]
+        e[0]["dr"] = snap0["dr"][:, i]
+        H = [snap0["hist"][(t0 - 1 - k) % nh, :, i] for k in range(nh)]
+        ep = int(snap0["ep_step"][i])
+        ret = float(snap0["ep_return"][i])
+        for k in range(T):
+            t = t0 + k
+            rec = tr[k, j]
+            e[0]["s"] = rec[:17]
+            e[0]["ep_step"] = ep
+            e[0]["ep_return"] = ret
+            e[0]["hist"][:] = 0
+            if nh:
+                e[0]["hist"][:nh] = np.array(H)
+            a_gpu = rec[17:21].astype(np.float64)
+            if k % check_every == 0:
+                ob = oracle.observe(cfg, e[0], int(i), t)
+                a_ref = oracle.mlp(ph, ob)
+                d = np.max(np.abs(a_gpu - a_ref))
+                assert d <= 2e-3, (j, k, a_gpu, a_ref)
+                if oracle.mlp_midpoint_margin(ph, ob) > 1e-5:
+                    worst = max(worst, d)
+                else:
+                    n_excl += 1
+                n_checked += 1
+            so = oracle.env_step(cfg, e, int(i), t, a_gpu)
+            assert np.all(close(rec[21:25], so.a_applied, abs_=2e-6)), (j, k)
+            assert close(rec[25], so.reward, abs_=1e-5), (j, k, rec[25], so.reward)
+            assert int(rec[26]) == so.flags or abs(min(so.margin, key=abs)) < 1e-4, (j, k, rec[26], so.flags)
+            if int(rec[26]) != so.flags:
+                break  # near-threshold flip (Q22): stop following this env
+            nxt = tr[k + 1, j, :17] if k + 1 < T else after["state"][:, i]
+            ref_next = e[0]["s"]
+            prev = rec[:17] if not (so.flags & oracle.FLAG_RESET) else ref_next
+            assert np.all(close_step(nxt, ref_next, prev)), (j, k, nxt - ref_next)
+            ep, ret = int(e[0]["ep_step"]), float(e[0]["ep_return"])
+            if so.flags & oracle.FLAG_RESET:
+                H = [e[0]["hist"][kk].copy() for kk in range(nh)]  # fill of the new episode
+            elif nh:
+                H = [np.array(rec[21:25], dtype=np.float64)] + H[:-1]
+            # the new episode's dist / dr come from the oracle's own reset (same Philox counter)
+    return n_checked, n_excl, worst, after, tr, ids
+
+
+def test_mlp_rollout_teacher_forced_c4(pkg):
+    cfg = inputs.config_c4()
+    n_checked, n_excl, worst, _, _, _ = _teacher_forced(pkg, cfg, n=2000, T=60, K=48)
+    assert n_checked > 1000
+    assert worst <= 1e-4, worst
+
+
+def test_mlp_rollout_teacher_forced_c5_curriculum_dr(pkg):
+    """C5 features with a curriculum stage boundary inside the rollout, plus DR."""
+    cfg = inputs.config_c5(flags=inputs.ALL_NO_DR | inputs.DOMAIN_RAND)
+    cfg["curriculum"]["interval"] = 20
+    _, _, worst, _, _, _ = _teacher_forced(pkg, cfg, n=700, T=45, K=32, t0=7)
+    assert worst <= 1e-4
+
+
+@pytest.mark.parametrize("nh", [4, 8, 0])
+def test_mlp_rollout_history_lengths(pkg, nh):
+    cfg = inputs.config_c4(n_hist=nh)
+    _, _, worst, _, _, _ = _teacher_forced(pkg, cfg, n=300, T=40, K=16)
+    assert worst <= 1e-4
+
+
+def test_mlp_rollout_history_writeback_and_continuation(pkg):
+    """After a rollout the HBM ring holds q16(a') of the last N_H steps in ring order, so a
+    second rollout (or l2f_step) continues exactly where the first stopped."""
+    cfg = inputs.config_c4()
+    n, nh = 512, cfg["n_hist"]
+    W = inputs.policy_weights(146, 64, seed=5, out_bias=inputs.hover_policy_bias())
+    pol = pkg.Policy(W)
+    env = pkg.Env(cfg, n)
+    env.reset()
+    ids = np.arange(0, n, 37)
+    tr = env.rollout(50, policy=pol, trace_ids=torch.as_tensor(ids)).cpu().numpy()
+    after = snapshot(env)
+    for j, i in enumerate(ids):
+        fl = tr[:, j, 26].astype(int)
+        last_reset = max([k for k in range(50) if fl[k] & 8], default=-1)
+        for k in range(max(last_reset + 1, 50 - nh), 50):
+            exp = np.asarray(tr[k, j, 21:25], dtype=np.float16).astype(np.float32)
+            assert np.array_equal(after["hist"][k % nh, :, i], exp), (i, k)
+    # continuation: rollout(20) + rollout(30) == rollout(50) bitwise
+    e1 = pkg.Env(cfg, n)
+    e1.reset()
+    e1.rollout(20, policy=pol)
+    e1.rollout(30, policy=pol)
+    e2 = pkg.Env(cfg, n)
+    e2.reset()
+    e2.rollout(50, policy=pol)
+    s1, s2 = snapshot(e1), snapshot(e2)
+    for k in s1:
+        assert np.array_equal(s1[k], s2[k]), k
+
+
+def test_mlp_rollout_shard_invariance_and_determinism(pkg):
+    cfg = inputs.config_c5()
+    n = 3 * 128 * 5 + 77
+    W = inputs.policy_weights(146, 64, seed=5, out_bias=inputs.hover_policy_bias())
+    pol = pkg.Policy(W)
+    big = pkg.Env(cfg, n)
+    big.reset()
+    big.rollout(30, policy=pol)
+    sb = snapshot(big)
+    big2 = pkg.Env(cfg, n)
+    big2.reset()
+    big2.rollout(30, policy=pol)
+    assert all(np.array_equal(sb[k], snapshot(big2)[k]) for k in sb)
+    lo = 1000
+    a = pkg.Env(cfg, lo)
+    a.reset()
+    a.rollout(30, policy=pol)
+    b = pkg.Env(cfg, n - lo, env_id_offset=lo)
+    b.reset()
+    b.rollout(30, policy=pol)
+    sa, sb2 = snapshot(a), snapshot(b)
+    for k in ("state", "dist", "hist"):
+        assert np.array_equal(sb[k], np.concatenate([sa[k], sb2[k]], axis=-1)), k
+
+
+def test_mlp_rollout_distribution_matches_oracle(pkg):
+    """Free-running closed loop: episode statistics agree in distribution (parity of long
+    trajectories is unpinned): mean length / return within 4 SE."""
+    cfg = inputs.config_c4()
+    n, T = 8192, 120
+    W = inputs.policy_weights(146, 64, seed=7, out_bias=inputs.hover_policy_bias())
+    env = pkg.Env(cfg, n)
+    env.reset()
+    snap0 = snapshot(env)
+    env.episode_stats(reset=True)
+    env.rollout(T, policy=pkg.Policy(W))
+    st = env.episode_stats().cpu().numpy()
+    ids = np.arange(n, dtype=np.uint64)
+    E = oracle.reset_many(cfg, ids, 0)
+    ost, _ = oracle.rollout(cfg, E, ids, 0, T, oracle.MODE_POLICY, policy=oracle.PolicyHandle(W), nthreads=8)
+    assert st[7] == ost[7] == n * T
+    for s in (st, ost):
+        assert s[0] > 1000
+    m_g, m_o = st[4] / st[0], ost[4] / ost[0]
+    r_g, r_o = st[5] / st[0], ost[5] / ost[0]
+    var_r = ost[6] / ost[0] - r_o ** 2
+    se_r = np.sqrt(var_r / ost[0])
+    assert abs(r_g - r_o) <= 4 * np.sqrt(2) * se_r, (r_g, r_o, se_r)
+    assert abs(st[0] - ost[0]) <= 4 * np.sqrt(ost[0]) + 0.02 * ost[0]
+    assert abs(m_g - m_o) <= 0.05 * m_o
