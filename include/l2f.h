@@ -167,9 +167,14 @@ typedef struct {
     float* dist;       /* [6][N]  */
     float* dr;         /* [5][N]  factors (1 when DR is off) */
     float* hist;       /* [N_H][4][N] ring: slot (tau mod N_H) holds the action applied at step tau */
+    int32_t* hist_t0;  /* [N] first step of the current episode */
+    float* hist_fill;  /* [4][N] the episode's initial history value (Q10)                      */
+                       /* Logical history at step t, H[k] (k-th most recent): tau = t-1-k;
+                          H[k] = hist[tau mod N_H] if tau >= hist_t0 else hist_fill.  A reset
+                          writes only hist_t0 / hist_fill (O(1) bytes per env, not N_H x 16).  */
     int32_t* ep_step;  /* [N] */
     float* ep_return;  /* [N] */
-    uint64_t t;        /* global step counter: the next l2f_step is step t */
+    uint64_t t;        /* global step counter: the next l2f_step is step t (< 2^31) */
     int64_t num_envs;
     int32_t action_history;
 } l2f_state_view;

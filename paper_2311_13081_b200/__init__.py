@@ -109,6 +109,8 @@ class Env:
         self.dist = view(v.dist, 6 * n, torch.float32, (6, n))
         self.dr = view(v.dr, 5 * n, torch.float32, (5, n))
         self.hist = view(v.hist, nh * 4 * n, torch.float32, (nh, 4, n))
+        self.hist_t0 = view(v.hist_t0, n, torch.int32, (n,))
+        self.hist_fill = view(v.hist_fill, 4 * n, torch.float32, (4, n))
         self.ep_step = view(v.ep_step, n, torch.int32, (n,))
         self.ep_return = view(v.ep_return, n, torch.float32, (n,))
 

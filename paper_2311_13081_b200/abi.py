@@ -61,7 +61,7 @@ class PolicyS(C.Structure):
 
 class StateView(C.Structure):
     _fields_ = [("state", C.c_void_p), ("dist", C.c_void_p), ("dr", C.c_void_p), ("hist", C.c_void_p),
-                ("ep_step", C.c_void_p), ("ep_return", C.c_void_p), ("t", C.c_uint64),
+                ("hist_t0", C.c_void_p), ("hist_fill", C.c_void_p), ("ep_step", C.c_void_p), ("ep_return", C.c_void_p), ("t", C.c_uint64),
                 ("num_envs", C.c_int64), ("action_history", C.c_int32)]
 
 

@@ -48,7 +48,7 @@ constexpr size_t kPolicyMaxIn = 18 + 4 * L2F_MAX_HIST;
 constexpr size_t kPolicyHalfs = 64 * kPolicyMaxIn + 64 + 64 * 64 + 64 + 4 * 64 + 4;
 
 struct Layout {
-    size_t state, dist, dr, hist, ep_step, ep_return, slots, stats_out, st_act, st_obs, st_rew, st_flags,
+    size_t state, dist, dr, hist, hist_t0, hist_fill, ep_step, ep_return, slots, stats_out, st_act, st_obs, st_rew, st_flags,
         st_policy, total;
     int32_t n_slots;
 };
@@ -68,6 +68,8 @@ Layout layout_for(const l2f_config& c)
     L.dist = take(4 * N * L2F_DIST_DIM);
     L.dr = take(4 * N * L2F_DR_DIM);
     L.hist = take(4 * N * 4 * (size_t)(c.action_history > 0 ? c.action_history : 1));
+    L.hist_t0 = take(4 * N);
+    L.hist_fill = take(4 * N * 4);
     L.ep_step = take(4 * N);
     L.ep_return = take(4 * N);
     L.slots = take(8 * (size_t)L.n_slots * L2F_STATS_LEN);
@@ -298,6 +300,8 @@ l2f_status l2f_create(const l2f_config* cfg, void* d_workspace, size_t bytes, l2
     env->B.dist = (float*)(env->ws + L.dist);
     env->B.dr = (float*)(env->ws + L.dr);
     env->B.hist = (float*)(env->ws + L.hist);
+    env->B.hist_t0 = (int32_t*)(env->ws + L.hist_t0);
+    env->B.hist_fill = (float*)(env->ws + L.hist_fill);
     env->B.ep_step = (int32_t*)(env->ws + L.ep_step);
     env->B.ep_return = (float*)(env->ws + L.ep_return);
     env->B.slots = (double*)(env->ws + L.slots);
@@ -321,7 +325,11 @@ l2f_status l2f_reset(l2f_env* env, const uint8_t* d_mask, const l2f_step_out* ou
     DevParams P;
     params_for(env, env->t, 1, P);
     if (!d_mask) {
+        // full reset: statistics and the (lazily overwritten) history ring start from zero, so
+        // the whole workspace state is a deterministic function of (config, t, actions)
         cudaError_t e = cudaMemsetAsync(env->B.slots, 0, sizeof(double) * L2F_STATS_LEN * env->L.n_slots, s);
+        if (e == cudaSuccess && env->cfg.action_history > 0)
+            e = cudaMemsetAsync(env->B.hist, 0, sizeof(float) * 4 * (size_t)env->cfg.action_history * env->cfg.num_envs, s);
         if (e != cudaSuccess) return cuda_fail(e, "l2f_reset memset");
     }
     return launched(launch_reset(P, env->B, d_mask, to_dev(out), s), "l2f_reset");
@@ -461,6 +469,8 @@ l2f_status l2f_get_state(l2f_env* env, l2f_state_view* out)
     out->dist = env->B.dist;
     out->dr = env->B.dr;
     out->hist = env->B.hist;
+    out->hist_t0 = env->B.hist_t0;
+    out->hist_fill = env->B.hist_fill;
     out->ep_step = env->B.ep_step;
     out->ep_return = env->B.ep_return;
     out->t = env->t;
@@ -472,7 +482,7 @@ l2f_status l2f_get_state(l2f_env* env, l2f_state_view* out)
 l2f_status l2f_set_t(l2f_env* env, uint64_t t)
 {
     if (!env) return fail(L2F_ERR_INVALID_ARGUMENT, "env is NULL");
-    if (t >= (1ull << 32)) return fail(L2F_ERR_INVALID_ARGUMENT, "t must be < 2^32 (Philox counter word)");
+    if (t >= (1ull << 31)) return fail(L2F_ERR_INVALID_ARGUMENT, "t must be < 2^31");
     env->t = t;
     return L2F_OK;
 }

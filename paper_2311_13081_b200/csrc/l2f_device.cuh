@@ -66,7 +66,9 @@ struct DevBufs {
     float* state;     // [17][N]
     float* dist;      // [6][N]
     float* dr;        // [5][N]
-    float* hist;      // [N_H][4][N]
+    float* hist;      // [N_H][4][N] ring: slot (tau mod N_H) = action applied at step tau
+    int32_t* hist_t0; // [N] first step of the current episode: ring entries with tau < hist_t0
+    float* hist_fill; // [4][N]   read as hist_fill (the episode's initial history, Q10)
     int32_t* ep_step; // [N]
     float* ep_return; // [N]
     double* slots;    // [n_slots][8] per-block statistics partials
@@ -342,15 +344,26 @@ __device__ __forceinline__ void transition(const DevParams& P, EnvReg& e, uint32
 
 __device__ __forceinline__ float uab(float a, float b, uint32_t x) { return fmaf(b - a, unif(x), a); }
 
-// Reset of one env from Philox counter `ctr` (Q17-Q19): state, disturbance,
-// DR factors, episode counters.  Returns the history fill value per rotor (Q10) in hfill.
-__device__ __forceinline__ void reset_env(const DevParams& P, EnvReg& e, uint32_t gid, uint32_t ctr,
-                                          float hfill[4])
+// Philox blocks of one reset (Q20): RESET 0..3 at slots 0..3, DIST 0..1 at slots 4..5,
+// DR 0..1 at slots 6..7 (fixed slots keep the block array in registers).
+__device__ __forceinline__ int reset_nblocks(const DevParams& P)
 {
-    const uint4 b0 = draw(P, gid, ctr, S_RESET, 0);
-    const uint4 b1 = draw(P, gid, ctr, S_RESET, 1);
-    const uint4 b2 = draw(P, gid, ctr, S_RESET, 2);
-    const uint4 b3 = draw(P, gid, ctr, S_RESET, 3);
+    return (P.flags & (F_DISTURBANCE | F_DOMAIN_RAND)) ? 8 : 4;
+}
+
+__device__ __forceinline__ uint4 reset_block(const DevParams& P, uint32_t gid, uint32_t ctr, int b)
+{
+    const uint32_t stream = b < 4 ? S_RESET : (b < 6 ? S_DIST : S_DR);
+    const uint32_t blk = (uint32_t)(b < 4 ? b : (b < 6 ? b - 4 : b - 6));
+    return draw(P, gid, ctr, stream, blk);
+}
+
+// Reset sampling from the drawn blocks (Q17-Q19): state, disturbance, DR
+// factors, episode counters; the history fill value per rotor (Q10) in hfill.
+__device__ __forceinline__ void reset_from_blocks(const DevParams& P, const uint4 (&blk)[8], EnvReg& e,
+                                                  float hfill[4])
+{
+    const uint4 b0 = blk[0], b1 = blk[1], b2 = blk[2], b3 = blk[3];
     e.s[0] = uab(-P.init_pos, P.init_pos, b0.x);
     e.s[1] = uab(-P.init_pos, P.init_pos, b0.y);
     e.s[2] = uab(-P.init_pos, P.init_pos, b0.z);
@@ -376,8 +389,7 @@ __device__ __forceinline__ void reset_env(const DevParams& P, EnvReg& e, uint32_
     e.s[15] = uab(P.init_rpm_lo, P.init_rpm_hi, b3.z);
     e.s[16] = uab(P.init_rpm_lo, P.init_rpm_hi, b3.w);
     if (P.flags & F_DISTURBANCE) {
-        const uint4 d0 = draw(P, gid, ctr, S_DIST, 0);
-        const uint4 d1 = draw(P, gid, ctr, S_DIST, 1);
+        const uint4 d0 = blk[4], d1 = blk[5];
         e.dist[0] = uab(-P.dist_force, P.dist_force, d0.x);
         e.dist[1] = uab(-P.dist_force, P.dist_force, d0.y);
         e.dist[2] = uab(-P.dist_force, P.dist_force, d0.z);
@@ -389,8 +401,7 @@ __device__ __forceinline__ void reset_env(const DevParams& P, EnvReg& e, uint32_
         for (int j = 0; j < 6; ++j) e.dist[j] = 0.0f;
     }
     if (P.flags & F_DOMAIN_RAND) {
-        const uint4 r0 = draw(P, gid, ctr, S_DR, 0);
-        const uint4 r1 = draw(P, gid, ctr, S_DR, 1);
+        const uint4 r0 = blk[6], r1 = blk[7];
         e.dr[0] = uab(P.dr_lo, P.dr_hi, r0.x);
         e.dr[1] = uab(P.dr_lo, P.dr_hi, r0.y);
         e.dr[2] = uab(P.dr_lo, P.dr_hi, r0.z);
@@ -404,6 +415,57 @@ __device__ __forceinline__ void reset_env(const DevParams& P, EnvReg& e, uint32_
     for (int i = 0; i < 4; ++i) hfill[i] = fmaf(e.s[13 + i] - P.rpm_min, P.inv_rpm_span2, -1.0f);
     e.ep_step = 0;
     e.ep_return = 0.0f;
+}
+
+// Reset of one env from Philox counter `ctr` (thread-local draws).
+__device__ __forceinline__ void reset_env(const DevParams& P, EnvReg& e, uint32_t gid, uint32_t ctr, float hfill[4])
+{
+    uint4 blk[8];
+    const int nb = reset_nblocks(P);
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+        if (b < nb) blk[b] = reset_block(P, gid, ctr, b);
+    reset_from_blocks(P, blk, e, hfill);
+}
+
+// Warp-cooperative reset (all 32 lanes must call; gids of a warp are consecutive): the Philox
+// blocks of every lane that needs a reset are drawn by all lanes in parallel and shuffled to
+// their owner, so a warp with k ending episodes pays ceil(k * nb / 32) Philox rounds instead
+// of nb serial ones.  Bitwise identical to reset_env (integer Philox, owner-lane sampling).
+__device__ __forceinline__ bool reset_env_warp(const DevParams& P, EnvReg& e, uint32_t gid, uint32_t ctr, bool need,
+                                               float hfill[4])
+{
+    const unsigned m = __ballot_sync(0xffffffffu, need);
+    if (m == 0u) return false;
+    const int lane = threadIdx.x & 31;
+    const int nb = reset_nblocks(P);
+    const int nr = __popc(m);
+    const int rank = __popc(m & ((1u << lane) - 1u));
+    uint4 blk[8];
+    for (int base = 0; base < nr * nb; base += 32) {
+        const int j = base + lane;
+        uint4 x = make_uint4(0u, 0u, 0u, 0u);
+        if (j < nr * nb) {
+            const int r = j / nb, b = j - r * nb;
+            const int src = (int)__fns(m, 0u, r + 1);
+            x = reset_block(P, gid - (uint32_t)lane + (uint32_t)src, ctr, b);
+        }
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            if (b < nb) {
+                const int sj = rank * nb + b - base;
+                const int sl = sj & 31;
+                uint4 v;
+                v.x = __shfl_sync(0xffffffffu, x.x, sl);
+                v.y = __shfl_sync(0xffffffffu, x.y, sl);
+                v.z = __shfl_sync(0xffffffffu, x.z, sl);
+                v.w = __shfl_sync(0xffffffffu, x.w, sl);
+                if (sj >= 0 && sj < 32) blk[b] = v;
+            }
+        }
+    }
+    if (need) reset_from_blocks(P, blk, e, hfill);
+    return need;
 }
 
 // Noisy core observation {p, R(q) row-major, v, w} (Q8); obs-noise normal i is
@@ -443,6 +505,22 @@ __device__ __forceinline__ void observe_core(const DevParams& P, const float* s,
             const int g = i < 3 ? 0 : (i < 12 ? 1 : (i < 15 ? 2 : 3));
             o[i] = fmaf(P.obs_sigma[g], z[i], o[i]);
         }
+    }
+}
+
+// Logical history entry H[k] (k-th most recent action, most recent first) at step t:
+// tau = t - 1 - k; ring slot (tau mod N_H) if tau >= hist_t0, else the episode's fill value.
+__device__ __forceinline__ void hist_entry(const DevBufs& B, int64_t N, int n_hist, int64_t i, int64_t t, int k,
+                                           int32_t t0, float h[4])
+{
+    const int64_t tau = t - 1 - k;
+    if (tau >= (int64_t)t0) {
+        const int slot = (int)(((tau % n_hist) + n_hist) % n_hist);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) h[c] = B.hist[((int64_t)slot * 4 + c) * N + i];
+    } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) h[c] = B.hist_fill[(int64_t)c * N + i];
     }
 }
 

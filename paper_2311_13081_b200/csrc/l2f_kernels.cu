@@ -30,6 +30,20 @@ __device__ __forceinline__ void load_env(const DevParams& P, const DevBufs& B, i
     e.ep_return = B.ep_return[i];
 }
 
+// Placeholder env for lanes past N: keeps warps convergent (shuffles, warp-cooperative reset).
+__device__ __forceinline__ void dummy_env(EnvReg& e)
+{
+#pragma unroll
+    for (int c = 0; c < kStateDim; ++c) e.s[c] = 0.0f;
+    e.s[3] = 1.0f;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) e.dist[c] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 5; ++c) e.dr[c] = 1.0f;
+    e.ep_step = 0;
+    e.ep_return = 0.0f;
+}
+
 __device__ __forceinline__ void store_state(const DevParams& P, const DevBufs& B, int64_t i, const EnvReg& e)
 {
     const int64_t N = P.n;
@@ -52,26 +66,31 @@ __device__ __forceinline__ void store_episode_consts(const DevParams& P, const D
     }
 }
 
-__device__ __forceinline__ void hist_fill(const DevParams& P, const DevBufs& B, int64_t i, const float h[4])
+// A new episode starting at step t0: O(1) bytes (marker + fill value), the ring itself is
+// overwritten lazily by the episode's own actions (Q10).
+__device__ __forceinline__ void hist_restart(const DevParams& P, const DevBufs& B, int64_t i, uint32_t t0,
+                                             const float h[4])
 {
     const int64_t N = P.n;
-    for (int k = 0; k < P.n_hist; ++k)
+    B.hist_t0[i] = (int32_t)t0;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) B.hist[((int64_t)k * 4 + c) * N + i] = h[c];
+    for (int c = 0; c < 4; ++c) B.hist_fill[(int64_t)c * N + i] = h[c];
 }
 
-// Dense actor observation row [18 + 4 N_H]: obs_core then H most-recent-first,
-// H[k] = ring[(t_last - k) mod N_H] where t_last is the step that wrote the newest slot.
+// Dense actor observation row [18 + 4 N_H]: obs_core then H most-recent-first at
+// step t_next (the step this observation feeds).
 __device__ __forceinline__ void write_dense(const DevParams& P, const DevBufs& B, int64_t i,
-                                           const float ob[kObsCore], uint32_t t_last, float* row)
+                                           const float ob[kObsCore], uint32_t t_next, float* row)
 {
     const int64_t N = P.n;
 #pragma unroll
     for (int j = 0; j < kObsCore; ++j) row[j] = ob[j];
+    const int32_t t0 = B.hist_t0[i];
     for (int k = 0; k < P.n_hist; ++k) {
-        const int slot = (int)(((int64_t)t_last - k) % P.n_hist + P.n_hist) % P.n_hist;
+        float h[4];
+        hist_entry(B, N, P.n_hist, i, (int64_t)t_next, k, t0, h);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) row[kObsCore + 4 * k + c] = B.hist[((int64_t)slot * 4 + c) * N + i];
+        for (int c = 0; c < 4; ++c) row[kObsCore + 4 * k + c] = h[c];
     }
 }
 
@@ -100,38 +119,40 @@ __global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, con
     const int64_t i = (int64_t)blockIdx.x * kStepBlock + threadIdx.x;
     const bool active = i < N;
     const uint32_t t = P.t0;
+    const uint32_t gid = P.id_offset + (uint32_t)i;
     StatAcc st;
     stat_zero(st);
+    EnvReg e;
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
     if (active) {
-        const uint32_t gid = P.id_offset + (uint32_t)i;
-        EnvReg e;
         load_env(P, B, i, e);
-        float a[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) a[c] = __ldg(act + c * N + i);
-        Trans o;
-        transition(P, e, gid, t, a, o);
-        uint32_t fl = o.flags;
-        if (O.final_state) {
+    } else {
+        dummy_env(e);
+    }
+    Trans o;
+    transition(P, e, gid, t, a, o);
+    uint32_t fl = o.flags;
+    if (active && O.final_state) {
 #pragma unroll
-            for (int c = 0; c < kStateDim; ++c) O.final_state[c * N + i] = e.s[c];
-        }
-        bool did_reset = false;
-        float hf[4];
-        if (fl & (D_TERM | D_TRUNC)) {
-            stat_episode(st, o);
-            if (P.flags & F_AUTO_RESET) {
-                reset_env(P, e, gid, t + 1, hf);
-                fl |= D_RESET;
-                did_reset = true;
-            } else {
-                e.ep_step = 0;
-                e.ep_return = 0.0f;
-            }
-        }
+        for (int c = 0; c < kStateDim; ++c) O.final_state[c * N + i] = e.s[c];
+    }
+    const bool ended = active && (fl & (D_TERM | D_TRUNC));
+    if (ended) stat_episode(st, o);
+    bool did_reset = false;
+    float hf[4];
+    if (P.flags & F_AUTO_RESET) {
+        did_reset = reset_env_warp(P, e, gid, t + 1, ended, hf);
+        if (did_reset) fl |= D_RESET;
+    } else if (ended) {
+        e.ep_step = 0;
+        e.ep_return = 0.0f;
+    }
+    if (active) {
         if (P.n_hist > 0) {
             if (did_reset) {
-                hist_fill(P, B, i, hf);
+                hist_restart(P, B, i, t + 1, hf);
             } else {
                 const int slot = (int)(t % (uint32_t)P.n_hist);
 #pragma unroll
@@ -147,7 +168,7 @@ __global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, con
 #pragma unroll
                 for (int j = 0; j < kObsCore; ++j) O.obs_core[j * N + i] = ob[j];
             }
-            if (O.obs_dense) write_dense(P, B, i, ob, t, O.obs_dense + i * (kObsCore + 4 * P.n_hist));
+            if (O.obs_dense) write_dense(P, B, i, ob, t + 1, O.obs_dense + i * (kObsCore + 4 * P.n_hist));
         }
         if (O.reward) O.reward[i] = o.reward;
         if (O.flags) O.flags[i] = (uint8_t)fl;
@@ -176,7 +197,7 @@ __global__ void __launch_bounds__(kStepBlock) reset_kernel(const DevParams P, co
     for (int c = 0; c < 6; ++c) B.dist[c * NN + i] = e.dist[c];
 #pragma unroll
     for (int c = 0; c < 5; ++c) B.dr[c * NN + i] = e.dr[c];
-    hist_fill(P, B, i, hf);
+    if (P.n_hist > 0) hist_restart(P, B, i, P.t0, hf);
     if (O.obs_core || O.obs_dense) {
         float ob[kObsCore];
         observe_core(P, e.s, gid, P.t0, ob);
@@ -204,66 +225,67 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
     const int64_t N = P.n;
     const int64_t i = (int64_t)blockIdx.x * kRolloutBlock + threadIdx.x;
     const bool active = i < N;
+    const uint32_t gid = P.id_offset + (uint32_t)i;
     StatAcc st;
     stat_zero(st);
-    if (active) {
-        const uint32_t gid = P.id_offset + (uint32_t)i;
-        int tslot = -1;
-        if (trace)
-            for (int k = 0; k < K; ++k)
-                if (trace_ids[k] == i) tslot = k;
-        EnvReg e;
+    int tslot = -1;
+    if (trace && active)
+        for (int k = 0; k < K; ++k)
+            if (trace_ids[k] == i) tslot = k;
+    EnvReg e;
+    if (active)
         load_env(P, B, i, e);
-        for (int32_t k = 0; k < T; ++k) {
-            const uint32_t t = P.t0 + (uint32_t)k;
-            float a[4];
-            if (act) {
+    else
+        dummy_env(e);
+    for (int32_t k = 0; k < T; ++k) {
+        const uint32_t t = P.t0 + (uint32_t)k;
+        float a[4];
+        if (act) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) a[c] = __ldg(act + ((int64_t)k * 4 + c) * N + i);
+            for (int c = 0; c < 4; ++c) a[c] = active ? __ldg(act + ((int64_t)k * 4 + c) * N + i) : 0.0f;
+        } else {
+            random_action(P, gid, t, a);
+        }
+        float* tr = (tslot >= 0) ? trace + ((int64_t)k * K + tslot) * kTraceFields : nullptr;
+        if (tr) {
+#pragma unroll
+            for (int c = 0; c < kStateDim; ++c) tr[c] = e.s[c];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tr[17 + c] = a[c];
+        }
+        Trans o;
+        transition(P, e, gid, t, a, o);
+        uint32_t fl = o.flags;
+        const bool ended = active && (fl & (D_TERM | D_TRUNC));
+        if (ended) stat_episode(st, o);
+        bool did_reset = false;
+        float hf[4];
+        if (P.flags & F_AUTO_RESET) {
+            did_reset = reset_env_warp(P, e, gid, t + 1, ended, hf);
+            if (did_reset) fl |= D_RESET;
+        } else if (ended) {
+            e.ep_step = 0;
+            e.ep_return = 0.0f;
+        }
+        if (active && P.n_hist > 0) {
+            if (did_reset) {
+                hist_restart(P, B, i, t + 1, hf);
             } else {
-                random_action(P, gid, t, a);
-            }
-            float* tr = (tslot >= 0) ? trace + ((int64_t)k * K + tslot) * kTraceFields : nullptr;
-            if (tr) {
+                const int slot = (int)(t % (uint32_t)P.n_hist);
 #pragma unroll
-                for (int c = 0; c < kStateDim; ++c) tr[c] = e.s[c];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) tr[17 + c] = a[c];
-            }
-            Trans o;
-            transition(P, e, gid, t, a, o);
-            uint32_t fl = o.flags;
-            bool did_reset = false;
-            float hf[4];
-            if (fl & (D_TERM | D_TRUNC)) {
-                stat_episode(st, o);
-                if (P.flags & F_AUTO_RESET) {
-                    reset_env(P, e, gid, t + 1, hf);
-                    fl |= D_RESET;
-                    did_reset = true;
-                } else {
-                    e.ep_step = 0;
-                    e.ep_return = 0.0f;
-                }
-            }
-            if (P.n_hist > 0) {
-                if (did_reset) {
-                    hist_fill(P, B, i, hf);
-                } else {
-                    const int slot = (int)(t % (uint32_t)P.n_hist);
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) B.hist[((int64_t)slot * 4 + c) * N + i] = o.a[c];
-                }
-            }
-            if (tr) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) tr[21 + c] = o.a[c];
-                tr[25] = o.reward;
-                tr[26] = (float)fl;
-                tr[27] = (float)e.ep_step;
-                tr[28] = tr[29] = tr[30] = tr[31] = 0.0f;
+                for (int c = 0; c < 4; ++c) B.hist[((int64_t)slot * 4 + c) * N + i] = o.a[c];
             }
         }
+        if (tr) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tr[21 + c] = o.a[c];
+            tr[25] = o.reward;
+            tr[26] = (float)fl;
+            tr[27] = (float)e.ep_step;
+            tr[28] = tr[29] = tr[30] = tr[31] = 0.0f;
+        }
+    }
+    if (active) {
         store_state(P, B, i, e);
         store_episode_consts(P, B, i, e);
     }

@@ -302,14 +302,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             e.ep_step = 0;
             e.ep_return = 0.0f;
         }
-        // history ring (HBM slot s holds a_tau with tau = s mod N_H) -> A1 position (-s) mod N_H
-        for (int s = 0; s < NH; ++s) {
-            float h[4] = {0.f, 0.f, 0.f, 0.f};
-            if (active)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) h[q] = B.hist[((int64_t)s * 4 + q) * N + i];
-            const int p = (NH - s) % NH;
-            tc::sts64(hist_addr(c, p), tc::pack_h2(h[0], h[1]), tc::pack_h2(h[2], h[3]));
+        // logical history at t0 (H[k] = a_{t0-1-k}, or the episode fill) -> A1 position (-tau) mod N_H
+        {
+            const int32_t h0 = active ? B.hist_t0[i] : 0;
+            for (int k = 0; k < NH; ++k) {
+                float h[4] = {0.f, 0.f, 0.f, 0.f};
+                if (active) hist_entry(B, N, NH, i, (int64_t)P.t0, k, h0, h);
+                const int64_t tau = (int64_t)P.t0 - 1 - k;
+                const int p = (int)(((-tau) % NH + NH) % NH);
+                tc::sts64(hist_addr(c, p), tc::pack_h2(h[0], h[1]), tc::pack_h2(h[2], h[3]));
+            }
         }
         int tslot = -1;
         if (trace && active)
@@ -334,18 +336,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             Trans o;
             transition(P, e, gid, t, a, o);
             uint32_t fl = o.flags;
+            const bool ended = (fl & (D_TERM | D_TRUNC)) != 0;
+            if (ended && active) stat_episode(st, o);
             bool did_reset = false;
             float hf[4];
-            if (fl & (D_TERM | D_TRUNC)) {
-                if (active) stat_episode(st, o);
-                if (P.flags & F_AUTO_RESET) {
-                    reset_env(P, e, gid, t + 1, hf);
-                    fl |= D_RESET;
-                    did_reset = true;
-                } else {
-                    e.ep_step = 0;
-                    e.ep_return = 0.0f;
-                }
+            if (P.flags & F_AUTO_RESET) {
+                did_reset = reset_env_warp(P, e, gid, t + 1, ended && active, hf);
+                if (did_reset) fl |= D_RESET;
+            }
+            if (ended && !did_reset) {
+                e.ep_step = 0;
+                e.ep_return = 0.0f;
             }
             if (NH > 0) {
                 if (did_reset) {
@@ -380,6 +381,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int q = 0; q < 5; ++q) B.dr[q * N + i] = e.dr[q];
             B.ep_step[i] = e.ep_step;
             B.ep_return[i] = e.ep_return;
+            // the ring now holds the full logical history: every entry valid
+            if (NH > 0) B.hist_t0[i] = (int32_t)(P.t0 + (uint32_t)T) - NH;
             for (int s = 0; s < NH; ++s) {
                 uint32_t h01, h23;
                 tc::lds64(hist_addr(c, (NH - s) % NH), h01, h23);

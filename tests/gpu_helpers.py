@@ -42,7 +42,7 @@ def close_obs(gpu_obs, ref_obs, s_prev):
 def snapshot(env) -> dict:
     torch.cuda.synchronize()
     return {k: getattr(env, k).detach().cpu().numpy().copy()
-            for k in ("state", "dist", "dr", "hist", "ep_step", "ep_return")}
+            for k in ("state", "dist", "dr", "hist", "hist_t0", "hist_fill", "ep_step", "ep_return")}
 
 
 def load_snapshot(env, snap: dict):
@@ -51,25 +51,30 @@ def load_snapshot(env, snap: dict):
     torch.cuda.synchronize()
 
 
+def logical_hist(snap: dict, i: int, t_next: int, n_hist: int) -> np.ndarray:
+    """Most-recent-first history H[k] of env i when the next step is t_next (include/l2f.h):
+    tau = t_next - 1 - k; ring slot (tau mod N_H) if tau >= hist_t0 else hist_fill."""
+    out = np.zeros((n_hist, 4))
+    t0 = int(snap["hist_t0"][i])
+    for k in range(n_hist):
+        tau = t_next - 1 - k
+        out[k] = snap["hist"][tau % n_hist, :, i] if tau >= t0 else snap["hist_fill"][:, i]
+    return out
+
+
 def to_oracle(snap: dict, idx, t: int, n_hist: int) -> np.ndarray:
-    """GPU SoA (ring slot tau mod N_H holds a_tau) -> oracle records (H[k] = a_{t-1-k})."""
+    """GPU SoA workspace -> oracle records (H[k] = a_{t-1-k}, most recent first)."""
     idx = np.asarray(idx)
     E = oracle.new_envs(len(idx))
     for j, i in enumerate(idx):
         E[j]["s"] = snap["state"][:, i]
         E[j]["dist"] = snap["dist"][:, i]
         E[j]["dr"] = snap["dr"][:, i]
-        for k in range(n_hist):
-            slot = (t - 1 - k) % n_hist
-            E[j]["hist"][k] = snap["hist"][slot, :, i]
+        if n_hist:
+            E[j]["hist"][:n_hist] = logical_hist(snap, i, t, n_hist)
         E[j]["ep_step"] = snap["ep_step"][i]
         E[j]["ep_return"] = snap["ep_return"][i]
     return E
-
-
-def ring_to_mrf(hist_ring: np.ndarray, i: int, t_next: int, n_hist: int) -> np.ndarray:
-    """Most-recent-first history of env i when the next step is t_next."""
-    return np.array([hist_ring[(t_next - 1 - k) % n_hist, :, i] for k in range(n_hist)])
 
 
 def near_threshold(so, cfg, extra: float = 0.0) -> bool:

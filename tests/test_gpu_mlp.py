@@ -11,7 +11,7 @@ import torch
 
 import inputs
 import oracle
-from gpu_helpers import close, close_step, snapshot
+from gpu_helpers import close, close_step, logical_hist, snapshot
 
 pytestmark = pytest.mark.gpu
 
@@ -83,7 +83,7 @@ def _teacher_forced(pkg, cfg, n, T, K, t0=0, seed=7, check_every=1):
         e = oracle.new_envs(1)
         e[0]["dist"] = snap0["dist"][:, i]
         e[0]["dr"] = snap0["dr"][:, i]
-        H = [snap0["hist"][(t0 - 1 - k) % nh, :, i] for k in range(nh)]
+        H = list(logical_hist(snap0, i, t0, nh)) if nh else []
         ep = int(snap0["ep_step"][i])
         ret = float(snap0["ep_return"][i])
         for k in range(T):
@@ -159,6 +159,7 @@ def test_mlp_rollout_history_writeback_and_continuation(pkg):
     ids = np.arange(0, n, 37)
     tr = env.rollout(50, policy=pol, trace_ids=torch.as_tensor(ids)).cpu().numpy()
     after = snapshot(env)
+    assert np.all(after["hist_t0"] == 50 - nh)
     for j, i in enumerate(ids):
         fl = tr[:, j, 26].astype(int)
         last_reset = max([k for k in range(50) if fl[k] & 8], default=-1)

@@ -13,7 +13,7 @@ import torch
 
 import inputs
 import oracle
-from gpu_helpers import close, close_obs, close_step, load_snapshot, near_threshold, ring_to_mrf, snapshot, to_oracle
+from gpu_helpers import close, close_obs, close_step, load_snapshot, logical_hist, near_threshold, snapshot, to_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -64,8 +64,9 @@ def test_reset_matches_oracle(pkg, flags):
         assert np.all(close(snap["state"][j], E["s"][:, j])), j
     assert np.all(close(snap["dist"], E["dist"].T))
     assert np.all(close(snap["dr"], E["dr"].T))
-    for k in range(cfg["n_hist"]):
-        assert np.all(close(snap["hist"][k], E["hist"][:, k, :].T))
+    for i in range(0, n, 7):
+        assert np.all(close(logical_hist(snap, i, 0, cfg["n_hist"]), E[i]["hist"][:cfg["n_hist"]]))
+    assert np.all(snap["hist_t0"] == 0)
     assert np.all(snap["ep_step"] == 0) and np.all(snap["ep_return"] == 0)
     obs = out["obs_core"].cpu().numpy()
     dense = out["obs_dense"].cpu().numpy()
@@ -95,7 +96,8 @@ def test_single_step_parity(pkg, flags):
     env.reset()
     rs = inputs.random_states(n, seed=21)
     snap = {"state": rs["state"], "dist": rs["dist"], "dr": rs["dr"] if flags & inputs.DOMAIN_RAND else np.ones((5, n)),
-            "hist": rs["hist"], "ep_step": rs["ep_step"], "ep_return": rs["ep_return"]}
+            "hist": rs["hist"], "hist_t0": np.full(n, -(1 << 30), dtype=np.int32), "hist_fill": np.zeros((4, n)),
+            "ep_step": rs["ep_step"], "ep_return": rs["ep_return"]}
     load_snapshot(env, snap)
     snap = snapshot(env)  # fp32-rounded inputs, shared by both sides
     env.t = t
@@ -131,7 +133,7 @@ def test_single_step_parity(pkg, flags):
         assert np.all(close_obs(dense[i][:18], ob[:18], sp)), i
         assert np.all(close(dense[i][18:], ob[18:])), i
         # history ring: slot t mod N_H holds a'_t unless the env was reset (filled)
-        H = ring_to_mrf(after["hist"], i, t + 1, cfg["n_hist"])
+        H = logical_hist(after, i, t + 1, cfg["n_hist"])
         assert np.all(close(H, e[0]["hist"][:cfg["n_hist"]])), i
     assert n_excl < n // 100
 
@@ -333,7 +335,7 @@ def test_edge_sizes_and_history_lengths(pkg, n, nh):
         sp = snap["state"][:, i]
         assert np.all(close_step(out["final_state"].cpu().numpy()[:, i], so.final_s, sp))
         if nh:
-            H = ring_to_mrf(after["hist"], i, 6, nh)
+            H = logical_hist(after, i, 6, nh)
             assert np.all(close(H, e[0]["hist"][:nh]))
         ob = oracle.observe(cfg, e[0], i, 6)
         sp2 = e[0]["s"] if so.flags & oracle.FLAG_RESET else sp
