@@ -123,29 +123,34 @@ def dist_setup(args):
     return world, rank, local
 
 
-def cpu_baseline(cfg, policy_w, target_s=12.0, nthreads=None):
-    """The oracle as it stands (FP64 C, std::thread-style pthreads over all host cores) on a
-    bounded sample of the same workload: n_s envs x T_s steps of the fused MLP env step."""
+def cpu_baseline(cfg, policy_w, target_s=15.0, nthreads=None):
+    """The oracle as it stands (FP64 C, pthreads over all host cores) on a bounded sample of the
+    same workload: n_s envs (ids spread over the GPU's shard) x T_s fused MLP env-steps, with
+    n_s sized from a short probe so the sample costs about target_s seconds."""
     import numpy as np
 
     import oracle
 
     nthreads = nthreads or os.cpu_count() or 1
     pol = oracle.PolicyHandle(policy_w)
-    n_s = max(nthreads * 8, 64)
-    ids = np.arange(n_s, dtype=np.uint64) * 997
+    n_p = nthreads * 4
+    ids = np.arange(n_p, dtype=np.uint64) * 997
     E = oracle.reset_many(cfg, ids, 0)
     t0 = time.perf_counter()
-    oracle.rollout(cfg, E.copy(), ids, 0, 4, oracle.MODE_POLICY, policy=pol, nthreads=nthreads)
-    probe = time.perf_counter() - t0
-    T_s = int(max(4, min(1000, target_s / max(probe / 4, 1e-6))))
+    oracle.rollout(cfg, E, ids, 0, 20, oracle.MODE_POLICY, policy=pol, nthreads=nthreads)
+    rate = n_p * 20 / max(time.perf_counter() - t0, 1e-6)
+    T_s = 250
+    n_s = int(max(nthreads, min(1 << 16, target_s * rate / T_s)))
+    n_s -= n_s % nthreads if n_s >= nthreads else 0
+    ids = (np.arange(n_s, dtype=np.uint64) * ((ENVS_PER_GPU // max(n_s, 1)) or 1)).astype(np.uint64)
+    E = oracle.reset_many(cfg, ids, 0)
     t0 = time.perf_counter()
     oracle.rollout(cfg, E, ids, 0, T_s, oracle.MODE_POLICY, policy=pol, nthreads=nthreads)
     el = time.perf_counter() - t0
     v = n_s * T_s / el
     return {"value": v, "unit": "env-steps/s", "cores": nthreads, "kind": "oracle",
-            "sample": f"{n_s} envs (ids spread over the workload) x {T_s} fused MLP env-steps, FP64 C oracle, "
-                      f"{el:.1f} s wall"}
+            "sample": f"{n_s} envs (ids spread over the 2^21-env shard) x {T_s} fused MLP env-steps of the "
+                      f"C5 workload, FP64 C oracle on {nthreads} threads, {el:.1f} s wall"}
 
 
 def reference_arm(args):
@@ -198,6 +203,7 @@ def main():
 
     import inputs
     import paper_2311_13081_b200 as pkg
+    from paper_2311_13081_b200 import dist as l2fdist
 
     world, rank, local = dist_setup(args)
     torch.cuda.set_device(local)
@@ -211,7 +217,8 @@ def main():
 
     cfg = inputs.config_c5()
     W = inputs.policy_weights(18 + 4 * cfg["n_hist"], 64, seed=7, out_bias=inputs.hover_policy_bias())
-    env = pkg.Env(cfg, n, env_id_offset=rank * n, device=dev)
+    offset, n = l2fdist.shard(rank, world, n)  # weak scaling: rank r owns ids [r n, (r+1) n)
+    env = pkg.Env(cfg, n, env_id_offset=offset, device=dev)
     env.reset()
     pol = pkg.Policy(W, device=dev)
     stats_buf = torch.zeros(8, dtype=torch.float64, device=dev)
@@ -222,8 +229,7 @@ def main():
         else:
             env.rollout(T)  # open loop, Philox random actions
         st = env.episode_stats(reset=True)
-        if world > 1:
-            dist.all_reduce(st)
+        l2fdist.allreduce_stats(st)  # a15: NCCL SUM of the FP64 episode statistics
         stats_buf.add_(st)
 
     def barrier():
@@ -246,10 +252,7 @@ def main():
         barrier()
     launches = pkg.launch_count() - l0
     ms = ev0.elapsed_time(ev1)
-    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms_max = float(t_max.item())
+    ms_max = l2fdist.max_over_ranks(ms, dev)
     env_steps = world * n * T * args.steps
     value = env_steps / (ms_max / 1e3)
     stats = stats_buf.cpu().numpy()
@@ -279,7 +282,7 @@ def main():
     # ---- e2e through the public host-buffer API: H2D of the policy (pinned), rollout, D2H stats
     e2e_val, h2d = None, 0
     if args.mode == "mlp":
-        e2e_val, h2d = e2e_rollout(args, pkg, torch, dist, env, W, T, n, world, dev, stream, barrier)
+        e2e_val, h2d = e2e_rollout(args, pkg, torch, l2fdist, env, W, T, n, world, dev, stream, barrier)
     modes = {}
     if not args.no_secondary and rank == 0:
         modes = secondary(pkg, inputs, torch, dev, pk, f_clk)
@@ -316,7 +319,7 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_rollout(args, pkg, torch, dist, env, W, T, n, world, dev, stream, barrier):
+def e2e_rollout(args, pkg, torch, l2fdist, env, W, T, n, world, dev, stream, barrier):
     hpol = pkg.HostPolicy(W)
     h_stats = torch.zeros(8, dtype=torch.float64).pin_memory()
     h2d = sum(int(t.numel()) * 2 for t in hpol.t.values())
@@ -330,14 +333,11 @@ def e2e_rollout(args, pkg, torch, dist, env, W, T, n, world, dev, stream, barrie
     for _ in range(args.steps):
         e2e_env.rollout_host(hpol, T, h_stats)
         if world > 1:
-            st = torch.from_numpy(h_stats.numpy().copy()).to(dev)
-            dist.all_reduce(st)
+            l2fdist.allreduce_stats(torch.from_numpy(h_stats.numpy().copy()).to(dev))
     ev5.record(stream)
     barrier()
-    e2e_ms = torch.tensor([ev4.elapsed_time(ev5)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_val = world * n * T * args.steps / (float(e2e_ms.item()) / 1e3)
+    e2e_ms = l2fdist.max_over_ranks(ev4.elapsed_time(ev5), dev)
+    e2e_val = world * n * T * args.steps / (e2e_ms / 1e3)
 
     return e2e_val, h2d
 

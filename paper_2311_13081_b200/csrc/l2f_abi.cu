@@ -175,6 +175,10 @@ DevParams make_base(const l2f_config& c)
     std::memset(&P, 0, sizeof(P));
     P.key0 = (uint32_t)c.seed;
     P.key1 = (uint32_t)(c.seed >> 32);
+    for (int r = 0; r < 10; ++r) {  // Philox4x32-10 key schedule (Weyl constants)
+        P.rk0[r] = P.key0 + (uint32_t)r * 0x9E3779B9u;
+        P.rk1[r] = P.key1 + (uint32_t)r * 0xBB67AE85u;
+    }
     P.flags = c.flags;
     P.n_hist = c.action_history;
     P.max_ep = c.max_episode_steps;
@@ -215,7 +219,6 @@ DevParams make_base(const l2f_config& c)
     P.term_pos = (float)c.term_pos;
     P.term_vel2 = (float)(c.term_vel * c.term_vel);
     P.term_angvel2 = (float)(c.term_angvel * c.term_angvel);
-    P.interval = c.curriculum.interval;
     return P;
 }
 
@@ -224,6 +227,7 @@ bool params_for(const l2f_env* e, uint64_t t0, int64_t T, DevParams& P)
 {
     P = e->base;
     P.t0 = (uint32_t)t0;
+    P.hist_slot0 = e->cfg.action_history > 0 ? (int32_t)(t0 % (uint64_t)e->cfg.action_history) : 0;
     const int64_t I = e->cfg.curriculum.interval;
     int64_t k0 = 0, k1 = 0;
     if (I > 0) {
@@ -231,9 +235,11 @@ bool params_for(const l2f_env* e, uint64_t t0, int64_t T, DevParams& P)
         k1 = (int64_t)((t0 + (uint64_t)(T > 0 ? T - 1 : 0)) / (uint64_t)I);
     }
     if (k1 - k0 + 1 > kMaxStages) return false;
-    P.stage_first = k0;
     P.n_stages = (int32_t)(k1 - k0 + 1);
-    for (int64_t k = k0; k <= k1; ++k) P.stage[k - k0] = stage_weights(e->cfg, k);
+    for (int64_t k = k0; k <= k1; ++k) {
+        P.stage[k - k0] = stage_weights(e->cfg, k);
+        P.stage_end[k - k0] = (uint32_t)((k + 1) * (I > 0 ? I : 0));  // stage k covers [k I, (k+1) I)
+    }
     return true;
 }
 

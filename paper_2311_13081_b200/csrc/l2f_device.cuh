@@ -37,8 +37,10 @@ struct StageW {
 // Launch-uniform parameters, passed by value (constant bank) to every kernel.
 struct DevParams {
     uint32_t key0, key1;       // Philox key = seed (Q20)
+    uint32_t rk0[10], rk1[10]; // Philox4x32-10 round keys (key + r * Weyl constants)
     uint32_t flags;
     int32_t n_hist;
+    int32_t hist_slot0;        // t0 mod N_H (0 when N_H = 0)
     int32_t max_ep;
     uint32_t id_offset;        // global env id of local env 0
     int64_t n;                 // envs
@@ -54,10 +56,10 @@ struct DevParams {
     // observation noise (Q8), termination (Q14)
     float obs_sigma[4];
     float term_pos, term_vel2, term_angvel2;
-    // curriculum slice covering [t0, t0 + T): stage of step t = stage_base + floor(t/interval)
-    int64_t interval;          // 0 = single stage
-    int64_t stage_first;       // global stage index of stage[0]
+    // curriculum slice covering [t0, t0 + T): stage[j] holds the weights of steps
+    // [stage_end[j-1], stage_end[j]); host-computed, so the kernel only compares step indices
     int32_t n_stages;
+    uint32_t stage_end[kMaxStages];
     StageW stage[kMaxStages];
 };
 
@@ -106,16 +108,35 @@ __device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, u
     return make_uint4(c0, c1, c2, c3);
 }
 
+// Same rounds with the 10 round keys precomputed on the host (DevParams.rk): the key
+// schedule is launch-uniform, so each round is 2 IMAD.WIDE + 2 LOP3 with constant-bank keys.
+__device__ __forceinline__ uint4 philox_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                           const uint32_t (&rk0)[10], const uint32_t (&rk1)[10])
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        c0 = hi1 ^ c1 ^ rk0[r];
+        c2 = hi0 ^ c3 ^ rk1[r];
+        c1 = lo1;
+        c3 = lo0;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
 __device__ __forceinline__ uint4 draw(const DevParams& P, uint32_t gid, uint32_t t,
                                       uint32_t stream, uint32_t block)
 {
-    return philox(gid, t, stream, block, P.key0, P.key1);
+    return philox_rk(gid, t, stream, block, P.rk0, P.rk1);
 }
 
-// u = (2 (x >> 9) + 1) 2^-24, exact in fp32 (Q20)
+// u = (2 (x >> 9) + 1) 2^-24 = ((x >> 9) + 1/2) 2^-23, exact in fp32 (Q20).  Built from the
+// bits: 1 + (x >> 9) 2^-23 is the float with exponent 0 and mantissa x >> 9; subtracting
+// 1 - 2^-24 is exact (Sterbenz), so no int->float conversion is needed.
 __device__ __forceinline__ float unif(uint32_t x)
 {
-    return __uint2float_rn(((x >> 9) << 1) | 1u) * 5.9604644775390625e-08f;
+    return __uint_as_float(0x3F800000u | (x >> 9)) - 0.99999994039535522f;
 }
 
 // ln(u) for u in (0,1): log1p series near 1 (where MUFU.LG2's absolute error would swamp
@@ -148,10 +169,7 @@ __device__ __forceinline__ void box_muller(uint32_t xa, uint32_t xb, float& z0, 
 __device__ __forceinline__ const StageW& stage_of(const DevParams& P, uint32_t t)
 {
     int k = 0;
-    if (P.interval > 0) {
-        long long g = (long long)(t / (uint64_t)P.interval) - P.stage_first;
-        k = (int)min(max(g, 0ll), (long long)(P.n_stages - 1));
-    }
+    for (int j = 0; j + 1 < P.n_stages; ++j) k += (t >= P.stage_end[j]) ? 1 : 0;
     return P.stage[k];
 }
 
@@ -162,6 +180,7 @@ struct Phys {
     float c0, c1, c2;       // thrust coefficients x DR thrust scale
     float inv_m;
     float Jx, Jy, Jz, iJx, iJy, iJz;
+    float dJzy, dJxz, dJyx; // Jz - Jy, Jx - Jz, Jy - Jx (gyroscopic term)
     float u_tm[4];          // setpoint / T_m
 };
 
@@ -185,6 +204,9 @@ __device__ __forceinline__ void make_phys(const DevParams& P, const EnvReg& e, c
         ph.Jy = P.J[1];
         ph.Jz = P.J[2];
     }
+    ph.dJzy = ph.Jz - ph.Jy;
+    ph.dJxz = ph.Jx - ph.Jz;
+    ph.dJyx = ph.Jy - ph.Jx;
     ph.iJx = __fdividef(1.0f, ph.Jx);
     ph.iJy = __fdividef(1.0f, ph.Jy);
     ph.iJz = __fdividef(1.0f, ph.Jz);
@@ -227,9 +249,9 @@ __device__ __forceinline__ void deriv(const DevParams& P, const Phys& ph, const 
     ds[8] = fmaf(r12, T, d[1]) * ph.inv_m;
     ds[9] = fmaf(fmaf(r22, T, d[2]), ph.inv_m, -P.gravity);
     // Euler: J w' = tau - w x (J w)
-    const float cx = (ph.Jz - ph.Jy) * (wy * wz);
-    const float cy = (ph.Jx - ph.Jz) * (wz * wx);
-    const float cz = (ph.Jy - ph.Jx) * (wx * wy);
+    const float cx = ph.dJzy * (wy * wz);
+    const float cy = ph.dJxz * (wz * wx);
+    const float cz = ph.dJyx * (wx * wy);
     ds[10] = (tx - cx) * ph.iJx;
     ds[11] = (ty - cy) * ph.iJy;
     ds[12] = (tz - cz) * ph.iJz;
@@ -267,9 +289,12 @@ __device__ __forceinline__ bool rk4_step(const DevParams& P, const Phys& ph, con
     const float inv = rsqrtf(n2);
 #pragma unroll
     for (int i = 3; i < 7; ++i) s[i] *= inv;
-    bool bad = false;
+    // any NaN/Inf component makes the sum non-finite (finite overflow to inf also counts as
+    // diverged, |x| > 1e38 is divergence in any sense)
+    float sum = 0.0f;
 #pragma unroll
-    for (int i = 0; i < kStateDim; ++i) bad |= !isfinite(s[i]);
+    for (int i = 0; i < kStateDim; ++i) sum += s[i];
+    const bool bad = !isfinite(sum);
 #pragma unroll
     for (int i = 13; i < 17; ++i) s[i] = fminf(fmaxf(s[i], P.rpm_min), P.rpm_max);
     return bad;
@@ -289,17 +314,22 @@ struct Trans {
 // One env transition s_t -> s_{t+1}: exploration noise + clip (Q7),
 // action map, RK4 dynamics, reward on s' (Q12), termination (Q14),
 // truncation (Q15).  Episode counters are advanced; the caller handles history and reset.
-__device__ __forceinline__ void transition(const DevParams& P, EnvReg& e, uint32_t gid, uint32_t t,
-                                           const float a_in[4], Trans& o)
+// Exploration-noise normals of step t (stream ACT, Q20); zeros when the feature is off.
+__device__ __forceinline__ void action_noise(const DevParams& P, uint32_t gid, uint32_t t, float z[4])
 {
-    const StageW& W = stage_of(P, t);
-    float z[4] = {0.f, 0.f, 0.f, 0.f};
-    const bool act_noise = (P.flags & F_ACTION_NOISE) != 0;
-    if (act_noise) {
+    z[0] = z[1] = z[2] = z[3] = 0.0f;
+    if (P.flags & F_ACTION_NOISE) {
         const uint4 x = draw(P, gid, t, S_ACT, 0);
         box_muller(x.x, x.y, z[0], z[1]);
         box_muller(x.z, x.w, z[2], z[3]);
     }
+}
+
+__device__ __forceinline__ void transition(const DevParams& P, EnvReg& e, uint32_t gid, uint32_t t,
+                                           const float a_in[4], const float z[4], Trans& o)
+{
+    const StageW& W = stage_of(P, t);
+    const bool act_noise = (P.flags & F_ACTION_NOISE) != 0;
     float u[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -425,20 +455,22 @@ __device__ __forceinline__ void reset_env(const DevParams& P, EnvReg& e, uint32_
 #pragma unroll
     for (int b = 0; b < 8; ++b)
         if (b < nb) blk[b] = reset_block(P, gid, ctr, b);
-    reset_from_blocks(P, blk, e, hfill);
+    reset_from_blocks(P, blk, e, hfill);  // unused DIST/DR slots are ignored
 }
 
 // Warp-cooperative reset (all 32 lanes must call; gids of a warp are consecutive): the Philox
-// blocks of every lane that needs a reset are drawn by all lanes in parallel and shuffled to
-// their owner, so a warp with k ending episodes pays ceil(k * nb / 32) Philox rounds instead
-// of nb serial ones.  Bitwise identical to reset_env (integer Philox, owner-lane sampling).
+// blocks of every lane that needs a reset are drawn by all lanes in parallel and handed to
+// their owner through a 32-entry shared-memory scratch of the warp, so a warp with k ending
+// episodes pays ceil(k * nb / 32) Philox rounds instead of nb serial ones.  Bitwise identical
+// to reset_env (integer Philox, owner-lane sampling).
 __device__ __forceinline__ bool reset_env_warp(const DevParams& P, EnvReg& e, uint32_t gid, uint32_t ctr, bool need,
-                                               float hfill[4])
+                                               float hfill[4], uint4* scratch)
 {
     const unsigned m = __ballot_sync(0xffffffffu, need);
     if (m == 0u) return false;
     const int lane = threadIdx.x & 31;
-    const int nb = reset_nblocks(P);
+    const int lnb = (P.flags & (F_DISTURBANCE | F_DOMAIN_RAND)) ? 3 : 2;  // log2(reset_nblocks)
+    const int nb = 1 << lnb;
     const int nr = __popc(m);
     const int rank = __popc(m & ((1u << lane) - 1u));
     uint4 blk[8];
@@ -446,32 +478,50 @@ __device__ __forceinline__ bool reset_env_warp(const DevParams& P, EnvReg& e, ui
         const int j = base + lane;
         uint4 x = make_uint4(0u, 0u, 0u, 0u);
         if (j < nr * nb) {
-            const int r = j / nb, b = j - r * nb;
-            const int src = (int)__fns(m, 0u, r + 1);
-            x = reset_block(P, gid - (uint32_t)lane + (uint32_t)src, ctr, b);
+            const int r = j >> lnb, b = j & (nb - 1);
+            const bool used = b < 4 || (b < 6 && (P.flags & F_DISTURBANCE)) || (b >= 6 && (P.flags & F_DOMAIN_RAND));
+            // lane of the r-th resetting env: walk the (few) set bits of m
+            int src = 0;
+            unsigned mm = m;
+            for (int q = 0; q <= r; ++q) {
+                src = __ffs(mm) - 1;
+                mm &= mm - 1u;
+            }
+            if (used) x = reset_block(P, gid - (uint32_t)lane + (uint32_t)src, ctr, b);
         }
+        __syncwarp();
+        scratch[lane] = x;
+        __syncwarp();
+        if (need) {
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            if (b < nb) {
+            for (int b = 0; b < 8; ++b) {
                 const int sj = rank * nb + b - base;
-                const int sl = sj & 31;
-                uint4 v;
-                v.x = __shfl_sync(0xffffffffu, x.x, sl);
-                v.y = __shfl_sync(0xffffffffu, x.y, sl);
-                v.z = __shfl_sync(0xffffffffu, x.z, sl);
-                v.w = __shfl_sync(0xffffffffu, x.w, sl);
-                if (sj >= 0 && sj < 32) blk[b] = v;
+                if (b < nb && sj >= 0 && sj < 32) blk[b] = scratch[sj];
             }
         }
     }
+    __syncwarp();
     if (need) reset_from_blocks(P, blk, e, hfill);
     return need;
 }
 
-// Noisy core observation {p, R(q) row-major, v, w} (Q8); obs-noise normal i is
-// normal (i mod 4) of Philox block floor(i/4) of stream OBS at counter t (Q20).
-__device__ __forceinline__ void observe_core(const DevParams& P, const float* s, uint32_t gid,
-                                             uint32_t t, float o[kObsCore])
+// Observation-noise normal i in [0,18) is normal (i mod 4) of Philox block floor(i/4) of
+// stream OBS at counter t (Q20).  Blocks [b0, b1) only, so callers can spread the work.
+__device__ __forceinline__ void obs_noise_blocks(const DevParams& P, uint32_t gid, uint32_t t, int b0, int b1,
+                                                 float z[20])
+{
+#pragma unroll
+    for (int b = 0; b < 5; ++b) {
+        if (b < b0 || b >= b1) continue;
+        const uint4 x = draw(P, gid, t, S_OBS, (uint32_t)b);
+        box_muller(x.x, x.y, z[4 * b], z[4 * b + 1]);
+        if (b < 4) box_muller(x.z, x.w, z[4 * b + 2], z[4 * b + 3]);
+    }
+}
+
+// Noisy core observation {p, R(q) row-major, v, w} (Q8) from given normals.
+__device__ __forceinline__ void observe_core_z(const DevParams& P, const float* s, const float z[20],
+                                               float o[kObsCore])
 {
     const float qw = s[3], qx = s[4], qy = s[5], qz = s[6];
     o[0] = s[0];
@@ -493,19 +543,20 @@ __device__ __forceinline__ void observe_core(const DevParams& P, const float* s,
     o[16] = s[11];
     o[17] = s[12];
     if (P.flags & F_OBS_NOISE) {
-        float z[20];
-#pragma unroll
-        for (int b = 0; b < 5; ++b) {
-            const uint4 x = draw(P, gid, t, S_OBS, (uint32_t)b);
-            box_muller(x.x, x.y, z[4 * b], z[4 * b + 1]);
-            if (b < 4) box_muller(x.z, x.w, z[4 * b + 2], z[4 * b + 3]);
-        }
 #pragma unroll
         for (int i = 0; i < kObsCore; ++i) {
             const int g = i < 3 ? 0 : (i < 12 ? 1 : (i < 15 ? 2 : 3));
             o[i] = fmaf(P.obs_sigma[g], z[i], o[i]);
         }
     }
+}
+
+__device__ __forceinline__ void observe_core(const DevParams& P, const float* s, uint32_t gid, uint32_t t,
+                                             float o[kObsCore])
+{
+    float z[20];
+    if (P.flags & F_OBS_NOISE) obs_noise_blocks(P, gid, t, 0, 5, z);
+    observe_core_z(P, s, z, o);
 }
 
 // Logical history entry H[k] (k-th most recent action, most recent first) at step t:

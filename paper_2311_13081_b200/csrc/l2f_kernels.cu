@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, con
                                                           const float* __restrict__ act, const StepOutDev O)
 {
     __shared__ double srow[(kStepBlock / 32) * kStatsLen];
+    __shared__ uint4 rscratch[kStepBlock];  // 32 entries per warp for the cooperative reset
     const int64_t N = P.n;
     const int64_t i = (int64_t)blockIdx.x * kStepBlock + threadIdx.x;
     const bool active = i < N;
@@ -132,7 +133,9 @@ __global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, con
         dummy_env(e);
     }
     Trans o;
-    transition(P, e, gid, t, a, o);
+    float za[4];
+    action_noise(P, gid, t, za);
+    transition(P, e, gid, t, a, za, o);
     uint32_t fl = o.flags;
     if (active && O.final_state) {
 #pragma unroll
@@ -143,7 +146,7 @@ __global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, con
     bool did_reset = false;
     float hf[4];
     if (P.flags & F_AUTO_RESET) {
-        did_reset = reset_env_warp(P, e, gid, t + 1, ended, hf);
+        did_reset = reset_env_warp(P, e, gid, t + 1, ended, hf, rscratch + (threadIdx.x & ~31));
         if (did_reset) fl |= D_RESET;
     } else if (ended) {
         e.ep_step = 0;
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, con
             if (did_reset) {
                 hist_restart(P, B, i, t + 1, hf);
             } else {
-                const int slot = (int)(t % (uint32_t)P.n_hist);
+                const int slot = P.hist_slot0;  // t0 mod N_H
 #pragma unroll
                 for (int c = 0; c < 4; ++c) B.hist[((int64_t)slot * 4 + c) * N + i] = o.a[c];
             }
@@ -222,6 +225,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
                                                                      int32_t K)
 {
     __shared__ double srow[(kRolloutBlock / 32) * kStatsLen];
+    __shared__ uint4 rscratch[kRolloutBlock];
     const int64_t N = P.n;
     const int64_t i = (int64_t)blockIdx.x * kRolloutBlock + threadIdx.x;
     const bool active = i < N;
@@ -237,6 +241,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
         load_env(P, B, i, e);
     else
         dummy_env(e);
+    int slot = P.hist_slot0;  // (t mod N_H), advanced incrementally
     for (int32_t k = 0; k < T; ++k) {
         const uint32_t t = P.t0 + (uint32_t)k;
         float a[4];
@@ -254,14 +259,16 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
             for (int c = 0; c < 4; ++c) tr[17 + c] = a[c];
         }
         Trans o;
-        transition(P, e, gid, t, a, o);
+        float za[4];
+        action_noise(P, gid, t, za);
+        transition(P, e, gid, t, a, za, o);
         uint32_t fl = o.flags;
         const bool ended = active && (fl & (D_TERM | D_TRUNC));
         if (ended) stat_episode(st, o);
         bool did_reset = false;
         float hf[4];
         if (P.flags & F_AUTO_RESET) {
-            did_reset = reset_env_warp(P, e, gid, t + 1, ended, hf);
+            did_reset = reset_env_warp(P, e, gid, t + 1, ended, hf, rscratch + (threadIdx.x & ~31));
             if (did_reset) fl |= D_RESET;
         } else if (ended) {
             e.ep_step = 0;
@@ -271,11 +278,11 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
             if (did_reset) {
                 hist_restart(P, B, i, t + 1, hf);
             } else {
-                const int slot = (int)(t % (uint32_t)P.n_hist);
 #pragma unroll
                 for (int c = 0; c < 4; ++c) B.hist[((int64_t)slot * 4 + c) * N + i] = o.a[c];
             }
         }
+        if (++slot == P.n_hist) slot = 0;
         if (tr) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) tr[21 + c] = o.a[c];
@@ -329,7 +336,13 @@ __global__ void philox_selftest_kernel(int64_t n, uint32_t k0, uint32_t k1, uint
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t c0 = (uint32_t)i, c2 = (uint32_t)(i % 7), c3 = (uint32_t)(i % 5);
-    ours[i] = philox(c0, t, c2, c3, k0, k1);
+    uint32_t rk0[10], rk1[10];  // the same key schedule the host packs into DevParams
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        rk0[r] = k0 + (uint32_t)r * 0x9E3779B9u;
+        rk1[r] = k1 + (uint32_t)r * 0xBB67AE85u;
+    }
+    ours[i] = philox_rk(c0, t, c2, c3, rk0, rk1);
     ref[i] = curand_Philox4x32_10(make_uint4(c0, t, c2, c3), make_uint2(k0, k1));
 }
 

@@ -50,10 +50,13 @@ constexpr uint32_t OFF_W3 = OFF_W2 + kW2Bytes;
 constexpr uint32_t OFF_ONES = OFF_W3 + kW3Bytes;
 constexpr uint32_t OFF_BAR = OFF_ONES + kOnesBytes;   // kTiles mbarriers
 constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * kTiles;
-constexpr uint32_t OFF_STAT = OFF_TMEM + 8;           // (kThreads/32) x 8 doubles
-constexpr uint32_t kSmemBytes = OFF_STAT + (kThreads / 32) * kStatsLen * 8;
+constexpr uint32_t OFF_STAT = OFF_TMEM + 8;           // reset scratch (32 uint4 per warp); reused by stats
+constexpr uint32_t kScratchBytes = (kThreads / 32) * 32 * 16;
+static_assert(kScratchBytes >= (kThreads / 32) * kStatsLen * 8, "stats rows fit in the scratch");
+constexpr uint32_t kSmemBytes = OFF_STAT + kScratchBytes;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
-constexpr uint32_t kTmemCols = 256;  // kTiles x 64, power of two
+constexpr uint32_t kTmemCols = 512;  // accumulators: kTiles x 64 columns from 0; noise stash: 32 per tile from 256
+constexpr uint32_t kStashCol = 256;
 
 constexpr uint32_t kIdescN64 = tc::make_idesc(128, 64, 0, 0);
 constexpr uint32_t kIdescN64BMN = tc::make_idesc(128, 64, 0, 1);
@@ -113,6 +116,7 @@ struct TileCtx {
     uint32_t mbar;
     uint32_t tmem_row;        // TMEM address of (this thread's lane, tile column 0)
     uint32_t tmem_tile;       // TMEM address of (lane 0, tile column 0)
+    uint32_t stash_row;       // TMEM address of this thread's 32-column noise stash
     uint32_t bar_id;
     uint32_t phase;
     bool leader;
@@ -147,9 +151,17 @@ __device__ __forceinline__ void wait_mma(TileCtx& c)
     tc::fence_after();
 }
 
+struct NoHook {
+    __device__ __forceinline__ void operator()(int) const {}
+};
+
 // The three layers on the tensor core for one tile.  Precondition: A1 rows written by all 128
-// threads.  `rot` = rotation of the history ring (W1 history row offset in slots).
-__device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist, uint32_t rot, float a[4])
+// threads.  `rot` = rotation of the history ring (W1 history row offset in slots).  hook(l) runs
+// on every thread right after layer l's MMAs were issued, i.e. inside the MMA latency (used to
+// draw the next step's noise).
+template <class Hook>
+__device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist, uint32_t rot, float a[4],
+                                         const Hook& hook)
 {
     const uint32_t hk = 4u * (uint32_t)n_hist;
     handoff_to_mma(c);
@@ -166,6 +178,7 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
                         kIdescN64BMN, 1);
         tc::commit(c.mbar);
     }
+    hook(1);
     wait_mma(c);
     epilogue_hidden(c);
     handoff_to_mma(c);
@@ -179,6 +192,7 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
                     tc::make_desc(sbase + OFF_W2 + 8 * (kHid * 16), kHid * 16, 128), kIdescN64, 1);
         tc::commit(c.mbar);
     }
+    hook(2);
     wait_mma(c);
     epilogue_hidden(c);
     handoff_to_mma(c);
@@ -192,6 +206,7 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
                     tc::make_desc(sbase + OFF_W3 + 8 * 256, 256, 128), kIdescN16, 1);
         tc::commit(c.mbar);
     }
+    hook(3);
     wait_mma(c);
     uint32_t v[4];
     tc::tmem_ld4(c.tmem_row, v);
@@ -199,6 +214,41 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
     tc::fence_before();
 #pragma unroll
     for (int j = 0; j < 4; ++j) a[j] = tanh_fast(__uint_as_float(v[j]));
+}
+
+// Observation-noise normals of one step, stashed per thread in TMEM (columns 0..17 of the
+// thread's stash) so they can be drawn inside the previous step's MMA latency without
+// holding registers across the RK4.
+__device__ __forceinline__ void stash_obs_noise(const DevParams& P, const TileCtx& c, uint32_t gid, uint32_t t,
+                                                int part)
+{
+    float z[20];
+    if (part == 0 || part == 3) {
+        obs_noise_blocks(P, gid, t, 0, 2, z);
+        tc::tmem_st8(c.stash_row + 0, z, 0);
+    }
+    if (part == 1 || part == 3) {
+        obs_noise_blocks(P, gid, t, 2, 4, z);
+        tc::tmem_st8(c.stash_row + 8, z, 8);
+    }
+    if (part == 2 || part == 3) {
+        obs_noise_blocks(P, gid, t, 4, 5, z);
+        tc::tmem_st2(c.stash_row + 16, z[16], z[17]);
+    }
+}
+
+__device__ __forceinline__ void load_obs_noise(const TileCtx& c, float z[20])
+{
+    uint32_t v[16], w[4];
+    tc::tmem_wait_st();
+    tc::tmem_ld16(c.stash_row, v);
+    tc::tmem_ld4(c.stash_row + 16, w);
+    tc::tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) z[j] = __uint_as_float(v[j]);
+    z[16] = __uint_as_float(w[0]);
+    z[17] = __uint_as_float(w[1]);
+    z[18] = z[19] = 0.0f;
 }
 
 __device__ __forceinline__ void write_obs_row(const TileCtx& c, const float o[kObsCore])
@@ -243,6 +293,7 @@ __device__ __forceinline__ TileCtx make_ctx(uint32_t sbase)
     c.mbar = sbase + OFF_BAR + 8 * g;
     c.tmem_tile = tbase + 64 * g;
     c.tmem_row = c.tmem_tile + ((uint32_t)(32 * (r / 32)) << 16);
+    c.stash_row = tbase + kStashCol + 32 * g + ((uint32_t)(32 * (r / 32)) << 16);
     c.bar_id = 1 + g;
     c.phase = 0;
     c.leader = (r == 0);
@@ -318,14 +369,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int q = 0; q < K; ++q)
                 if (trace_ids[q] == i) tslot = q;
 
+        const bool obs_noise = (P.flags & F_OBS_NOISE) != 0;
+        if (obs_noise) stash_obs_noise(P, c, gid, P.t0, 3);
+        // ring rotation (t - 1) mod N_H and write position (-t) mod N_H, advanced incrementally
+        uint32_t rot = NH > 0 ? (P.t0 + (uint32_t)NH - 1u) % (uint32_t)NH : 0u;
+        int wpos = NH > 0 ? (int)(((uint32_t)NH - P.t0 % (uint32_t)NH) % (uint32_t)NH) : 0;
         for (int32_t k = 0; k < T; ++k) {
             const uint32_t t = P.t0 + (uint32_t)k;
             float ob[kObsCore];
-            observe_core(P, e.s, gid, t, ob);
+            {
+                float z[20];
+                if (obs_noise) load_obs_noise(c, z);
+                observe_core_z(P, e.s, z, ob);
+            }
             write_obs_row(c, ob);
-            float a[4];
-            const uint32_t rot = NH > 0 ? (t + (uint32_t)NH - 1u) % (uint32_t)NH : 0u;
-            mlp_tile(c, sbase, NH, rot, a);
+            float a[4], za[4];
+            mlp_tile(c, sbase, NH, rot, a, [&](int l) {
+                if (l == 1) action_noise(P, gid, t, za);
+                if (obs_noise) stash_obs_noise(P, c, gid, t + 1, l - 1);
+            });
+            if (NH > 0 && ++rot == (uint32_t)NH) rot = 0;
             float* tr = (tslot >= 0) ? trace + ((int64_t)k * K + tslot) * kTraceFields : nullptr;
             if (tr) {
 #pragma unroll
@@ -334,14 +397,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int q = 0; q < 4; ++q) tr[17 + q] = a[q];
             }
             Trans o;
-            transition(P, e, gid, t, a, o);
+            transition(P, e, gid, t, a, za, o);
             uint32_t fl = o.flags;
             const bool ended = (fl & (D_TERM | D_TRUNC)) != 0;
             if (ended && active) stat_episode(st, o);
             bool did_reset = false;
             float hf[4];
             if (P.flags & F_AUTO_RESET) {
-                did_reset = reset_env_warp(P, e, gid, t + 1, ended && active, hf);
+                did_reset = reset_env_warp(P, e, gid, t + 1, ended && active, hf,
+                                           reinterpret_cast<uint4*>(smem + OFF_STAT) + (threadIdx.x & ~31));
                 if (did_reset) fl |= D_RESET;
             }
             if (ended && !did_reset) {
@@ -349,17 +413,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                 e.ep_return = 0.0f;
             }
             if (NH > 0) {
-                if (did_reset) {
+                if (!did_reset)
+                    tc::sts64(hist_addr(c, wpos), tc::pack_h2(o.a[0], o.a[1]), tc::pack_h2(o.a[2], o.a[3]));
+                if (--wpos < 0) wpos = NH - 1;
+                // new episodes: the whole history row takes the fill value (Q10); the N_H/2
+                // 16-byte chunks of each resetting lane's row are written by N_H/2 lanes at once
+                unsigned rm = __ballot_sync(0xffffffffu, did_reset);
+                if (rm) {
                     const uint32_t h01 = tc::pack_h2(hf[0], hf[1]), h23 = tc::pack_h2(hf[2], hf[3]);
-                    for (int p = 0; p < NH; p += 2) {
-                        if (p + 1 < NH)
-                            tc::sts128(hist_addr(c, p), h01, h23, h01, h23);
-                        else
-                            tc::sts64(hist_addr(c, p), h01, h23);
+                    const int lane = threadIdx.x & 31;
+                    while (rm) {
+                        const int src = __ffs(rm) - 1;
+                        rm &= rm - 1u;
+                        const uint32_t v01 = __shfl_sync(0xffffffffu, h01, src);
+                        const uint32_t v23 = __shfl_sync(0xffffffffu, h23, src);
+                        if (lane < NH / 2)
+                            tc::sts128(c.a1_row + (uint32_t)(src - lane) * 16u + (4 + lane) * kChunkA, v01, v23,
+                                       v01, v23);
                     }
-                } else {
-                    const int p = (int)((uint32_t)NH - t % (uint32_t)NH) % NH;
-                    tc::sts64(hist_addr(c, p), tc::pack_h2(o.a[0], o.a[1]), tc::pack_h2(o.a[2], o.a[3]));
                 }
             }
             if (tr) {
@@ -398,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // statistics: warp -> fixed-order block sum -> this CTA's slot
     double* srow = reinterpret_cast<double*>(smem + OFF_STAT);
     const int warp = threadIdx.x >> 5;
+    __syncthreads();  // the reset scratch is reused for the statistics rows
     stat_warp_to_smem(st, srow + warp * kStatsLen);
     double sd = steps_done;
 #pragma unroll
@@ -443,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::sts64(hist_addr(c, p), tc::pack_h2(h[0], h[1]), tc::pack_h2(h[2], h[3]));
         }
         float a[4];
-        mlp_tile(c, sbase, NH, 0u, a);
+        mlp_tile(c, sbase, NH, 0u, a, NoHook{});
         if (active)
 #pragma unroll
             for (int q = 0; q < 4; ++q) act[i * 4 + q] = a[q];

@@ -113,6 +113,20 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4])
                  : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// 32 lanes x 32-bit stores of consecutive columns (thread t -> its own lane).
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v, int off)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+                 "f"(v[off + 0]), "f"(v[off + 1]), "f"(v[off + 2]), "f"(v[off + 3]), "f"(v[off + 4]),
+                 "f"(v[off + 5]), "f"(v[off + 6]), "f"(v[off + 7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, float a, float b)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "f"(a), "f"(b) : "memory");
+}
 
 __device__ __forceinline__ void sts128(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
 {
@@ -132,12 +146,13 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi)
     __half2 h = __floats2half2_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&h);
 }
-// relu on two packed fp32 accumulators -> packed fp16 (relu commutes with RNE rounding)
+// relu on two fp32 accumulators -> packed fp16 in one cvt (relu commutes with RNE rounding);
+// a goes to the low half (lower K index).
 __device__ __forceinline__ uint32_t relu_pack(uint32_t a, uint32_t b)
 {
-    __half2 h = __floats2half2_rn(__uint_as_float(a), __uint_as_float(b));
-    h = __hmax2(h, __float2half2_rn(0.0f));
-    return *reinterpret_cast<uint32_t*>(&h);
+    uint32_t d;
+    asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(d) : "r"(b), "r"(a));
+    return d;
 }
 
 }  // namespace tc
