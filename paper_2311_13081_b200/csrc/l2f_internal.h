@@ -6,7 +6,7 @@
 
 namespace l2f {
 
-constexpr int kStepBlock = 256;
+constexpr int kStepBlock = 128;
 constexpr int kRolloutBlock = 128;
 
 struct StepOutDev {

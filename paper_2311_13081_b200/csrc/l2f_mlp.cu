@@ -48,9 +48,9 @@ constexpr uint32_t OFF_W1H = OFF_W1O + kW1oBytes;
 constexpr uint32_t OFF_W2 = OFF_W1H + kW1hBytes;
 constexpr uint32_t OFF_W3 = OFF_W2 + kW2Bytes;
 constexpr uint32_t OFF_ONES = OFF_W3 + kW3Bytes;
-constexpr uint32_t OFF_BAR = OFF_ONES + kOnesBytes;   // kTiles mbarriers
+constexpr uint32_t OFF_BAR = OFF_ONES + kOnesBytes;   // kTiles MMA-done mbarriers
 constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * kTiles;
-constexpr uint32_t OFF_STAT = OFF_TMEM + 8;           // reset scratch (32 uint4 per warp); reused by stats
+constexpr uint32_t OFF_STAT = (OFF_TMEM + 8 + 127) & ~127u;  // reset scratch (32 uint4 per warp); reused by stats
 constexpr uint32_t kScratchBytes = (kThreads / 32) * 32 * 16;
 static_assert(kScratchBytes >= (kThreads / 32) * kStatsLen * 8, "stats rows fit in the scratch");
 constexpr uint32_t kSmemBytes = OFF_STAT + kScratchBytes;
@@ -137,7 +137,11 @@ __device__ __forceinline__ void epilogue_hidden(const TileCtx& c)
     }
 }
 
-__device__ __forceinline__ void handoff_to_mma(const TileCtx& c)
+// The tile's 128 threads hand their freshly written A rows (and finished TMEM reads) to the
+// MMA issuer: proxy fence + tcgen05 fence + a 128-thread named barrier (id 1 + tile).  (An
+// mbarrier arrive/wait variant that lets early warps run ahead measured slower: the waiting
+// warps then spin instead of sleeping at the barrier.)
+__device__ __forceinline__ void handoff_to_mma(TileCtx& c)
 {
     tc::fence_proxy_async();
     tc::fence_before();
@@ -270,7 +274,7 @@ __device__ void setup_cta(const PolicyDev& W, uint32_t sbase, int n_hist)
 {
     stage_weights(W, sbase, n_hist);
     if (threadIdx.x == 0) {
-        for (int g = 0; g < kTiles; ++g) tc::mbar_init(sbase + OFF_BAR + 8 * g, 1);
+        for (int g = 0; g < kTiles; ++g) tc::mbar_init(sbase + OFF_BAR + 8 * g, 1);  // MMA done
         tc::fence_mbar_init();
     }
     if (threadIdx.x < 32) tc::tmem_alloc(sbase + OFF_TMEM, kTmemCols);

@@ -68,6 +68,11 @@ __device__ __forceinline__ void fence_mbar_init()
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar_saddr)
+{
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(mbar_saddr) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint32_t mbar_saddr, uint32_t parity)
 {
     asm volatile(
