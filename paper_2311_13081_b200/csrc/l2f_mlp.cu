@@ -30,6 +30,8 @@ constexpr int kTiles = 3;
 constexpr int kM = 128;
 constexpr int kThreads = kTiles * kM;
 constexpr int kHid = 64;
+// Hidden activations (A operand of layers 2 and 3) in TMEM instead of shared memory.
+constexpr bool kA2InTmem = true;
 
 // shared-memory map (bytes)
 constexpr uint32_t kChunkA = kM * 16;                 // one 8-wide K chunk of a 128-row A tile
@@ -43,7 +45,7 @@ constexpr uint32_t kOnesBytes = 2 * kChunkA;          // A K16 slice: column 0 =
 
 constexpr uint32_t OFF_A1 = 0;
 constexpr uint32_t OFF_A2 = OFF_A1 + kTiles * kA1Bytes;
-constexpr uint32_t OFF_W1O = OFF_A2 + kTiles * kA2Bytes;
+constexpr uint32_t OFF_W1O = OFF_A2 + (kA2InTmem ? 0u : kTiles * kA2Bytes);
 constexpr uint32_t OFF_W1H = OFF_W1O + kW1oBytes;
 constexpr uint32_t OFF_W2 = OFF_W1H + kW1hBytes;
 constexpr uint32_t OFF_W3 = OFF_W2 + kW2Bytes;
@@ -57,6 +59,7 @@ constexpr uint32_t kSmemBytes = OFF_STAT + kScratchBytes;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 constexpr uint32_t kTmemCols = 512;  // accumulators: kTiles x 64 columns from 0; noise stash: 32 per tile from 256
 constexpr uint32_t kStashCol = 256;
+constexpr uint32_t kA2Col = 384;  // TMEM A2 (h1/h2 as fp16, 32 columns + 8 with the ones column) per tile: 40 columns
 
 constexpr uint32_t kIdescN64 = tc::make_idesc(128, 64, 0, 0);
 constexpr uint32_t kIdescN64BMN = tc::make_idesc(128, 64, 0, 1);
@@ -117,23 +120,38 @@ struct TileCtx {
     uint32_t tmem_row;        // TMEM address of (this thread's lane, tile column 0)
     uint32_t tmem_tile;       // TMEM address of (lane 0, tile column 0)
     uint32_t stash_row;       // TMEM address of this thread's 32-column noise stash
+    uint32_t a2_tmem;         // TMEM address of (lane 0, this tile's A2 column 0)
+    uint32_t a2_trow;         // ... of this thread's lane
     uint32_t bar_id;
     uint32_t phase;
     bool leader;
 };
 
-// Epilogue of L1 / L2: accumulator row -> relu -> fp16 -> A2 row.
+// Epilogue of L1 / L2: accumulator row -> relu -> fp16 -> A2 row (TMEM or shared memory).
 __device__ __forceinline__ void epilogue_hidden(const TileCtx& c)
 {
+    if constexpr (kA2InTmem) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        uint32_t v[16];
-        tc::tmem_ld16(c.tmem_row + 16 * q, v);
-        tc::tmem_wait_ld();
-        tc::sts128(c.a2_row + (2 * q) * kChunkA, tc::relu_pack(v[0], v[1]), tc::relu_pack(v[2], v[3]),
-                   tc::relu_pack(v[4], v[5]), tc::relu_pack(v[6], v[7]));
-        tc::sts128(c.a2_row + (2 * q + 1) * kChunkA, tc::relu_pack(v[8], v[9]), tc::relu_pack(v[10], v[11]),
-                   tc::relu_pack(v[12], v[13]), tc::relu_pack(v[14], v[15]));
+        for (int q = 0; q < 4; ++q) {
+            uint32_t v[16];
+            tc::tmem_ld16(c.tmem_row + 16 * q, v);
+            tc::tmem_wait_ld();
+            tc::tmem_st8u(c.a2_trow + 8 * q, tc::relu_pack(v[0], v[1]), tc::relu_pack(v[2], v[3]),
+                          tc::relu_pack(v[4], v[5]), tc::relu_pack(v[6], v[7]), tc::relu_pack(v[8], v[9]),
+                          tc::relu_pack(v[10], v[11]), tc::relu_pack(v[12], v[13]), tc::relu_pack(v[14], v[15]));
+        }
+        tc::tmem_wait_st();
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t v[16];
+            tc::tmem_ld16(c.tmem_row + 16 * q, v);
+            tc::tmem_wait_ld();
+            tc::sts128(c.a2_row + (2 * q) * kChunkA, tc::relu_pack(v[0], v[1]), tc::relu_pack(v[2], v[3]),
+                       tc::relu_pack(v[4], v[5]), tc::relu_pack(v[6], v[7]));
+            tc::sts128(c.a2_row + (2 * q + 1) * kChunkA, tc::relu_pack(v[8], v[9]), tc::relu_pack(v[10], v[11]),
+                       tc::relu_pack(v[12], v[13]), tc::relu_pack(v[14], v[15]));
+        }
     }
 }
 
@@ -188,12 +206,19 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
     handoff_to_mma(c);
     if (c.leader) {
         tc::fence_after();
+        if constexpr (kA2InTmem) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            tc::mma_f16(c.tmem_tile, tc::make_desc(c.a2 + 2 * j * kChunkA, kChunkA, 128),
-                        tc::make_desc(sbase + OFF_W2 + 2 * j * (kHid * 16), kHid * 16, 128), kIdescN64, j);
-        tc::mma_f16(c.tmem_tile, tc::make_desc(sbase + OFF_ONES, kChunkA, 128),
-                    tc::make_desc(sbase + OFF_W2 + 8 * (kHid * 16), kHid * 16, 128), kIdescN64, 1);
+            for (int j = 0; j < 5; ++j)  // j = 4: the ones column (bias row of W2)
+                tc::mma_f16_ts(c.tmem_tile, c.a2_tmem + 8 * j,
+                               tc::make_desc(sbase + OFF_W2 + 2 * j * (kHid * 16), kHid * 16, 128), kIdescN64, j);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                tc::mma_f16(c.tmem_tile, tc::make_desc(c.a2 + 2 * j * kChunkA, kChunkA, 128),
+                            tc::make_desc(sbase + OFF_W2 + 2 * j * (kHid * 16), kHid * 16, 128), kIdescN64, j);
+            tc::mma_f16(c.tmem_tile, tc::make_desc(sbase + OFF_ONES, kChunkA, 128),
+                        tc::make_desc(sbase + OFF_W2 + 8 * (kHid * 16), kHid * 16, 128), kIdescN64, 1);
+        }
         tc::commit(c.mbar);
     }
     hook(2);
@@ -202,12 +227,19 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
     handoff_to_mma(c);
     if (c.leader) {
         tc::fence_after();
+        if constexpr (kA2InTmem) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            tc::mma_f16(c.tmem_tile, tc::make_desc(c.a2 + 2 * j * kChunkA, kChunkA, 128),
-                        tc::make_desc(sbase + OFF_W3 + 2 * j * 256, 256, 128), kIdescN16, j);
-        tc::mma_f16(c.tmem_tile, tc::make_desc(sbase + OFF_ONES, kChunkA, 128),
-                    tc::make_desc(sbase + OFF_W3 + 8 * 256, 256, 128), kIdescN16, 1);
+            for (int j = 0; j < 5; ++j)
+                tc::mma_f16_ts(c.tmem_tile, c.a2_tmem + 8 * j, tc::make_desc(sbase + OFF_W3 + 2 * j * 256, 256, 128),
+                               kIdescN16, j);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                tc::mma_f16(c.tmem_tile, tc::make_desc(c.a2 + 2 * j * kChunkA, kChunkA, 128),
+                            tc::make_desc(sbase + OFF_W3 + 2 * j * 256, 256, 128), kIdescN16, j);
+            tc::mma_f16(c.tmem_tile, tc::make_desc(sbase + OFF_ONES, kChunkA, 128),
+                        tc::make_desc(sbase + OFF_W3 + 8 * 256, 256, 128), kIdescN16, 1);
+        }
         tc::commit(c.mbar);
     }
     hook(3);
@@ -298,6 +330,12 @@ __device__ __forceinline__ TileCtx make_ctx(uint32_t sbase)
     c.tmem_tile = tbase + 64 * g;
     c.tmem_row = c.tmem_tile + ((uint32_t)(32 * (r / 32)) << 16);
     c.stash_row = tbase + kStashCol + 32 * g + ((uint32_t)(32 * (r / 32)) << 16);
+    c.a2_tmem = tbase + kA2Col + 40 * g;
+    c.a2_trow = c.a2_tmem + ((uint32_t)(32 * (r / 32)) << 16);
+    if constexpr (kA2InTmem) {  // constant ones column (K index 64 of layers 2 and 3) + zero pad
+        tc::tmem_st8u(c.a2_trow + 32, 0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u);
+        tc::tmem_wait_st();
+    }
     c.bar_id = 1 + g;
     c.phase = 0;
     c.leader = (r == 0);
