@@ -194,6 +194,11 @@ DevParams make_base(const l2f_config& c)
         P.c[j] = (float)p.thrust_c[j];
     }
     P.ctau = (float)p.torque_c;
+    P.inv_mass = (float)(1.0 / p.mass);
+    for (int j = 0; j < 3; ++j) P.iJ[j] = (float)(1.0 / p.J[j]);
+    P.dJ[0] = (float)p.J[2] - (float)p.J[1];  // same fp32 arithmetic as the DR path
+    P.dJ[1] = (float)p.J[0] - (float)p.J[2];
+    P.dJ[2] = (float)p.J[1] - (float)p.J[0];
     P.inv_tm = (float)(1.0 / p.motor_tau);
     P.rpm_min = (float)p.rpm_min;
     P.rpm_max = (float)p.rpm_max;

@@ -50,6 +50,7 @@ struct DevParams {
     // nominal parameters; DR factors scale mass, J, thrust coefficients (Q19)
     float mass, J[3], c[3], ctau, inv_tm, rpm_min, rpm_max, gravity, rpm_half_span, inv_rpm_span2;
     float rx[4], ry[4], spin[4];
+    float inv_mass, iJ[3], dJ[3];  // nominal 1/m, 1/J_ii, (Jz-Jy, Jx-Jz, Jy-Jx): DR-free fast path
     // reset distribution (Q17-Q19)
     float init_pos, init_angle, init_vel, init_angvel, init_rpm_lo, init_rpm_hi;
     float dist_force, dist_torque, dr_lo, dr_hi;
@@ -173,6 +174,12 @@ __device__ __forceinline__ const StageW& stage_of(const DevParams& P, uint32_t t
     return P.stage[k];
 }
 
+// Last step (exclusive) of launch stage sg when the launch covers [t0, t0 + T).
+__device__ __forceinline__ uint32_t stage_stop(const DevParams& P, int sg, uint32_t t_last)
+{
+    return (sg + 1 < P.n_stages) ? min(P.stage_end[sg], t_last) : t_last;
+}
+
 // ---------------------------------------------------------------------------------------
 // Dynamics: per-step constants of one env, then f(s).
 // ---------------------------------------------------------------------------------------
@@ -184,10 +191,10 @@ struct Phys {
     float u_tm[4];          // setpoint / T_m
 };
 
-__device__ __forceinline__ void make_phys(const DevParams& P, const EnvReg& e, const float u[4],
-                                          bool dr_on, Phys& ph)
+template <bool kDR>
+__device__ __forceinline__ void make_phys(const DevParams& P, const EnvReg& e, const float u[4], Phys& ph)
 {
-    if (dr_on) {
+    if constexpr (kDR) {
         ph.c0 = P.c[0] * e.dr[4];
         ph.c1 = P.c[1] * e.dr[4];
         ph.c2 = P.c[2] * e.dr[4];
@@ -195,21 +202,27 @@ __device__ __forceinline__ void make_phys(const DevParams& P, const EnvReg& e, c
         ph.Jx = P.J[0] * e.dr[1];
         ph.Jy = P.J[1] * e.dr[2];
         ph.Jz = P.J[2] * e.dr[3];
-    } else {
+        ph.dJzy = ph.Jz - ph.Jy;
+        ph.dJxz = ph.Jx - ph.Jz;
+        ph.dJyx = ph.Jy - ph.Jx;
+        ph.iJx = __fdividef(1.0f, ph.Jx);
+        ph.iJy = __fdividef(1.0f, ph.Jy);
+        ph.iJz = __fdividef(1.0f, ph.Jz);
+    } else {  // launch-uniform constants (constant-bank operands, no registers)
         ph.c0 = P.c[0];
         ph.c1 = P.c[1];
         ph.c2 = P.c[2];
-        ph.inv_m = __fdividef(1.0f, P.mass);
+        ph.inv_m = P.inv_mass;
         ph.Jx = P.J[0];
         ph.Jy = P.J[1];
         ph.Jz = P.J[2];
+        ph.dJzy = P.dJ[0];
+        ph.dJxz = P.dJ[1];
+        ph.dJyx = P.dJ[2];
+        ph.iJx = P.iJ[0];
+        ph.iJy = P.iJ[1];
+        ph.iJz = P.iJ[2];
     }
-    ph.dJzy = ph.Jz - ph.Jy;
-    ph.dJxz = ph.Jx - ph.Jz;
-    ph.dJyx = ph.Jy - ph.Jx;
-    ph.iJx = __fdividef(1.0f, ph.Jx);
-    ph.iJy = __fdividef(1.0f, ph.Jy);
-    ph.iJz = __fdividef(1.0f, ph.Jz);
 #pragma unroll
     for (int i = 0; i < 4; ++i) ph.u_tm[i] = u[i] * P.inv_tm;
 }
@@ -325,10 +338,13 @@ __device__ __forceinline__ void action_noise(const DevParams& P, uint32_t gid, u
     }
 }
 
-__device__ __forceinline__ void transition(const DevParams& P, EnvReg& e, uint32_t gid, uint32_t t,
-                                           const float a_in[4], const float z[4], Trans& o)
+// W: the curriculum stage of step t (stage_of), hoisted by the callers' stage loops.
+// kDR: per-env domain-randomised parameters (compile-time so the DR-free path keeps the
+// nominal parameters in the constant bank instead of registers).
+template <bool kDR>
+__device__ __forceinline__ void transition(const DevParams& P, const StageW& W, EnvReg& e, uint32_t gid,
+                                           uint32_t t, const float a_in[4], const float z[4], Trans& o)
 {
-    const StageW& W = stage_of(P, t);
     const bool act_noise = (P.flags & F_ACTION_NOISE) != 0;
     float u[4];
 #pragma unroll
@@ -338,7 +354,7 @@ __device__ __forceinline__ void transition(const DevParams& P, EnvReg& e, uint32
         u[i] = fmaf(o.a[i] + 1.0f, P.rpm_half_span, P.rpm_min);
     }
     Phys ph;
-    make_phys(P, e, u, (P.flags & F_DOMAIN_RAND) != 0, ph);
+    make_phys<kDR>(P, e, u, ph);
     const bool div = rk4_step(P, ph, e.dist, e.s);
 
     const float* s = e.s;

@@ -12,6 +12,7 @@
 
 namespace l2f {
 
+template <bool kDR>
 __device__ __forceinline__ void load_env(const DevParams& P, const DevBufs& B, int64_t i, EnvReg& e)
 {
     const int64_t N = P.n;
@@ -19,7 +20,7 @@ __device__ __forceinline__ void load_env(const DevParams& P, const DevBufs& B, i
     for (int c = 0; c < kStateDim; ++c) e.s[c] = B.state[c * N + i];
 #pragma unroll
     for (int c = 0; c < 6; ++c) e.dist[c] = B.dist[c * N + i];
-    if (P.flags & F_DOMAIN_RAND) {
+    if (kDR) {
 #pragma unroll
         for (int c = 0; c < 5; ++c) e.dr[c] = B.dr[c * N + i];
     } else {
@@ -111,6 +112,7 @@ __device__ __forceinline__ void stats_block_end(const StatAcc& st, double* srow,
 // ---------------------------------------------------------------------------------------
 // l2f_step: one transition for every env.
 // ---------------------------------------------------------------------------------------
+template <bool kDR>
 __global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, const DevBufs B,
                                                           const float* __restrict__ act, const StepOutDev O)
 {
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, con
     EnvReg e;
     float a[4] = {0.f, 0.f, 0.f, 0.f};
     if (active) {
-        load_env(P, B, i, e);
+        load_env<kDR>(P, B, i, e);
 #pragma unroll
         for (int c = 0; c < 4; ++c) a[c] = __ldg(act + c * N + i);
     } else {
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, con
     Trans o;
     float za[4];
     action_noise(P, gid, t, za);
-    transition(P, e, gid, t, a, za, o);
+    transition<kDR>(P, stage_of(P, t), e, gid, t, a, za, o);
     uint32_t fl = o.flags;
     if (active && O.final_state) {
 #pragma unroll
@@ -218,6 +220,7 @@ __global__ void __launch_bounds__(kStepBlock) reset_kernel(const DevParams P, co
 // Open-loop fused rollout: T transitions with the state in registers (N3).  Actions from a
 // [T][4][N] buffer or the Philox RAND_ACT stream.  The history ring stays in HBM.
 // ---------------------------------------------------------------------------------------
+template <bool kDR>
 __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevParams P, const DevBufs B,
                                                                      const float* __restrict__ act, int32_t T,
                                                                      float* __restrict__ trace,
@@ -238,12 +241,16 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
             if (trace_ids[k] == i) tslot = k;
     EnvReg e;
     if (active)
-        load_env(P, B, i, e);
+        load_env<kDR>(P, B, i, e);
     else
         dummy_env(e);
     int slot = P.hist_slot0;  // (t mod N_H), advanced incrementally
-    for (int32_t k = 0; k < T; ++k) {
-        const uint32_t t = P.t0 + (uint32_t)k;
+    const uint32_t t_last = P.t0 + (uint32_t)T;
+    uint32_t t = P.t0;
+    for (int sg = 0; sg < P.n_stages; ++sg) {  // curriculum stages of this launch
+    const StageW& W = P.stage[sg];
+    for (const uint32_t t_stop = stage_stop(P, sg, t_last); t < t_stop; ++t) {
+        const int32_t k = (int32_t)(t - P.t0);
         float a[4];
         if (act) {
 #pragma unroll
@@ -261,7 +268,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
         Trans o;
         float za[4];
         action_noise(P, gid, t, za);
-        transition(P, e, gid, t, a, za, o);
+        transition<kDR>(P, W, e, gid, t, a, za, o);
         uint32_t fl = o.flags;
         const bool ended = active && (fl & (D_TERM | D_TRUNC));
         if (ended) stat_episode(st, o);
@@ -291,6 +298,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
             tr[27] = (float)e.ep_step;
             tr[28] = tr[29] = tr[30] = tr[31] = 0.0f;
         }
+    }
     }
     if (active) {
         store_state(P, B, i, e);
@@ -361,7 +369,10 @@ cudaError_t launch_step(const DevParams& P, const DevBufs& B, const float* act, 
                         cudaStream_t s)
 {
     const int64_t grid = (P.n + kStepBlock - 1) / kStepBlock;
-    step_kernel<<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, act, O);
+    if (P.flags & F_DOMAIN_RAND)
+        step_kernel<true><<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, act, O);
+    else
+        step_kernel<false><<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, act, O);
     return cudaGetLastError();
 }
 
@@ -377,7 +388,10 @@ cudaError_t launch_rollout_open(const DevParams& P, const DevBufs& B, const floa
                                 const int64_t* trace_ids, int32_t K, cudaStream_t s)
 {
     const int64_t grid = (P.n + kRolloutBlock - 1) / kRolloutBlock;
-    rollout_open_kernel<<<(unsigned)grid, kRolloutBlock, 0, s>>>(P, B, act, T, trace, trace_ids, K);
+    if (P.flags & F_DOMAIN_RAND)
+        rollout_open_kernel<true><<<(unsigned)grid, kRolloutBlock, 0, s>>>(P, B, act, T, trace, trace_ids, K);
+    else
+        rollout_open_kernel<false><<<(unsigned)grid, kRolloutBlock, 0, s>>>(P, B, act, T, trace, trace_ids, K);
     return cudaGetLastError();
 }
 

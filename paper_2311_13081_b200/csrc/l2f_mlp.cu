@@ -23,10 +23,14 @@
 #include "l2f_internal.h"
 #include "l2f_tcgen05.cuh"
 
+#ifndef L2F_MLP_TILES
+#define L2F_MLP_TILES 3
+#endif
+
 namespace l2f {
 namespace {
 
-constexpr int kTiles = 3;
+constexpr int kTiles = L2F_MLP_TILES;
 constexpr int kM = 128;
 constexpr int kThreads = kTiles * kM;
 constexpr int kHid = 64;
@@ -58,8 +62,11 @@ static_assert(kScratchBytes >= (kThreads / 32) * kStatsLen * 8, "stats rows fit 
 constexpr uint32_t kSmemBytes = OFF_STAT + kScratchBytes;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 constexpr uint32_t kTmemCols = 512;  // accumulators: kTiles x 64 columns from 0; noise stash: 32 per tile from 256
-constexpr uint32_t kStashCol = 256;
-constexpr uint32_t kA2Col = 384;  // TMEM A2 (h1/h2 as fp16, 32 columns + 8 with the ones column) per tile: 40 columns
+// TMEM map: accumulators 64 columns per tile from 0; A2 (h1/h2 as fp16: 32 columns + 8 with the
+// ones column) 40 per tile from 64 kTiles; the per-thread noise stash (18 used) 24 per tile after.
+constexpr uint32_t kA2Col = 64 * kTiles;
+constexpr uint32_t kStashCol = kA2Col + 40 * kTiles;
+static_assert(kStashCol + 24 * kTiles <= kTmemCols, "TMEM budget");
 
 constexpr uint32_t kIdescN64 = tc::make_idesc(128, 64, 0, 0);
 constexpr uint32_t kIdescN64BMN = tc::make_idesc(128, 64, 0, 1);
@@ -329,7 +336,7 @@ __device__ __forceinline__ TileCtx make_ctx(uint32_t sbase)
     c.mbar = sbase + OFF_BAR + 8 * g;
     c.tmem_tile = tbase + 64 * g;
     c.tmem_row = c.tmem_tile + ((uint32_t)(32 * (r / 32)) << 16);
-    c.stash_row = tbase + kStashCol + 32 * g + ((uint32_t)(32 * (r / 32)) << 16);
+    c.stash_row = tbase + kStashCol + 24 * g + ((uint32_t)(32 * (r / 32)) << 16);
     c.a2_tmem = tbase + kA2Col + 40 * g;
     c.a2_trow = c.a2_tmem + ((uint32_t)(32 * (r / 32)) << 16);
     if constexpr (kA2InTmem) {  // constant ones column (K index 64 of layers 2 and 3) + zero pad
@@ -355,6 +362,7 @@ __device__ void teardown_cta()
 // -------------------------------------------------------------------------------------------
 // Fused rollout: T steps of {obs -> MLP (tensor cores) -> env transition} per env.
 // -------------------------------------------------------------------------------------------
+template <bool kDR>
 __global__ void __launch_bounds__(kThreads, 1)
     rollout_mlp_kernel(const DevParams P, const DevBufs B, const PolicyDev W, int32_t T, float* __restrict__ trace,
                        const int64_t* __restrict__ trace_ids, int32_t K, int32_t n_tiles)
@@ -381,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int q = 0; q < 6; ++q) e.dist[q] = B.dist[q * N + i];
 #pragma unroll
-            for (int q = 0; q < 5; ++q) e.dr[q] = (P.flags & F_DOMAIN_RAND) ? B.dr[q * N + i] : 1.0f;
+            for (int q = 0; q < 5; ++q) e.dr[q] = kDR ? B.dr[q * N + i] : 1.0f;
             e.ep_step = B.ep_step[i];
             e.ep_return = B.ep_return[i];
         } else {
@@ -416,8 +424,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ring rotation (t - 1) mod N_H and write position (-t) mod N_H, advanced incrementally
         uint32_t rot = NH > 0 ? (P.t0 + (uint32_t)NH - 1u) % (uint32_t)NH : 0u;
         int wpos = NH > 0 ? (int)(((uint32_t)NH - P.t0 % (uint32_t)NH) % (uint32_t)NH) : 0;
-        for (int32_t k = 0; k < T; ++k) {
-            const uint32_t t = P.t0 + (uint32_t)k;
+        const uint32_t t_last = P.t0 + (uint32_t)T;
+        uint32_t t = P.t0;
+        for (int sg = 0; sg < P.n_stages; ++sg) {  // curriculum stages of this launch
+        const StageW& W = P.stage[sg];
+        for (const uint32_t t_stop = stage_stop(P, sg, t_last); t < t_stop; ++t) {
+            const int32_t k = (int32_t)(t - P.t0);
             float ob[kObsCore];
             {
                 float z[20];
@@ -439,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int q = 0; q < 4; ++q) tr[17 + q] = a[q];
             }
             Trans o;
-            transition(P, e, gid, t, a, za, o);
+            transition<kDR>(P, W, e, gid, t, a, za, o);
             uint32_t fl = o.flags;
             const bool ended = (fl & (D_TERM | D_TRUNC)) != 0;
             if (ended && active) stat_episode(st, o);
@@ -484,12 +496,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tr[28] = tr[29] = tr[30] = tr[31] = 0.0f;
             }
         }
+        }
         if (active) {
 #pragma unroll
             for (int q = 0; q < kStateDim; ++q) B.state[q * N + i] = e.s[q];
 #pragma unroll
             for (int q = 0; q < 6; ++q) B.dist[q * N + i] = e.dist[q];
-            if (P.flags & F_DOMAIN_RAND)
+            if (kDR)
 #pragma unroll
                 for (int q = 0; q < 5; ++q) B.dr[q * N + i] = e.dr[q];
             B.ep_step[i] = e.ep_step;
@@ -600,12 +613,19 @@ cudaError_t launch_rollout_mlp(const DevParams& P, const DevBufs& B, const Polic
     if (P.n_hist % 4 != 0 || W.hidden != kHid || W.in_dim != 18 + 4 * P.n_hist) return cudaErrorNotSupported;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(rollout_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaError_t e =
+            cudaFuncSetAttribute(rollout_mlp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(rollout_mlp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kSmemBytes);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     const int n_tiles = (int)((P.n + kM - 1) / kM);
-    rollout_mlp_kernel<<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, n_tiles);
+    if (P.flags & F_DOMAIN_RAND)
+        rollout_mlp_kernel<true><<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, n_tiles);
+    else
+        rollout_mlp_kernel<false><<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, n_tiles);
     return cudaGetLastError();
 }
 
