@@ -165,6 +165,7 @@ struct l2f_env {
     DevBufs B;
     DevParams base;
     uint64_t t;
+    double steps;  // env-steps since the statistics were last reset (exact, host-side)
 };
 
 namespace {
@@ -319,6 +320,7 @@ l2f_status l2f_create(const l2f_config* cfg, void* d_workspace, size_t bytes, l2
     env->B.n_slots = L.n_slots;
     env->base = make_base(*cfg);
     env->t = 0;
+    env->steps = 0.0;
     *out = env;
     return L2F_OK;
 }
@@ -342,6 +344,7 @@ l2f_status l2f_reset(l2f_env* env, const uint8_t* d_mask, const l2f_step_out* ou
         if (e == cudaSuccess && env->cfg.action_history > 0)
             e = cudaMemsetAsync(env->B.hist, 0, sizeof(float) * 4 * (size_t)env->cfg.action_history * env->cfg.num_envs, s);
         if (e != cudaSuccess) return cuda_fail(e, "l2f_reset memset");
+        env->steps = 0.0;
     }
     return launched(launch_reset(P, env->B, d_mask, to_dev(out), s), "l2f_reset");
 }
@@ -352,7 +355,10 @@ l2f_status l2f_step(l2f_env* env, const float* d_actions, const l2f_step_out* ou
     DevParams P;
     params_for(env, env->t, 1, P);
     l2f_status st = launched(launch_step(P, env->B, d_actions, to_dev(out), (cudaStream_t)stream), "l2f_step");
-    if (st == L2F_OK) env->t += 1;
+    if (st == L2F_OK) {
+        env->t += 1;
+        env->steps += (double)env->cfg.num_envs;
+    }
     return st;
 }
 
@@ -393,6 +399,7 @@ l2f_status l2f_rollout(l2f_env* env, const l2f_policy* policy, const float* d_ac
         l2f_status st = launched(e, "l2f_rollout");
         if (st != L2F_OK) return st;
         env->t += (uint64_t)chunk;
+        env->steps += (double)chunk * (double)env->cfg.num_envs;
         done += chunk;
     }
     return L2F_OK;
@@ -401,9 +408,11 @@ l2f_status l2f_rollout(l2f_env* env, const l2f_policy* policy, const float* d_ac
 l2f_status l2f_episode_stats(l2f_env* env, double* d_out, int32_t reset_accumulators, void* stream)
 {
     if (!env || !d_out) return fail(L2F_ERR_INVALID_ARGUMENT, "env/out is NULL");
-    return launched(launch_stats_finalize(env->B.slots, env->L.n_slots, d_out, reset_accumulators,
-                                          (cudaStream_t)stream),
-                    "l2f_episode_stats");
+    l2f_status st = launched(launch_stats_finalize(env->B.slots, env->L.n_slots, d_out, reset_accumulators,
+                                                   env->steps, (cudaStream_t)stream),
+                             "l2f_episode_stats");
+    if (st == L2F_OK && reset_accumulators) env->steps = 0.0;
+    return st;
 }
 
 l2f_status l2f_step_host(l2f_env* env, const float* h_actions, float* h_obs_core, float* h_reward, uint8_t* h_flags,

@@ -17,6 +17,7 @@ constexpr int kMaxHist = 32;
 constexpr int kMaxStages = 8;
 constexpr int kStatsLen = 8;
 constexpr int kTraceFields = 32;
+constexpr int kResetScratch = 40;  // uint4 per warp for reset_env_warp
 
 enum : uint32_t {
     F_OBS_NOISE = 1u << 0,
@@ -274,30 +275,76 @@ __device__ __forceinline__ void deriv(const DevParams& P, const Phys& ph, const 
 
 // Classical RK4 with zero-order-hold setpoints (Q1), then q renormalisation and rotor-speed
 // clamp (Q5).  Returns true if the result is non-finite.
+#ifndef L2F_F2
+#define L2F_F2 1
+#endif
+// RK4 stage combinations on component pairs with the sm_100 packed FP32 pipe (FFMA2/FADD2):
+// each lane of a packed op is an IEEE fma/add exactly like the scalar instruction, so results
+// are bitwise those of the scalar loop; 17 components -> 8 packed pairs + 1 scalar.
+__device__ __forceinline__ void stage_axpy(const float* k, const float* s, float h, float* out)
+{
+#if L2F_F2
+    const float2 hh = make_float2(h, h);
+#pragma unroll
+    for (int i = 0; i + 1 < kStateDim; i += 2) {
+        const float2 r = __ffma2_rn(make_float2(k[i], k[i + 1]), hh, make_float2(s[i], s[i + 1]));
+        out[i] = r.x;
+        out[i + 1] = r.y;
+    }
+    out[kStateDim - 1] = fmaf(h, k[kStateDim - 1], s[kStateDim - 1]);
+#else
+#pragma unroll
+    for (int i = 0; i < kStateDim; ++i) out[i] = fmaf(h, k[i], s[i]);
+#endif
+}
+
+__device__ __forceinline__ void acc_2k(const float* k, float* acc)
+{
+#if L2F_F2
+    const float2 two = make_float2(2.0f, 2.0f);
+#pragma unroll
+    for (int i = 0; i + 1 < kStateDim; i += 2) {
+        const float2 r = __ffma2_rn(make_float2(k[i], k[i + 1]), two, make_float2(acc[i], acc[i + 1]));
+        acc[i] = r.x;
+        acc[i + 1] = r.y;
+    }
+    acc[kStateDim - 1] = fmaf(2.0f, k[kStateDim - 1], acc[kStateDim - 1]);
+#else
+#pragma unroll
+    for (int i = 0; i < kStateDim; ++i) acc[i] = fmaf(2.0f, k[i], acc[i]);
+#endif
+}
+
 __device__ __forceinline__ bool rk4_step(const DevParams& P, const Phys& ph, const float* d, float* s)
 {
     float acc[kStateDim], tmp[kStateDim], k[kStateDim];
     deriv(P, ph, d, s, k);
 #pragma unroll
-    for (int i = 0; i < kStateDim; ++i) {
-        acc[i] = k[i];
-        tmp[i] = fmaf(P.half_dt, k[i], s[i]);
-    }
+    for (int i = 0; i < kStateDim; ++i) acc[i] = k[i];
+    stage_axpy(k, s, P.half_dt, tmp);
     deriv(P, ph, d, tmp, k);
+    acc_2k(k, acc);
+    stage_axpy(k, s, P.half_dt, tmp);
+    deriv(P, ph, d, tmp, k);
+    acc_2k(k, acc);
+    stage_axpy(k, s, P.dt, tmp);
+    deriv(P, ph, d, tmp, k);
+#if L2F_F2
+    {
+        const float2 h6 = make_float2(P.dt_6, P.dt_6);
 #pragma unroll
-    for (int i = 0; i < kStateDim; ++i) {
-        acc[i] = fmaf(2.0f, k[i], acc[i]);
-        tmp[i] = fmaf(P.half_dt, k[i], s[i]);
+        for (int i = 0; i + 1 < kStateDim; i += 2) {
+            const float2 a = __fadd2_rn(make_float2(acc[i], acc[i + 1]), make_float2(k[i], k[i + 1]));
+            const float2 r = __ffma2_rn(h6, a, make_float2(s[i], s[i + 1]));
+            s[i] = r.x;
+            s[i + 1] = r.y;
+        }
+        s[kStateDim - 1] = fmaf(P.dt_6, acc[kStateDim - 1] + k[kStateDim - 1], s[kStateDim - 1]);
     }
-    deriv(P, ph, d, tmp, k);
-#pragma unroll
-    for (int i = 0; i < kStateDim; ++i) {
-        acc[i] = fmaf(2.0f, k[i], acc[i]);
-        tmp[i] = fmaf(P.dt, k[i], s[i]);
-    }
-    deriv(P, ph, d, tmp, k);
+#else
 #pragma unroll
     for (int i = 0; i < kStateDim; ++i) s[i] = fmaf(P.dt_6, acc[i] + k[i], s[i]);
+#endif
     const float n2 = (s[3] * s[3] + s[4] * s[4]) + (s[5] * s[5] + s[6] * s[6]);
     const float inv = rsqrtf(n2);
 #pragma unroll
@@ -476,7 +523,8 @@ __device__ __forceinline__ void reset_env(const DevParams& P, EnvReg& e, uint32_
 
 // Warp-cooperative reset (all 32 lanes must call; gids of a warp are consecutive): the Philox
 // blocks of every lane that needs a reset are drawn by all lanes in parallel and handed to
-// their owner through a 32-entry shared-memory scratch of the warp, so a warp with k ending
+// their owner through a shared-memory scratch of the warp (kResetScratch uint4: 32 blocks +
+// a 32-int rank->lane table), so a warp with k ending
 // episodes pays ceil(k * nb / 32) Philox rounds instead of nb serial ones.  Bitwise identical
 // to reset_env (integer Philox, owner-lane sampling).
 __device__ __forceinline__ bool reset_env_warp(const DevParams& P, EnvReg& e, uint32_t gid, uint32_t ctr, bool need,
@@ -489,21 +537,18 @@ __device__ __forceinline__ bool reset_env_warp(const DevParams& P, EnvReg& e, ui
     const int nb = 1 << lnb;
     const int nr = __popc(m);
     const int rank = __popc(m & ((1u << lane) - 1u));
+    // rank -> lane table in the scratch's tail words (entries 32..39 hold 32 ints)
+    int* tab = reinterpret_cast<int*>(scratch + 32);
+    if (need) tab[rank] = lane;
+    __syncwarp();
     uint4 blk[8];
     for (int base = 0; base < nr * nb; base += 32) {
         const int j = base + lane;
         uint4 x = make_uint4(0u, 0u, 0u, 0u);
         if (j < nr * nb) {
-            const int r = j >> lnb, b = j & (nb - 1);
+            const int b = j & (nb - 1);
             const bool used = b < 4 || (b < 6 && (P.flags & F_DISTURBANCE)) || (b >= 6 && (P.flags & F_DOMAIN_RAND));
-            // lane of the r-th resetting env: walk the (few) set bits of m
-            int src = 0;
-            unsigned mm = m;
-            for (int q = 0; q <= r; ++q) {
-                src = __ffs(mm) - 1;
-                mm &= mm - 1u;
-            }
-            if (used) x = reset_block(P, gid - (uint32_t)lane + (uint32_t)src, ctr, b);
+            if (used) x = reset_block(P, gid - (uint32_t)lane + (uint32_t)tab[j >> lnb], ctr, b);
         }
         __syncwarp();
         scratch[lane] = x;

@@ -25,13 +25,20 @@ struct PolicyDev {
 
 cudaError_t launch_step(const DevParams& P, const DevBufs& B, const float* act, const StepOutDev& O,
                         cudaStream_t s);
+cudaError_t launch_step_plain(const DevParams& P, const DevBufs& B, const float* act, const StepOutDev& O,
+                              cudaStream_t s);
+bool step_tma_ok(const DevParams& P, const float* act, const StepOutDev& O);
+int step_tma_grid(int64_t n);
+cudaError_t launch_step_tma(const DevParams& P, const DevBufs& B, const float* act, const StepOutDev& O,
+                            cudaStream_t s);
 cudaError_t launch_reset(const DevParams& P, const DevBufs& B, const uint8_t* mask, const StepOutDev& O,
                          cudaStream_t s);
 cudaError_t launch_rollout_open(const DevParams& P, const DevBufs& B, const float* act, int32_t T, float* trace,
                                 const int64_t* trace_ids, int32_t K, cudaStream_t s);
 cudaError_t launch_philox_selftest(int64_t n, uint64_t seed, uint32_t t, uint32_t* ours, uint32_t* ref,
                                    cudaStream_t s);
-cudaError_t launch_stats_finalize(double* slots, int32_t n_slots, double* out, int32_t reset, cudaStream_t s);
+cudaError_t launch_stats_finalize(double* slots, int32_t n_slots, double* out, int32_t reset, double host_steps,
+                                  cudaStream_t s);
 
 // tcgen05 actor-MLP rollout (l2f_mlp.cu).  Returns cudaErrorNotSupported for unsupported shapes.
 int mlp_rollout_grid(int64_t n);

@@ -5,6 +5,8 @@
 // Step kernel bytes per env-step (algorithmic): reads state 68 + action 16 +
 // disturbance 24 + counters 8 (+ DR 20), writes state 68 + counters 8 + history slot 16 +
 // obs_core 72 + reward 4 + flags 1.
+#include <cstdlib>
+
 #include <curand_philox4x32_x.h>
 
 #include "l2f_device.cuh"
@@ -117,7 +119,7 @@ __global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, con
                                                           const float* __restrict__ act, const StepOutDev O)
 {
     __shared__ double srow[(kStepBlock / 32) * kStatsLen];
-    __shared__ uint4 rscratch[kStepBlock];  // 32 entries per warp for the cooperative reset
+    __shared__ uint4 rscratch[(kStepBlock / 32) * kResetScratch];  // cooperative reset scratch per warp
     const int64_t N = P.n;
     const int64_t i = (int64_t)blockIdx.x * kStepBlock + threadIdx.x;
     const bool active = i < N;
@@ -148,7 +150,7 @@ __global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, con
     bool did_reset = false;
     float hf[4];
     if (P.flags & F_AUTO_RESET) {
-        did_reset = reset_env_warp(P, e, gid, t + 1, ended, hf, rscratch + (threadIdx.x & ~31));
+        did_reset = reset_env_warp(P, e, gid, t + 1, ended, hf, rscratch + (threadIdx.x >> 5) * kResetScratch);
         if (did_reset) fl |= D_RESET;
     } else if (ended) {
         e.ep_step = 0;
@@ -156,13 +158,10 @@ __global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, con
     }
     if (active) {
         if (P.n_hist > 0) {
-            if (did_reset) {
-                hist_restart(P, B, i, t + 1, hf);
-            } else {
-                const int slot = P.hist_slot0;  // t0 mod N_H
+            const int slot = P.hist_slot0;  // t0 mod N_H (written for every env: deterministic ring)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) B.hist[((int64_t)slot * 4 + c) * N + i] = o.a[c];
-            }
+            for (int c = 0; c < 4; ++c) B.hist[((int64_t)slot * 4 + c) * N + i] = o.a[c];
+            if (did_reset) hist_restart(P, B, i, t + 1, hf);
         }
         store_state(P, B, i, e);
         if (did_reset) store_episode_consts(P, B, i, e);
@@ -178,8 +177,7 @@ __global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, con
         if (O.reward) O.reward[i] = o.reward;
         if (O.flags) O.flags[i] = (uint8_t)fl;
     }
-    const int64_t rem = N - (int64_t)blockIdx.x * kStepBlock;
-    stats_block_end(st, srow, (double)(rem < kStepBlock ? rem : kStepBlock), B.slots + (size_t)blockIdx.x * kStatsLen);
+    stats_block_end(st, srow, 0.0, B.slots + (size_t)blockIdx.x * kStatsLen);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -228,7 +226,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
                                                                      int32_t K)
 {
     __shared__ double srow[(kRolloutBlock / 32) * kStatsLen];
-    __shared__ uint4 rscratch[kRolloutBlock];
+    __shared__ uint4 rscratch[(kRolloutBlock / 32) * kResetScratch];
     const int64_t N = P.n;
     const int64_t i = (int64_t)blockIdx.x * kRolloutBlock + threadIdx.x;
     const bool active = i < N;
@@ -275,19 +273,16 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
         bool did_reset = false;
         float hf[4];
         if (P.flags & F_AUTO_RESET) {
-            did_reset = reset_env_warp(P, e, gid, t + 1, ended, hf, rscratch + (threadIdx.x & ~31));
+            did_reset = reset_env_warp(P, e, gid, t + 1, ended, hf, rscratch + (threadIdx.x >> 5) * kResetScratch);
             if (did_reset) fl |= D_RESET;
         } else if (ended) {
             e.ep_step = 0;
             e.ep_return = 0.0f;
         }
         if (active && P.n_hist > 0) {
-            if (did_reset) {
-                hist_restart(P, B, i, t + 1, hf);
-            } else {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) B.hist[((int64_t)slot * 4 + c) * N + i] = o.a[c];
-            }
+            for (int c = 0; c < 4; ++c) B.hist[((int64_t)slot * 4 + c) * N + i] = o.a[c];
+            if (did_reset) hist_restart(P, B, i, t + 1, hf);
         }
         if (++slot == P.n_hist) slot = 0;
         if (tr) {
@@ -311,7 +306,8 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
 
 // Fixed-order reduction of all statistics slots into out[8] (one block of 256 threads).
 __global__ void __launch_bounds__(256) stats_finalize_kernel(double* __restrict__ slots, int32_t n_slots,
-                                                             double* __restrict__ out, int32_t reset)
+                                                             double* __restrict__ out, int32_t reset,
+                                                             double host_steps)
 {
     __shared__ double part[256 * kStatsLen];
     const int tid = threadIdx.x;
@@ -330,7 +326,7 @@ __global__ void __launch_bounds__(256) stats_finalize_kernel(double* __restrict_
             for (int j = 0; j < kStatsLen; ++j) part[tid * kStatsLen + j] += part[(tid + w) * kStatsLen + j];
         __syncthreads();
     }
-    if (tid < kStatsLen) out[tid] = part[tid];
+    if (tid < kStatsLen) out[tid] = tid == kStatsLen - 1 ? host_steps : part[tid];
     if (reset) {
         __syncthreads();
         for (int s = tid; s < n_slots * kStatsLen; s += 256) slots[s] = 0.0;
@@ -368,6 +364,18 @@ cudaError_t launch_philox_selftest(int64_t n, uint64_t seed, uint32_t t, uint32_
 cudaError_t launch_step(const DevParams& P, const DevBufs& B, const float* act, const StepOutDev& O,
                         cudaStream_t s)
 {
+    // L2F_STEP_PATH=plain|bulk selects the variant (diagnostics / A-B measurements); default plain
+    static const int path = [] {
+        const char* v = getenv("L2F_STEP_PATH");
+        return (v && v[0] == 'b') ? 1 : 0;
+    }();
+    if (path == 1 && step_tma_ok(P, act, O)) return launch_step_tma(P, B, act, O, s);
+    return launch_step_plain(P, B, act, O, s);
+}
+
+cudaError_t launch_step_plain(const DevParams& P, const DevBufs& B, const float* act, const StepOutDev& O,
+                              cudaStream_t s)
+{
     const int64_t grid = (P.n + kStepBlock - 1) / kStepBlock;
     if (P.flags & F_DOMAIN_RAND)
         step_kernel<true><<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, act, O);
@@ -395,9 +403,10 @@ cudaError_t launch_rollout_open(const DevParams& P, const DevBufs& B, const floa
     return cudaGetLastError();
 }
 
-cudaError_t launch_stats_finalize(double* slots, int32_t n_slots, double* out, int32_t reset, cudaStream_t s)
+cudaError_t launch_stats_finalize(double* slots, int32_t n_slots, double* out, int32_t reset, double host_steps,
+                                  cudaStream_t s)
 {
-    stats_finalize_kernel<<<1, 256, 0, s>>>(slots, n_slots, out, reset);
+    stats_finalize_kernel<<<1, 256, 0, s>>>(slots, n_slots, out, reset, host_steps);
     return cudaGetLastError();
 }
 

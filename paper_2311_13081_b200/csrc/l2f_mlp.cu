@@ -57,7 +57,7 @@ constexpr uint32_t OFF_ONES = OFF_W3 + kW3Bytes;
 constexpr uint32_t OFF_BAR = OFF_ONES + kOnesBytes;   // kTiles MMA-done mbarriers
 constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * kTiles;
 constexpr uint32_t OFF_STAT = (OFF_TMEM + 8 + 127) & ~127u;  // reset scratch (32 uint4 per warp); reused by stats
-constexpr uint32_t kScratchBytes = (kThreads / 32) * 32 * 16;
+constexpr uint32_t kScratchBytes = (kThreads / 32) * kResetScratch * 16;
 static_assert(kScratchBytes >= (kThreads / 32) * kStatsLen * 8, "stats rows fit in the scratch");
 constexpr uint32_t kSmemBytes = OFF_STAT + kScratchBytes;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             float hf[4];
             if (P.flags & F_AUTO_RESET) {
                 did_reset = reset_env_warp(P, e, gid, t + 1, ended && active, hf,
-                                           reinterpret_cast<uint4*>(smem + OFF_STAT) + (threadIdx.x & ~31));
+                                           reinterpret_cast<uint4*>(smem + OFF_STAT) + (threadIdx.x >> 5) * kResetScratch);
                 if (did_reset) fl |= D_RESET;
             }
             if (ended && !did_reset) {
