@@ -188,6 +188,7 @@ DevParams make_base(const l2f_config& c)
     P.dt = (float)c.dt;
     P.half_dt = (float)(0.5 * c.dt);
     P.dt_6 = (float)(c.dt / 6.0);
+    P.dt2_6 = (float)(c.dt * c.dt / 6.0);
     const l2f_params& p = c.params;
     P.mass = (float)p.mass;
     for (int j = 0; j < 3; ++j) {

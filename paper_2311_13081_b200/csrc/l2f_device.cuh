@@ -47,7 +47,7 @@ struct DevParams {
     int64_t n;                 // envs
     uint32_t t0;               // step counter at launch
     // integration
-    float dt, half_dt, dt_6;
+    float dt, half_dt, dt_6, dt2_6;
     // nominal parameters; DR factors scale mass, J, thrust coefficients (Q19)
     float mass, J[3], c[3], ctau, inv_tm, rpm_min, rpm_max, gravity, rpm_half_span, inv_rpm_span2;
     float rx[4], ry[4], spin[4];
@@ -228,14 +228,18 @@ __device__ __forceinline__ void make_phys(const DevParams& P, const EnvReg& e, c
     for (int i = 0; i < 4; ++i) ph.u_tm[i] = u[i] * P.inv_tm;
 }
 
-// ds = f(s): p' = v; q' = 1/2 q (x) (0,w); v' = (R e_z T + f_r)/m - g e_z;
-// w' = J^-1 (tau - w x J w); w_m' = (u - w_m)/T_m.
+// Derivative of the non-position part x = s[3..16] = (q, v, w, w_m):
+// q' = 1/2 q (x) (0,w); v' = (R e_z T + f_r)/m - g e_z; w' = J^-1 (tau - w x J w);
+// w_m' = (u - w_m)/T_m.  The position never feeds back (p' = v), so RK4 integrates it in
+// closed form from the stage velocities (rk4_step).  dx[j] = d/dt s[3 + j].
+constexpr int kX = 14;
 __device__ __forceinline__ void deriv(const DevParams& P, const Phys& ph, const float* d,
-                                      const float* s, float* ds)
+                                      const float* x, float* dx)
 {
+    const float* wm = x + 10;
     float f[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) f[i] = fmaf(fmaf(ph.c2, s[13 + i], ph.c1), s[13 + i], ph.c0);
+    for (int i = 0; i < 4; ++i) f[i] = fmaf(fmaf(ph.c2, wm[i], ph.c1), wm[i], ph.c0);
     const float T = (f[0] + f[1]) + (f[2] + f[3]);
     float tx = d[3], ty = d[4], tz = 0.0f;
 #pragma unroll
@@ -245,107 +249,84 @@ __device__ __forceinline__ void deriv(const DevParams& P, const Phys& ph, const 
         tz = fmaf(P.spin[i], f[i], tz);
     }
     tz = fmaf(P.ctau, tz, d[5]);
-    const float qw = s[3], qx = s[4], qy = s[5], qz = s[6];
-    const float wx = s[10], wy = s[11], wz = s[12];
-    ds[0] = s[7];
-    ds[1] = s[8];
-    ds[2] = s[9];
+    const float qw = x[0], qx = x[1], qy = x[2], qz = x[3];
+    const float wx = x[7], wy = x[8], wz = x[9];
     const float hx = 0.5f * wx, hy = 0.5f * wy, hz = 0.5f * wz;
-    ds[3] = -(qx * hx + qy * hy + qz * hz);
-    ds[4] = qw * hx + qy * hz - qz * hy;
-    ds[5] = qw * hy - qx * hz + qz * hx;
-    ds[6] = qw * hz + qx * hy - qy * hx;
+    dx[0] = -(qx * hx + qy * hy + qz * hz);
+    dx[1] = qw * hx + qy * hz - qz * hy;
+    dx[2] = qw * hy - qx * hz + qz * hx;
+    dx[3] = qw * hz + qx * hy - qy * hx;
     // third column of R(q): body z-axis in world
     const float r02 = 2.0f * (qx * qz + qw * qy);
     const float r12 = 2.0f * (qy * qz - qw * qx);
     const float r22 = 1.0f - 2.0f * (qx * qx + qy * qy);
-    ds[7] = fmaf(r02, T, d[0]) * ph.inv_m;
-    ds[8] = fmaf(r12, T, d[1]) * ph.inv_m;
-    ds[9] = fmaf(fmaf(r22, T, d[2]), ph.inv_m, -P.gravity);
+    dx[4] = fmaf(r02, T, d[0]) * ph.inv_m;
+    dx[5] = fmaf(r12, T, d[1]) * ph.inv_m;
+    dx[6] = fmaf(fmaf(r22, T, d[2]), ph.inv_m, -P.gravity);
     // Euler: J w' = tau - w x (J w)
     const float cx = ph.dJzy * (wy * wz);
     const float cy = ph.dJxz * (wz * wx);
     const float cz = ph.dJyx * (wx * wy);
-    ds[10] = (tx - cx) * ph.iJx;
-    ds[11] = (ty - cy) * ph.iJy;
-    ds[12] = (tz - cz) * ph.iJz;
+    dx[7] = (tx - cx) * ph.iJx;
+    dx[8] = (ty - cy) * ph.iJy;
+    dx[9] = (tz - cz) * ph.iJz;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) ds[13 + i] = fmaf(-s[13 + i], P.inv_tm, ph.u_tm[i]);
+    for (int i = 0; i < 4; ++i) dx[10 + i] = fmaf(-wm[i], P.inv_tm, ph.u_tm[i]);
 }
 
 // Classical RK4 with zero-order-hold setpoints (Q1), then q renormalisation and rotor-speed
 // clamp (Q5).  Returns true if the result is non-finite.
-#ifndef L2F_F2
-#define L2F_F2 1
-#endif
-// RK4 stage combinations on component pairs with the sm_100 packed FP32 pipe (FFMA2/FADD2):
-// each lane of a packed op is an IEEE fma/add exactly like the scalar instruction, so results
-// are bitwise those of the scalar loop; 17 components -> 8 packed pairs + 1 scalar.
-__device__ __forceinline__ void stage_axpy(const float* k, const float* s, float h, float* out)
+// The 14 non-position components use the sm_100 packed FP32 pipe (FFMA2/FADD2: each lane is
+// an IEEE fma/add like the scalar instruction) in 7 pairs.  Position: with p' = v and stage
+// velocities v1 = v, v2 = v + h/2 a1, v3 = v + h/2 a2, v4 = v + h a3, the RK4 combination
+// h/6 (v1 + 2 v2 + 2 v3 + v4) equals h v + h^2/6 (a1 + a2 + a3) exactly.
+__device__ __forceinline__ void pair_fma(const float* a, float h, const float* b, float* out)
 {
-#if L2F_F2
     const float2 hh = make_float2(h, h);
 #pragma unroll
-    for (int i = 0; i + 1 < kStateDim; i += 2) {
-        const float2 r = __ffma2_rn(make_float2(k[i], k[i + 1]), hh, make_float2(s[i], s[i + 1]));
+    for (int i = 0; i < kX; i += 2) {
+        const float2 r = __ffma2_rn(make_float2(a[i], a[i + 1]), hh, make_float2(b[i], b[i + 1]));
         out[i] = r.x;
         out[i + 1] = r.y;
     }
-    out[kStateDim - 1] = fmaf(h, k[kStateDim - 1], s[kStateDim - 1]);
-#else
-#pragma unroll
-    for (int i = 0; i < kStateDim; ++i) out[i] = fmaf(h, k[i], s[i]);
-#endif
-}
-
-__device__ __forceinline__ void acc_2k(const float* k, float* acc)
-{
-#if L2F_F2
-    const float2 two = make_float2(2.0f, 2.0f);
-#pragma unroll
-    for (int i = 0; i + 1 < kStateDim; i += 2) {
-        const float2 r = __ffma2_rn(make_float2(k[i], k[i + 1]), two, make_float2(acc[i], acc[i + 1]));
-        acc[i] = r.x;
-        acc[i + 1] = r.y;
-    }
-    acc[kStateDim - 1] = fmaf(2.0f, k[kStateDim - 1], acc[kStateDim - 1]);
-#else
-#pragma unroll
-    for (int i = 0; i < kStateDim; ++i) acc[i] = fmaf(2.0f, k[i], acc[i]);
-#endif
 }
 
 __device__ __forceinline__ bool rk4_step(const DevParams& P, const Phys& ph, const float* d, float* s)
 {
-    float acc[kStateDim], tmp[kStateDim], k[kStateDim];
-    deriv(P, ph, d, s, k);
+    float* x = s + 3;
+    float acc[kX], tmp[kX], k[kX];
+    deriv(P, ph, d, x, k);
+    float asum0 = k[4], asum1 = k[5], asum2 = k[6];  // a1 + a2 + a3 (v' of stages 1-3)
 #pragma unroll
-    for (int i = 0; i < kStateDim; ++i) acc[i] = k[i];
-    stage_axpy(k, s, P.half_dt, tmp);
+    for (int i = 0; i < kX; ++i) acc[i] = k[i];
+    pair_fma(k, P.half_dt, x, tmp);
     deriv(P, ph, d, tmp, k);
-    acc_2k(k, acc);
-    stage_axpy(k, s, P.half_dt, tmp);
+    asum0 += k[4];
+    asum1 += k[5];
+    asum2 += k[6];
+    pair_fma(k, 2.0f, acc, acc);
+    pair_fma(k, P.half_dt, x, tmp);
     deriv(P, ph, d, tmp, k);
-    acc_2k(k, acc);
-    stage_axpy(k, s, P.dt, tmp);
+    asum0 += k[4];
+    asum1 += k[5];
+    asum2 += k[6];
+    pair_fma(k, 2.0f, acc, acc);
+    pair_fma(k, P.dt, x, tmp);
     deriv(P, ph, d, tmp, k);
-#if L2F_F2
+    // position first (uses the pre-step velocity)
+    s[0] = fmaf(P.dt2_6, asum0, fmaf(P.dt, s[7], s[0]));
+    s[1] = fmaf(P.dt2_6, asum1, fmaf(P.dt, s[8], s[1]));
+    s[2] = fmaf(P.dt2_6, asum2, fmaf(P.dt, s[9], s[2]));
     {
         const float2 h6 = make_float2(P.dt_6, P.dt_6);
 #pragma unroll
-        for (int i = 0; i + 1 < kStateDim; i += 2) {
+        for (int i = 0; i < kX; i += 2) {
             const float2 a = __fadd2_rn(make_float2(acc[i], acc[i + 1]), make_float2(k[i], k[i + 1]));
-            const float2 r = __ffma2_rn(h6, a, make_float2(s[i], s[i + 1]));
-            s[i] = r.x;
-            s[i + 1] = r.y;
+            const float2 r = __ffma2_rn(h6, a, make_float2(x[i], x[i + 1]));
+            x[i] = r.x;
+            x[i + 1] = r.y;
         }
-        s[kStateDim - 1] = fmaf(P.dt_6, acc[kStateDim - 1] + k[kStateDim - 1], s[kStateDim - 1]);
-    }
-#else
-#pragma unroll
-    for (int i = 0; i < kStateDim; ++i) s[i] = fmaf(P.dt_6, acc[i] + k[i], s[i]);
-#endif
-    const float n2 = (s[3] * s[3] + s[4] * s[4]) + (s[5] * s[5] + s[6] * s[6]);
+    }    const float n2 = (s[3] * s[3] + s[4] * s[4]) + (s[5] * s[5] + s[6] * s[6]);
     const float inv = rsqrtf(n2);
 #pragma unroll
     for (int i = 3; i < 7; ++i) s[i] *= inv;

@@ -27,10 +27,6 @@ cudaError_t launch_step(const DevParams& P, const DevBufs& B, const float* act, 
                         cudaStream_t s);
 cudaError_t launch_step_plain(const DevParams& P, const DevBufs& B, const float* act, const StepOutDev& O,
                               cudaStream_t s);
-bool step_tma_ok(const DevParams& P, const float* act, const StepOutDev& O);
-int step_tma_grid(int64_t n);
-cudaError_t launch_step_tma(const DevParams& P, const DevBufs& B, const float* act, const StepOutDev& O,
-                            cudaStream_t s);
 cudaError_t launch_reset(const DevParams& P, const DevBufs& B, const uint8_t* mask, const StepOutDev& O,
                          cudaStream_t s);
 cudaError_t launch_rollout_open(const DevParams& P, const DevBufs& B, const float* act, int32_t T, float* trace,

@@ -5,9 +5,11 @@
 // Step kernel bytes per env-step (algorithmic): reads state 68 + action 16 +
 // disturbance 24 + counters 8 (+ DR 20), writes state 68 + counters 8 + history slot 16 +
 // obs_core 72 + reward 4 + flags 1.
-#include <cstdlib>
-
 #include <curand_philox4x32_x.h>
+
+#ifndef L2F_STEP_MINB
+#define L2F_STEP_MINB 5  // resident 128-thread blocks per SM the register budget targets
+#endif
 
 #include "l2f_device.cuh"
 #include "l2f_internal.h"
@@ -115,7 +117,7 @@ __device__ __forceinline__ void stats_block_end(const StatAcc& st, double* srow,
 // l2f_step: one transition for every env.
 // ---------------------------------------------------------------------------------------
 template <bool kDR>
-__global__ void __launch_bounds__(kStepBlock) step_kernel(const DevParams P, const DevBufs B,
+__global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const DevParams P, const DevBufs B,
                                                           const float* __restrict__ act, const StepOutDev O)
 {
     __shared__ double srow[(kStepBlock / 32) * kStatsLen];
@@ -364,12 +366,6 @@ cudaError_t launch_philox_selftest(int64_t n, uint64_t seed, uint32_t t, uint32_
 cudaError_t launch_step(const DevParams& P, const DevBufs& B, const float* act, const StepOutDev& O,
                         cudaStream_t s)
 {
-    // L2F_STEP_PATH=plain|bulk selects the variant (diagnostics / A-B measurements); default plain
-    static const int path = [] {
-        const char* v = getenv("L2F_STEP_PATH");
-        return (v && v[0] == 'b') ? 1 : 0;
-    }();
-    if (path == 1 && step_tma_ok(P, act, O)) return launch_step_tma(P, B, act, O, s);
     return launch_step_plain(P, B, act, O, s);
 }
 

@@ -34,27 +34,21 @@ constexpr int kTiles = L2F_MLP_TILES;
 constexpr int kM = 128;
 constexpr int kThreads = kTiles * kM;
 constexpr int kHid = 64;
-// Hidden activations (A operand of layers 2 and 3) in TMEM instead of shared memory.
-constexpr bool kA2InTmem = true;
 
 // shared-memory map (bytes)
 constexpr uint32_t kChunkA = kM * 16;                 // one 8-wide K chunk of a 128-row A tile
 constexpr uint32_t kA1Bytes = 20 * kChunkA;           // K = 32 (obs, ones, pad) + 128 (history)
-constexpr uint32_t kA2Bytes = 8 * kChunkA;            // K = 64
 constexpr uint32_t kW1oBytes = 4 * kHid * 16;         // K = 32 x N = 64, K-major
 constexpr uint32_t kW1hBytes = 8 * (8 * kMaxHist * 16);  // MN-major: 8 N-groups x 2*4*N_H K-rows
 constexpr uint32_t kW2Bytes = 10 * kHid * 16;         // K = 80 x N = 64, K-major
 constexpr uint32_t kW3Bytes = 10 * 16 * 16;           // K = 80 x N = 16, K-major
-constexpr uint32_t kOnesBytes = 2 * kChunkA;          // A K16 slice: column 0 = 1
 
 constexpr uint32_t OFF_A1 = 0;
-constexpr uint32_t OFF_A2 = OFF_A1 + kTiles * kA1Bytes;
-constexpr uint32_t OFF_W1O = OFF_A2 + (kA2InTmem ? 0u : kTiles * kA2Bytes);
+constexpr uint32_t OFF_W1O = OFF_A1 + kTiles * kA1Bytes;
 constexpr uint32_t OFF_W1H = OFF_W1O + kW1oBytes;
 constexpr uint32_t OFF_W2 = OFF_W1H + kW1hBytes;
 constexpr uint32_t OFF_W3 = OFF_W2 + kW2Bytes;
-constexpr uint32_t OFF_ONES = OFF_W3 + kW3Bytes;
-constexpr uint32_t OFF_BAR = OFF_ONES + kOnesBytes;   // kTiles MMA-done mbarriers
+constexpr uint32_t OFF_BAR = OFF_W3 + kW3Bytes;       // kTiles MMA-done mbarriers
 constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * kTiles;
 constexpr uint32_t OFF_STAT = (OFF_TMEM + 8 + 127) & ~127u;  // reset scratch (32 uint4 per warp); reused by stats
 constexpr uint32_t kScratchBytes = (kThreads / 32) * kResetScratch * 16;
@@ -108,10 +102,6 @@ __device__ void stage_weights(const PolicyDev& W, uint32_t sbase, int n_hist)
         if (n < 4) v = k < 64 ? h16(W.W3, n * 64 + k) : (k == 64 ? h16(W.b3, n) : (uint16_t)0);
         st_u16(sbase + OFF_W3 + (k / 8) * (16 * 16) + n * 16 + (k % 8) * 2, v);
     }
-    for (int r = tid; r < kM; r += blockDim.x) {  // ones column
-        tc::sts128(sbase + OFF_ONES + r * 16, 0x3C00u, 0u, 0u, 0u);
-        tc::sts128(sbase + OFF_ONES + kChunkA + r * 16, 0u, 0u, 0u, 0u);
-    }
 }
 
 __device__ __forceinline__ float tanh_fast(float z)
@@ -121,8 +111,8 @@ __device__ __forceinline__ float tanh_fast(float z)
 }
 
 struct TileCtx {
-    uint32_t a1_row, a2_row;  // this thread's row in the A1 / A2 tiles
-    uint32_t a1, a2;          // tile bases
+    uint32_t a1_row;          // this thread's row in the A1 tile
+    uint32_t a1;              // A1 tile base
     uint32_t mbar;
     uint32_t tmem_row;        // TMEM address of (this thread's lane, tile column 0)
     uint32_t tmem_tile;       // TMEM address of (lane 0, tile column 0)
@@ -134,32 +124,19 @@ struct TileCtx {
     bool leader;
 };
 
-// Epilogue of L1 / L2: accumulator row -> relu -> fp16 -> A2 row (TMEM or shared memory).
+// Epilogue of L1 / L2: accumulator row -> relu -> fp16 -> this thread's A2 row in TMEM.
 __device__ __forceinline__ void epilogue_hidden(const TileCtx& c)
 {
-    if constexpr (kA2InTmem) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            uint32_t v[16];
-            tc::tmem_ld16(c.tmem_row + 16 * q, v);
-            tc::tmem_wait_ld();
-            tc::tmem_st8u(c.a2_trow + 8 * q, tc::relu_pack(v[0], v[1]), tc::relu_pack(v[2], v[3]),
-                          tc::relu_pack(v[4], v[5]), tc::relu_pack(v[6], v[7]), tc::relu_pack(v[8], v[9]),
-                          tc::relu_pack(v[10], v[11]), tc::relu_pack(v[12], v[13]), tc::relu_pack(v[14], v[15]));
-        }
-        tc::tmem_wait_st();
-    } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            uint32_t v[16];
-            tc::tmem_ld16(c.tmem_row + 16 * q, v);
-            tc::tmem_wait_ld();
-            tc::sts128(c.a2_row + (2 * q) * kChunkA, tc::relu_pack(v[0], v[1]), tc::relu_pack(v[2], v[3]),
-                       tc::relu_pack(v[4], v[5]), tc::relu_pack(v[6], v[7]));
-            tc::sts128(c.a2_row + (2 * q + 1) * kChunkA, tc::relu_pack(v[8], v[9]), tc::relu_pack(v[10], v[11]),
-                       tc::relu_pack(v[12], v[13]), tc::relu_pack(v[14], v[15]));
-        }
+    for (int q = 0; q < 4; ++q) {
+        uint32_t v[16];
+        tc::tmem_ld16(c.tmem_row + 16 * q, v);
+        tc::tmem_wait_ld();
+        tc::tmem_st8u(c.a2_trow + 8 * q, tc::relu_pack(v[0], v[1]), tc::relu_pack(v[2], v[3]),
+                      tc::relu_pack(v[4], v[5]), tc::relu_pack(v[6], v[7]), tc::relu_pack(v[8], v[9]),
+                      tc::relu_pack(v[10], v[11]), tc::relu_pack(v[12], v[13]), tc::relu_pack(v[14], v[15]));
     }
+    tc::tmem_wait_st();
 }
 
 // The tile's 128 threads hand their freshly written A rows (and finished TMEM reads) to the
@@ -192,19 +169,19 @@ template <class Hook>
 __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist, uint32_t rot, float a[4],
                                          const Hook& hook)
 {
-    const uint32_t hk = 4u * (uint32_t)n_hist;
+    // descriptors = base descriptor + (byte offset >> 4) in the start-address field (addresses
+    // stay below 256 KB, so the 14-bit field never carries)
     handoff_to_mma(c);
     if (c.leader) {
         tc::fence_after();
-        // L1: obs part (K = 32) then history (K = 4 N_H), D = tile columns [0, 64)
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-            tc::mma_f16(c.tmem_tile, tc::make_desc(c.a1 + 2 * j * kChunkA, kChunkA, 128),
-                        tc::make_desc(sbase + OFF_W1O + 2 * j * (kHid * 16), kHid * 16, 128), kIdescN64, j);
+        const uint64_t dA1 = tc::make_desc(c.a1, kChunkA, 128);
+        const uint64_t dW1o = tc::make_desc(sbase + OFF_W1O, kHid * 16, 128);
+        const uint64_t dW1h = tc::make_desc(sbase + OFF_W1H, 128, 2u * 4u * (uint32_t)n_hist * 16u) + 4u * rot;
+        // L1: obs part (K = 32) then history (K = 4 N_H) with the rotated W1 history block
+        tc::mma_f16(c.tmem_tile, dA1, dW1o, kIdescN64, 0);
+        tc::mma_f16(c.tmem_tile, dA1 + 2 * kChunkA / 16, dW1o + 2 * (kHid * 16) / 16, kIdescN64, 1);
         for (int j = 0; j < n_hist / 4; ++j)
-            tc::mma_f16(c.tmem_tile, tc::make_desc(c.a1 + (4 + 2 * j) * kChunkA, kChunkA, 128),
-                        tc::make_desc(sbase + OFF_W1H + (16u * j + 4u * rot) * 16u, 128, 2u * hk * 16u),
-                        kIdescN64BMN, 1);
+            tc::mma_f16(c.tmem_tile, dA1 + (4 + 2 * j) * (kChunkA / 16), dW1h + 16u * j, kIdescN64BMN, 1);
         tc::commit(c.mbar);
     }
     hook(1);
@@ -213,19 +190,10 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
     handoff_to_mma(c);
     if (c.leader) {
         tc::fence_after();
-        if constexpr (kA2InTmem) {
+        const uint64_t dW2 = tc::make_desc(sbase + OFF_W2, kHid * 16, 128);
 #pragma unroll
-            for (int j = 0; j < 5; ++j)  // j = 4: the ones column (bias row of W2)
-                tc::mma_f16_ts(c.tmem_tile, c.a2_tmem + 8 * j,
-                               tc::make_desc(sbase + OFF_W2 + 2 * j * (kHid * 16), kHid * 16, 128), kIdescN64, j);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                tc::mma_f16(c.tmem_tile, tc::make_desc(c.a2 + 2 * j * kChunkA, kChunkA, 128),
-                            tc::make_desc(sbase + OFF_W2 + 2 * j * (kHid * 16), kHid * 16, 128), kIdescN64, j);
-            tc::mma_f16(c.tmem_tile, tc::make_desc(sbase + OFF_ONES, kChunkA, 128),
-                        tc::make_desc(sbase + OFF_W2 + 8 * (kHid * 16), kHid * 16, 128), kIdescN64, 1);
-        }
+        for (int j = 0; j < 5; ++j)  // A from TMEM; j = 4: the ones column (bias row of W2)
+            tc::mma_f16_ts(c.tmem_tile, c.a2_tmem + 8 * j, dW2 + j * (2 * kHid * 16 / 16), kIdescN64, j);
         tc::commit(c.mbar);
     }
     hook(2);
@@ -234,19 +202,10 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
     handoff_to_mma(c);
     if (c.leader) {
         tc::fence_after();
-        if constexpr (kA2InTmem) {
+        const uint64_t dW3 = tc::make_desc(sbase + OFF_W3, 256, 128);
 #pragma unroll
-            for (int j = 0; j < 5; ++j)
-                tc::mma_f16_ts(c.tmem_tile, c.a2_tmem + 8 * j, tc::make_desc(sbase + OFF_W3 + 2 * j * 256, 256, 128),
-                               kIdescN16, j);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                tc::mma_f16(c.tmem_tile, tc::make_desc(c.a2 + 2 * j * kChunkA, kChunkA, 128),
-                            tc::make_desc(sbase + OFF_W3 + 2 * j * 256, 256, 128), kIdescN16, j);
-            tc::mma_f16(c.tmem_tile, tc::make_desc(sbase + OFF_ONES, kChunkA, 128),
-                        tc::make_desc(sbase + OFF_W3 + 8 * 256, 256, 128), kIdescN16, 1);
-        }
+        for (int j = 0; j < 5; ++j)
+            tc::mma_f16_ts(c.tmem_tile, c.a2_tmem + 8 * j, dW3 + j * (2 * 256 / 16), kIdescN16, j);
         tc::commit(c.mbar);
     }
     hook(3);
@@ -330,19 +289,16 @@ __device__ __forceinline__ TileCtx make_ctx(uint32_t sbase)
     const uint32_t tbase = *reinterpret_cast<const uint32_t*>(smem + OFF_TMEM);
     TileCtx c;
     c.a1 = sbase + OFF_A1 + g * kA1Bytes;
-    c.a2 = sbase + OFF_A2 + g * kA2Bytes;
     c.a1_row = c.a1 + r * 16;
-    c.a2_row = c.a2 + r * 16;
     c.mbar = sbase + OFF_BAR + 8 * g;
     c.tmem_tile = tbase + 64 * g;
     c.tmem_row = c.tmem_tile + ((uint32_t)(32 * (r / 32)) << 16);
     c.stash_row = tbase + kStashCol + 24 * g + ((uint32_t)(32 * (r / 32)) << 16);
     c.a2_tmem = tbase + kA2Col + 40 * g;
     c.a2_trow = c.a2_tmem + ((uint32_t)(32 * (r / 32)) << 16);
-    if constexpr (kA2InTmem) {  // constant ones column (K index 64 of layers 2 and 3) + zero pad
-        tc::tmem_st8u(c.a2_trow + 32, 0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u);
-        tc::tmem_wait_st();
-    }
+    // constant ones column (K index 64 of layers 2 and 3) + zero pad
+    tc::tmem_st8u(c.a2_trow + 32, 0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u);
+    tc::tmem_wait_st();
     c.bar_id = 1 + g;
     c.phase = 0;
     c.leader = (r == 0);

@@ -404,32 +404,3 @@ def test_c3_full_size_sampled(pkg):
             sp2 = e[0]["s"] if so.flags & oracle.FLAG_RESET else sp
             assert np.all(close_step(after["state"][:, i], e[0]["s"], sp2)), i
 
-
-def test_step_bulk_path_equals_plain_path(pkg):
-    """The cp.async.bulk-staged l2f_step (L2F_STEP_PATH=bulk, used when N % 4 == 0 and no
-    final_state/obs_dense output) and the plain per-thread kernel (taken when final_state is
-    requested) run the same device arithmetic: bitwise equal state, history, outputs."""
-    import os
-    if os.environ.get("L2F_STEP_PATH", "plain")[0] != "b":
-        pytest.skip("bulk path not selected (run with L2F_STEP_PATH=bulk)")
-    cfg = inputs.config_c3()
-    n = 4 * 1000 + 4 * 37  # ragged last tile, multiple of 4
-    acts = [dev_actions(inputs.actions_near_hover(1, n, seed=40 + k)[0]) for k in range(6)]
-    res = []
-    for plain in (False, True):
-        env = pkg.Env(cfg, n)
-        env.reset()
-        outs = []
-        for k in range(6):
-            o = env.make_out(final_state=plain)
-            env.step(acts[k], o)
-            outs.append({kk: v.cpu().numpy() for kk, v in o.items() if v is not None and kk != "final_state"})
-        res.append((snapshot(env), outs, env.episode_stats().cpu().numpy()))
-    (s1, o1, st1), (s2, o2, st2) = res
-    for k in s1:
-        assert np.array_equal(s1[k], s2[k]), k
-    for a, b in zip(o1, o2):
-        for k in a:
-            assert np.array_equal(a[k], b[k]), k
-    assert np.array_equal(st1[[0, 1, 2, 3, 4, 7]], st2[[0, 1, 2, 3, 4, 7]])
-    assert np.allclose(st1, st2, rtol=1e-12)
