@@ -384,7 +384,25 @@ def secondary(pkg, inputs, torch, dev, pk, f_clk):
     el = (time.perf_counter() - t0) / 20
     out["C3_step_api"]["e2e"] = {"value": n / el, "unit": "env-steps/s", "h2d_bytes_per_step": 16 * n,
                                  "d2h_bytes_per_step": 77 * n}
-    del env, acts, o
+    # f2: reward recalculation over a device replay buffer of 2^24 transitions,
+    # HBM-bound: s' 68 B + a' 16 B read, r 4 B written per transition
+    m = 1 << 24
+    g = torch.Generator(device=dev).manual_seed(5)
+    sbuf = torch.rand(17, m, device=dev, generator=g) - 0.5
+    abuf = torch.rand(4, m, device=dev, generator=g) * 2 - 1
+    env.recompute_rewards(0, sbuf, abuf)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(10):
+        env.recompute_rewards(250000, sbuf, abuf)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    gbs = 88 * m / (ms / 1e3) / 1e9
+    out["recompute_rewards"] = {"value": m / (ms / 1e3), "unit": "transitions/s", "ms": ms,
+                                "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                                             "frac": gbs / pk["hbm_gbs"], "bytes_per_transition": 88}}
+    del env, acts, o, sbuf, abuf
     torch.cuda.empty_cache()
     # open-loop dynamics-only mode (paper-comparable): 2^20 envs x 1000 steps, flags 0
     cfg = inputs.config_c1()
@@ -402,6 +420,20 @@ def secondary(pkg, inputs, torch, dev, pk, f_clk):
     out["open_loop_dynamics"] = {"value": rate, "unit": "env-steps/s", "ms": ms,
                                  "workload": "2^20 envs x 1000 steps, Philox random actions, no noise/termination",
                                  "vs_paper_T2000": rate / 1.284e9}
+    del env
+    # the full C5 env step without the actor MLP (Philox random actions), for the MLP's share
+    n = 1 << 21
+    env = pkg.Env(inputs.config_c5(), n, device=dev)
+    env.reset()
+    env.rollout(20)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    env.rollout(200)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    out["open_loop_c5_features"] = {"value": n * 200 / (ms / 1e3), "unit": "env-steps/s", "ms": ms,
+                                    "workload": "2^21 envs x 200 steps, C5 features, Philox random actions"}
     del env
     torch.cuda.empty_cache()
     return out

@@ -47,7 +47,7 @@ extern "C" {
 #define L2F_API
 #endif
 
-#define L2F_ABI_VERSION 1
+#define L2F_ABI_VERSION 2
 #define L2F_STATE_DIM 17     /* p(3) q(4: w,x,y,z) v(3) omega(3) omega_m(4) */
 #define L2F_OBS_CORE 18      /* p(3) R(9, row-major) v(3) omega(3) */
 #define L2F_MAX_HIST 32      /* N_H upper bound                                  */
@@ -74,7 +74,10 @@ enum {
     L2F_TERMINATION = 1u << 2,    /* box / speed termination (Q14)                   */
     L2F_AUTO_RESET = 1u << 3,     /* same-step reset of ended envs (Q16)                    */
     L2F_DISTURBANCE = 1u << 4,    /* per-episode random force/torque                */
-    L2F_DOMAIN_RAND = 1u << 5     /* per-episode mass/inertia/thrust factors (Q19)          */
+    L2F_DOMAIN_RAND = 1u << 5,    /* per-episode mass/inertia/thrust factors (Q19)          */
+    L2F_NO_ROTOR_DELAY = 1u << 6  /* ablation (Table II "Rotor Delay"): the rotor
+                                     speeds are set to the setpoint at the start of each step
+                                      instead of following the first-order lag       */
 };
 
 /* Per-env step flags (l2f_step_out.flags, trace field 26). */
@@ -148,6 +151,8 @@ typedef struct {
     float* reward;      /* [N] */
     uint8_t* flags;     /* [N] L2F_DONE_* bits */
     float* final_state; /* [17][N]: s' before any auto-reset */
+    float* obs_critic;  /* [28][N]: privileged critic observation {p, R, v, omega, omega_m, f_r,
+                           tau_r}, noise-free, of the same state as obs_core */
 } l2f_step_out;
 
 /* Actor MLP in_dim -> hidden -> hidden -> 4 (BASELINE configs[3]; Q21): ReLU hidden layers,
@@ -222,6 +227,13 @@ L2F_API l2f_status l2f_rollout(l2f_env* env, const l2f_policy* policy, const flo
 /* Reduces the episode statistics accumulated since the last reset of the accumulators into
  * d_out[8] (FP64, fixed-order, deterministic).  reset_accumulators != 0 zeroes them. */
 L2F_API l2f_status l2f_episode_stats(l2f_env* env, double* d_out, int32_t reset_accumulators, void* stream);
+
+/* Reward recalculation over a replay buffer: rewards of M stored transitions
+ * (s' [17][M], applied action a' [4][M], device) under the curriculum stage of step t
+ * (P:152), into d_rewards [M].  Bitwise equal to the reward l2f_step returned for the same
+ * (s', a', stage); 0 for a non-finite s' (Q26).  Uses only env's config (no env state). */
+L2F_API l2f_status l2f_recompute_rewards(const l2f_env* env, uint64_t t, const float* d_next_state,
+                                         const float* d_actions, int64_t m, float* d_rewards, void* stream);
 
 /* ---- host-buffer entry points (end-to-end; synchronise the stream before returning) --- */
 

@@ -18,6 +18,7 @@ import math
 import numpy as np
 
 OBS_NOISE, ACTION_NOISE, TERMINATION, AUTO_RESET, DISTURBANCE, DOMAIN_RAND = (1, 2, 4, 8, 16, 32)
+NO_ROTOR_DELAY = 64  # ablation switch (Table II "Rotor Delay")
 ALL_NO_DR = OBS_NOISE | ACTION_NOISE | TERMINATION | AUTO_RESET | DISTURBANCE
 
 # Crazyflie 2.1-style defaults.  Paper values: m = 27 g, T_m = 0.15 s, dt = 0.01 s

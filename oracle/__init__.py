@@ -23,7 +23,8 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 
 # flags / indices (mirrors of the C enums)
-OBS_NOISE, ACTION_NOISE, TERMINATION, AUTO_RESET, DISTURBANCE, DOMAIN_RAND = (1, 2, 4, 8, 16, 32)
+OBS_NOISE, ACTION_NOISE, TERMINATION, AUTO_RESET, DISTURBANCE, DOMAIN_RAND, NO_ROTOR_DELAY = (1, 2, 4, 8, 16, 32,
+                                                                                   64)
 FLAG_TERMINATED, FLAG_TRUNCATED, FLAG_DIVERGED, FLAG_RESET = 1, 2, 4, 8
 STATS = ["episodes", "terminated", "truncated", "diverged", "sum_len", "sum_ret", "sum_ret_sq",
          "env_steps"]
@@ -112,6 +113,9 @@ def lib():
         L.or_reset.argtypes = [C.POINTER(Config), C.c_uint64, C.c_uint64, C.c_void_p]
         L.or_observe.argtypes = [C.POINTER(Config), C.c_void_p, C.c_uint64, C.c_uint64, dp]
         L.or_mlp.argtypes = [C.POINTER(Policy), dp, dp]
+        L.or_critic_observe.argtypes = [C.c_void_p, dp]
+        L.or_recompute_reward.restype = C.c_double
+        L.or_recompute_reward.argtypes = [C.POINTER(Config), C.c_int64, dp, dp]
         L.or_mlp_min_midpoint_margin.restype = C.c_double
         L.or_mlp_min_midpoint_margin.argtypes = [C.POINTER(Policy), dp]
         L.or_env_step.argtypes = [C.POINTER(Config), C.c_void_p, C.c_uint64, C.c_uint64, dp,
@@ -306,6 +310,18 @@ def observe(cfg: dict, env: np.ndarray, env_id: int, t: int) -> np.ndarray:
     c = config(cfg)
     lib().or_observe(C.byref(c), e.ctypes.data, int(env_id), int(t), _dp(obs))
     return obs
+
+
+def critic_observe(env: np.ndarray) -> np.ndarray:
+    e = np.ascontiguousarray(np.asarray(env, dtype=ENV_DTYPE).reshape(1))
+    obs = np.zeros(28)
+    lib().or_critic_observe(e.ctypes.data, _dp(obs))
+    return obs
+
+
+def recompute_reward(cfg: dict, t: int, s1, a) -> float:
+    c = config(cfg)
+    return lib().or_recompute_reward(C.byref(c), int(t), _dp(_d(s1)), _dp(_d(a)))
 
 
 class PolicyHandle:

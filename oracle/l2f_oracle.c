@@ -65,6 +65,7 @@ enum {
     OR_AUTO_RESET = 1u << 3,
     OR_DISTURBANCE = 1u << 4,
     OR_DOMAIN_RAND = 1u << 5,
+    OR_NO_ROTOR_DELAY = 1u << 6, /* ablation, Table II "Rotor Delay" */
 };
 
 enum { OR_FLAG_TERMINATED = 1, OR_FLAG_TRUNCATED = 2, OR_FLAG_DIVERGED = 4, OR_FLAG_RESET = 8 };
@@ -456,6 +457,33 @@ void or_observe(const or_config* cfg, const or_env* e, uint64_t env_id, uint64_t
         for (int i = 0; i < 4; ++i) obs[18 + 4 * k + i] = e->hist[k][i];
 }
 
+/* Privileged critic observation o_c = {p, R, v, omega, omega_m, f_r, tau_r}, 28-D,
+ * ground truth without noise. */
+void or_critic_observe(const or_env* e, double* obs)
+{
+    double R[9];
+    or_rotation(e->s + 3, R);
+    for (int j = 0; j < 3; ++j) obs[j] = e->s[j];
+    for (int j = 0; j < 9; ++j) obs[3 + j] = R[j];
+    for (int j = 0; j < 3; ++j) obs[12 + j] = e->s[7 + j];
+    for (int j = 0; j < 3; ++j) obs[15 + j] = e->s[10 + j];
+    for (int j = 0; j < 4; ++j) obs[18 + j] = e->s[13 + j];
+    for (int j = 0; j < 3; ++j) obs[22 + j] = e->dist[j];
+    for (int j = 0; j < 3; ++j) obs[25 + j] = e->dist[3 + j];
+}
+
+/* Reward recalculation of a stored transition: the reward of (s', a') under the
+ * curriculum stage of step t; 0 for a non-finite s' (Q26). */
+double or_recompute_reward(const or_config* cfg, int64_t t, const double s1[17], const double a[4])
+{
+    or_weights w;
+    double sg;
+    for (int i = 0; i < 17; ++i)
+        if (!isfinite(s1[i])) return 0.0;
+    or_stage(cfg, t, &w, &sg);
+    return or_reward(&w, s1, a);
+}
+
 /* ------------------------------------------------------------------------------------ */
 /* Actor MLP (architecture from BASELINE configs[3]; precision Q21).        */
 /* h1 = relu(W1 q16(o) + b1); h2 = relu(W2 q16(h1) + b2); a = tanh(W3 q16(h2) + b3).      */
@@ -545,6 +573,10 @@ void or_env_step(const or_config* cfg, or_env* e, uint64_t env_id, uint64_t t,
     /* 2. action -> RPM setpoints */
     double u[4];
     for (int i = 0; i < 4; ++i) u[i] = or_action_to_rpm(&cfg->nominal, a[i]);
+
+    /* ablation without rotor delay: the motors reach the setpoint instantly */
+    if (cfg->flags & OR_NO_ROTOR_DELAY)
+        for (int i = 0; i < 4; ++i) e->s[13 + i] = u[i];
 
     /* 3-4. RK4 + projection (Q1, Q5) */
     or_params P;

@@ -125,9 +125,11 @@ class Env:
     def t(self, value: int):
         _check(lib().l2f_set_t(self.h, int(value)), "l2f_set_t")
 
-    def make_out(self, obs_core=True, reward=True, flags=True, final_state=False, obs_dense=False):
+    def make_out(self, obs_core=True, reward=True, flags=True, final_state=False, obs_dense=False,
+                 obs_critic=False):
         d = self.device
         return {
+            "obs_critic": torch.empty(28, self.n, device=d) if obs_critic else None,
             "obs_core": torch.empty(18, self.n, device=d) if obs_core else None,
             "reward": torch.empty(self.n, device=d) if reward else None,
             "flags": torch.empty(self.n, device=d, dtype=torch.uint8) if flags else None,
@@ -139,7 +141,7 @@ class Env:
         if out is None:
             return None
         o = lib().StepOut()
-        for k in ("obs_core", "obs_dense", "reward", "flags", "final_state"):
+        for k in ("obs_core", "obs_dense", "reward", "flags", "final_state", "obs_critic"):
             t = out.get(k)
             if t is not None:
                 assert t.is_cuda and t.is_contiguous()
@@ -172,6 +174,17 @@ class Env:
         _check(lib().l2f_rollout(self.h, C.byref(policy.s) if policy is not None else None, _ptr(actions), int(T),
                                  _ptr(trace), _ptr(trace_ids), K, _stream(stream)), "l2f_rollout")
         return trace
+
+    def recompute_rewards(self, t: int, next_state: torch.Tensor, actions: torch.Tensor, stream=None):
+        """Rewards of stored transitions (s' [17][M], a' [4][M]) under the curriculum stage of
+        step t (P:231 reward recalculation)."""
+        assert next_state.is_cuda and actions.is_cuda and next_state.shape[0] == 17 and actions.shape[0] == 4
+        m = next_state.shape[1]
+        assert actions.shape[1] == m and next_state.is_contiguous() and actions.is_contiguous()
+        out = torch.empty(m, device=next_state.device)
+        _check(lib().l2f_recompute_rewards(self.h, int(t), _ptr(next_state), _ptr(actions), m, _ptr(out),
+                                           _stream(stream)), "l2f_recompute_rewards")
+        return out
 
     def episode_stats(self, reset: bool = False, stream=None) -> torch.Tensor:
         out = torch.empty(STATS_LEN, dtype=torch.float64, device=self.device)

@@ -7,13 +7,13 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libl2f.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 STATE_DIM, OBS_CORE, MAX_HIST, STATS_LEN, TRACE_FIELDS = 17, 18, 32, 8, 32
 DONE_TERMINATED, DONE_TRUNCATED, DONE_DIVERGED, DONE_RESET = 1, 2, 4, 8
 STATS = ["episodes", "terminated", "truncated", "diverged", "sum_len", "sum_ret", "sum_ret_sq", "env_steps"]
 EXPORTS = ["l2f_workspace_size", "l2f_create", "l2f_destroy", "l2f_reset", "l2f_step", "l2f_rollout",
            "l2f_episode_stats", "l2f_step_host", "l2f_rollout_host", "l2f_get_state", "l2f_set_t",
-           "l2f_policy_forward", "l2f_selftest_philox", "l2f_launch_count", "l2f_last_error", "l2f_abi_version"]
+           "l2f_policy_forward", "l2f_recompute_rewards", "l2f_selftest_philox", "l2f_launch_count", "l2f_last_error", "l2f_abi_version"]
 
 
 class L2FError(RuntimeError):
@@ -51,7 +51,7 @@ class Config(C.Structure):
 
 class StepOut(C.Structure):
     _fields_ = [("obs_core", C.c_void_p), ("obs_dense", C.c_void_p), ("reward", C.c_void_p),
-                ("flags", C.c_void_p), ("final_state", C.c_void_p)]
+                ("flags", C.c_void_p), ("final_state", C.c_void_p), ("obs_critic", C.c_void_p)]
 
 
 class PolicyS(C.Structure):
@@ -140,6 +140,7 @@ def lib():
         L.l2f_get_state.argtypes = [vp, C.POINTER(StateView)]
         L.l2f_set_t.argtypes = [vp, C.c_uint64]
         L.l2f_policy_forward.argtypes = [C.POINTER(PolicyS), vp, vp, C.c_int64, vp]
+        L.l2f_recompute_rewards.argtypes = [vp, C.c_uint64, vp, vp, C.c_int64, vp, vp]
         L.l2f_selftest_philox.argtypes = [C.c_int64, C.c_uint64, C.c_uint32, vp, vp, vp]
         L.l2f_launch_count.restype = C.c_uint64
         L.l2f_launch_count.argtypes = []

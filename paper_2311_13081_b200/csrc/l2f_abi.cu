@@ -252,13 +252,14 @@ bool params_for(const l2f_env* e, uint64_t t0, int64_t T, DevParams& P)
 
 StepOutDev to_dev(const l2f_step_out* o)
 {
-    StepOutDev d{nullptr, nullptr, nullptr, nullptr, nullptr};
+    StepOutDev d{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     if (o) {
         d.obs_core = o->obs_core;
         d.obs_dense = o->obs_dense;
         d.reward = o->reward;
         d.flags = o->flags;
         d.final_state = o->final_state;
+        d.obs_critic = o->obs_critic;
     }
     return d;
 }
@@ -519,6 +520,18 @@ l2f_status l2f_policy_forward(const l2f_policy* policy, const float* d_obs, floa
     cudaError_t e = launch_policy_forward(W, d_obs, d_act, n, (cudaStream_t)stream);
     if (e == cudaErrorNotSupported) return fail(L2F_ERR_NOT_SUPPORTED, "policy_forward not supported");
     return launched(e, "l2f_policy_forward");
+}
+
+l2f_status l2f_recompute_rewards(const l2f_env* env, uint64_t t, const float* d_next_state, const float* d_actions,
+                                 int64_t m, float* d_rewards, void* stream)
+{
+    if (!env || !d_next_state || !d_actions || !d_rewards || m <= 0)
+        return fail(L2F_ERR_INVALID_ARGUMENT, "bad recompute_rewards arguments");
+    const int64_t I = env->cfg.curriculum.interval;
+    const int64_t k = I > 0 ? (int64_t)(t / (uint64_t)I) : 0;
+    const StageW W = stage_weights(env->cfg, k);
+    return launched(launch_recompute_rewards(W, d_next_state, d_actions, m, d_rewards, (cudaStream_t)stream),
+                    "l2f_recompute_rewards");
 }
 
 l2f_status l2f_selftest_philox(int64_t n, uint64_t seed, uint32_t t, uint32_t* d_ours, uint32_t* d_curand,

@@ -26,6 +26,7 @@ enum : uint32_t {
     F_AUTO_RESET = 1u << 3,
     F_DISTURBANCE = 1u << 4,
     F_DOMAIN_RAND = 1u << 5,
+    F_NO_ROTOR_DELAY = 1u << 6,  // ablation (Table II "Rotor Delay"): w_m set to the setpoint
 };
 enum : uint32_t { D_TERM = 1, D_TRUNC = 2, D_DIV = 4, D_RESET = 8 };
 enum : uint32_t { S_ACT = 1, S_OBS = 2, S_RESET = 3, S_DIST = 4, S_DR = 5, S_RAND_ACT = 6 };
@@ -280,6 +281,16 @@ __device__ __forceinline__ void deriv(const DevParams& P, const Phys& ph, const 
 // an IEEE fma/add like the scalar instruction) in 7 pairs.  Position: with p' = v and stage
 // velocities v1 = v, v2 = v + h/2 a1, v3 = v + h/2 a2, v4 = v + h a3, the RK4 combination
 // h/6 (v1 + 2 v2 + 2 v3 + v4) equals h v + h^2/6 (a1 + a2 + a3) exactly.
+// Any NaN/Inf component makes the sum non-finite (a finite overflow to inf also counts:
+// |x| > 1e38 is divergence in any sense).  Checked on the projected state s'.
+__device__ __forceinline__ bool state_finite(const float* s)
+{
+    float sum = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kStateDim; ++i) sum += s[i];
+    return isfinite(sum);
+}
+
 __device__ __forceinline__ void pair_fma(const float* a, float h, const float* b, float* out)
 {
     const float2 hh = make_float2(h, h);
@@ -330,15 +341,9 @@ __device__ __forceinline__ bool rk4_step(const DevParams& P, const Phys& ph, con
     const float inv = rsqrtf(n2);
 #pragma unroll
     for (int i = 3; i < 7; ++i) s[i] *= inv;
-    // any NaN/Inf component makes the sum non-finite (finite overflow to inf also counts as
-    // diverged, |x| > 1e38 is divergence in any sense)
-    float sum = 0.0f;
-#pragma unroll
-    for (int i = 0; i < kStateDim; ++i) sum += s[i];
-    const bool bad = !isfinite(sum);
 #pragma unroll
     for (int i = 13; i < 17; ++i) s[i] = fminf(fmaxf(s[i], P.rpm_min), P.rpm_max);
-    return bad;
+    return !state_finite(s);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -366,6 +371,52 @@ __device__ __forceinline__ void action_noise(const DevParams& P, uint32_t gid, u
     }
 }
 
+// Reward r(s, a, s') on the post-transition state (Q12): the same function serves
+// the step and the replay-buffer recalculation (l2f_recompute_rewards).
+__device__ __forceinline__ float reward_of(const StageW& W, const float* s, const float a[4])
+{
+    const float pp = s[0] * s[0] + s[1] * s[1] + s[2] * s[2];
+    const float vv = s[7] * s[7] + s[8] * s[8] + s[9] * s[9];
+    const float ww = s[10] * s[10] + s[11] * s[11] + s[12] * s[12];
+    float aa = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float d = a[i] - W.C_rab[i];
+        aa = fmaf(d, d, aa);
+    }
+    float r = W.C_rs;
+    r = fmaf(-W.C_rp, pp, r);
+    r = fmaf(-W.C_rq, fmaf(-s[3], s[3], 1.0f), r);
+    r = fmaf(-W.C_rv, vv, r);
+    r = fmaf(-W.C_rw, ww, r);
+    r = fmaf(-W.C_ra, aa, r);
+    return r;
+}
+
+// Privileged critic observation o_c = {p, R, v, w, w_m, f_r, tau_r}, 28-D, noise-free
+// (P:137-139).
+constexpr int kObsCritic = 28;
+__device__ __forceinline__ void observe_critic(const float* s, const float* dist, float o[kObsCritic])
+{
+    const float qw = s[3], qx = s[4], qy = s[5], qz = s[6];
+    o[0] = s[0];
+    o[1] = s[1];
+    o[2] = s[2];
+    o[3] = 1.0f - 2.0f * (qy * qy + qz * qz);
+    o[4] = 2.0f * (qx * qy - qw * qz);
+    o[5] = 2.0f * (qx * qz + qw * qy);
+    o[6] = 2.0f * (qx * qy + qw * qz);
+    o[7] = 1.0f - 2.0f * (qx * qx + qz * qz);
+    o[8] = 2.0f * (qy * qz - qw * qx);
+    o[9] = 2.0f * (qx * qz - qw * qy);
+    o[10] = 2.0f * (qy * qz + qw * qx);
+    o[11] = 1.0f - 2.0f * (qx * qx + qy * qy);
+#pragma unroll
+    for (int j = 0; j < 10; ++j) o[12 + j] = s[7 + j];  // v, w, w_m
+#pragma unroll
+    for (int j = 0; j < 6; ++j) o[22 + j] = dist[j];
+}
+
 // W: the curriculum stage of step t (stage_of), hoisted by the callers' stage loops.
 // kDR: per-env domain-randomised parameters (compile-time so the DR-free path keeps the
 // nominal parameters in the constant bank instead of registers).
@@ -381,27 +432,18 @@ __device__ __forceinline__ void transition(const DevParams& P, const StageW& W, 
         o.a[i] = fminf(fmaxf(v, -1.0f), 1.0f);
         u[i] = fmaf(o.a[i] + 1.0f, P.rpm_half_span, P.rpm_min);
     }
+    if (P.flags & F_NO_ROTOR_DELAY) {  // ablation: rotors reach the setpoint instantly
+#pragma unroll
+        for (int i = 0; i < 4; ++i) e.s[13 + i] = u[i];
+    }
     Phys ph;
     make_phys<kDR>(P, e, u, ph);
     const bool div = rk4_step(P, ph, e.dist, e.s);
 
     const float* s = e.s;
-    const float pp = s[0] * s[0] + s[1] * s[1] + s[2] * s[2];
     const float vv = s[7] * s[7] + s[8] * s[8] + s[9] * s[9];
     const float ww = s[10] * s[10] + s[11] * s[11] + s[12] * s[12];
-    float aa = 0.0f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float d = o.a[i] - W.C_rab[i];
-        aa = fmaf(d, d, aa);
-    }
-    float r = W.C_rs;
-    r = fmaf(-W.C_rp, pp, r);
-    r = fmaf(-W.C_rq, fmaf(-s[3], s[3], 1.0f), r);
-    r = fmaf(-W.C_rv, vv, r);
-    r = fmaf(-W.C_rw, ww, r);
-    r = fmaf(-W.C_ra, aa, r);
-    if (div) r = 0.0f;  // Q26
+    const float r = div ? 0.0f : reward_of(W, s, o.a);  // Q26
     bool term = div;
     if (P.flags & F_TERMINATION) {
         const float pinf = fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2])));

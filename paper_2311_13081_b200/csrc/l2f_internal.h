@@ -15,6 +15,7 @@ struct StepOutDev {
     float* reward;
     uint8_t* flags;
     float* final_state;
+    float* obs_critic;  // [28][N] privileged critic observation (NEXT f1)
 };
 
 // Actor MLP parameters on the device (fp16 bits, row-major [out][in]).
@@ -33,6 +34,8 @@ cudaError_t launch_rollout_open(const DevParams& P, const DevBufs& B, const floa
                                 const int64_t* trace_ids, int32_t K, cudaStream_t s);
 cudaError_t launch_philox_selftest(int64_t n, uint64_t seed, uint32_t t, uint32_t* ours, uint32_t* ref,
                                    cudaStream_t s);
+cudaError_t launch_recompute_rewards(const StageW& W, const float* next_state, const float* actions, int64_t m,
+                                     float* rewards, cudaStream_t s);
 cudaError_t launch_stats_finalize(double* slots, int32_t n_slots, double* out, int32_t reset, double host_steps,
                                   cudaStream_t s);
 

@@ -176,6 +176,12 @@ __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const D
             }
             if (O.obs_dense) write_dense(P, B, i, ob, t + 1, O.obs_dense + i * (kObsCore + 4 * P.n_hist));
         }
+        if (O.obs_critic) {
+            float oc[kObsCritic];
+            observe_critic(e.s, e.dist, oc);
+#pragma unroll
+            for (int j = 0; j < kObsCritic; ++j) O.obs_critic[j * N + i] = oc[j];
+        }
         if (O.reward) O.reward[i] = o.reward;
         if (O.flags) O.flags[i] = (uint8_t)fl;
     }
@@ -211,6 +217,12 @@ __global__ void __launch_bounds__(kStepBlock) reset_kernel(const DevParams P, co
             for (int j = 0; j < kObsCore; ++j) O.obs_core[j * N + i] = ob[j];
         }
         if (O.obs_dense) write_dense(P, B, i, ob, P.t0, O.obs_dense + i * (kObsCore + 4 * P.n_hist));
+    }
+    if (O.obs_critic) {
+        float oc[kObsCritic];
+        observe_critic(e.s, e.dist, oc);
+#pragma unroll
+        for (int j = 0; j < kObsCritic; ++j) O.obs_critic[j * N + i] = oc[j];
     }
     if (O.flags) O.flags[i] = D_RESET;
     if (O.reward) O.reward[i] = 0.0f;
@@ -304,6 +316,36 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
     const int64_t rem = N - (int64_t)blockIdx.x * kRolloutBlock;
     const double steps = (double)(rem < kRolloutBlock ? rem : kRolloutBlock) * (double)T;
     stats_block_end(st, srow, steps, B.slots + (size_t)blockIdx.x * kStatsLen);
+}
+
+// Reward recalculation over stored transitions (after each curriculum change every
+// reward in the replay buffer is recomputed): r = reward_of(W, s', a'), 0 for a non-finite s'
+// (Q26).  Bitwise equal to the reward l2f_step returned for the same (s', a', stage).
+// HBM-bound: 84 B read + 4 B written per transition.
+__global__ void __launch_bounds__(256) recompute_rewards_kernel(const StageW W, const float* __restrict__ sn,
+                                                                const float* __restrict__ act, int64_t m,
+                                                                float* __restrict__ out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        float s[kStateDim], a[4];
+#pragma unroll
+        for (int c = 0; c < kStateDim; ++c) s[c] = __ldg(sn + c * m + i);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a[c] = __ldg(act + c * m + i);
+        out[i] = state_finite(s) ? reward_of(W, s, a) : 0.0f;
+    }
+}
+
+cudaError_t launch_recompute_rewards(const StageW& W, const float* next_state, const float* actions, int64_t m,
+                                     float* rewards, cudaStream_t s)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t grid = (m + 255) / 256;
+    if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
+    recompute_rewards_kernel<<<(unsigned)grid, 256, 0, s>>>(W, next_state, actions, m, rewards);
+    return cudaGetLastError();
 }
 
 // Fixed-order reduction of all statistics slots into out[8] (one block of 256 threads).

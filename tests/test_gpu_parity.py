@@ -404,3 +404,65 @@ def test_c3_full_size_sampled(pkg):
             sp2 = e[0]["s"] if so.flags & oracle.FLAG_RESET else sp
             assert np.all(close_step(after["state"][:, i], e[0]["s"], sp2)), i
 
+
+
+# ------------------------------------------------------------------------------------------
+# NEXT rows f1 (critic observation + rotor-delay ablation) and f2 (reward recalculation)
+@pytest.mark.parametrize("flags", [inputs.ALL_NO_DR | inputs.NO_ROTOR_DELAY, inputs.ALL_NO_DR | inputs.DOMAIN_RAND])
+def test_critic_obs_and_rotor_delay_ablation(pkg, flags):
+    cfg = inputs.config_c2(flags=flags)
+    n, t = 3000, 77
+    env = pkg.Env(cfg, n)
+    env.reset()
+    env.t = t
+    snap = snapshot(env)
+    acts = np.random.default_rng(9).uniform(-1, 1, (4, n))
+    out = env.make_out(final_state=True, obs_critic=True)
+    env.step(dev_actions(acts), out)
+    after = snapshot(env)
+    oc = out["obs_critic"].cpu().numpy()
+    fin = out["final_state"].cpu().numpy()
+    E = to_oracle(snap, np.arange(n), t, cfg["n_hist"])
+    for i in range(0, n, 3):
+        e = E[i:i + 1]
+        so = oracle.env_step(cfg, e, i, t, acts[:, i].astype(np.float32).astype(np.float64))
+        sp = snap["state"][:, i]
+        assert np.all(close_step(fin[:, i], so.final_s, sp)), i
+        if near_threshold(so, cfg):
+            continue
+        ref = oracle.critic_observe(e[0])
+        sp2 = e[0]["s"] if so.flags & oracle.FLAG_RESET else sp
+        prev = np.concatenate([sp2[0:3], np.ones(9), sp2[7:17], np.zeros(6)])
+        assert np.all(close_step(oc[:, i], ref, prev)), (i, oc[:, i] - ref)
+
+
+def test_recompute_rewards_bitwise_and_vs_oracle(pkg):
+    """Replay-buffer reward recalculation: recomputing the stored transitions at the
+    same stage reproduces l2f_step's rewards bit for bit; at a later curriculum stage it
+    matches the oracle's recomputation."""
+    cfg = inputs.config_c5()
+    cfg["curriculum"]["interval"] = 3
+    n, T = 4096, 8
+    env = pkg.Env(cfg, n)
+    env.reset()
+    S, A, R, TT = [], [], [], []
+    for k in range(T):
+        t = env.t
+        a = dev_actions(inputs.actions_near_hover(1, n, seed=60 + k)[0])
+        o = env.make_out(final_state=True)
+        env.step(a, o)
+        S.append(o["final_state"].clone())
+        A.append(env.hist[t % cfg["n_hist"]].clone())  # applied a' of step t (ring slot t mod N_H)
+        R.append(o["reward"].clone())
+        TT.append(t)
+    s_buf = torch.cat(S, dim=1).contiguous()
+    a_buf = torch.cat(A, dim=1).contiguous()
+    for k in range(T):  # same stage -> bitwise
+        r = env.recompute_rewards(TT[k], S[k].contiguous(), A[k].contiguous())
+        assert torch.equal(r, R[k]), k
+    later = 40
+    r2 = env.recompute_rewards(later, s_buf, a_buf).cpu().numpy()
+    s_np, a_np = s_buf.cpu().numpy().astype(np.float64), a_buf.cpu().numpy().astype(np.float64)
+    for j in range(0, s_np.shape[1], 97):
+        ref = oracle.recompute_reward(cfg, later, s_np[:, j], a_np[:, j])
+        assert close(r2[j], ref, abs_=1e-5), (j, r2[j], ref)

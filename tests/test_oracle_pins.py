@@ -580,3 +580,55 @@ def test_rollout_matches_stepwise_and_is_thread_invariant():
     fl = tr1[:, :, 26].astype(int)
     ended = (fl & (oracle.FLAG_TERMINATED | oracle.FLAG_TRUNCATED)) != 0
     assert st1[0] == ended.sum()
+
+
+# ---------------------------------------------------------------- NEXT f1/f2
+def test_no_rotor_delay_sets_rotor_speed_to_setpoint():
+    # with the rotor-delay switch off, omega_m equals the setpoint immediately
+    cfg = inputs.base_config(flags=inputs.NO_ROTOR_DELAY)
+    env = oracle.new_envs(1)
+    env[0]["s"] = hover_state()
+    env[0]["s"][13:17] = 1000.0
+    env[0]["dr"][:] = 1
+    a = np.array([0.3, -0.5, 0.9, -1.0])
+    oracle.env_step(cfg, env, 0, 0, a)
+    u = [oracle.action_to_rpm(_params(), x) for x in a]
+    assert np.allclose(env[0]["s"][13:17], u, rtol=0, atol=1e-9)
+    # and with the lag the rotors move only part of the way (63 % after T_m = 15 steps)
+    cfg2 = inputs.base_config(flags=0)
+    env2 = oracle.new_envs(1)
+    env2[0]["s"] = hover_state()
+    env2[0]["s"][13:17] = 1000.0
+    env2[0]["dr"][:] = 1
+    oracle.env_step(cfg2, env2, 0, 0, a)
+    assert np.all(np.abs(env2[0]["s"][13:17] - 1000.0) < np.abs(np.array(u) - 1000.0) * 0.1)
+
+
+def test_critic_observation():
+    gold = json.load(open(os.path.join(GOLD, "paper_constants.json")))
+    e = oracle.new_envs(1)[0]
+    e["s"] = hover_state()
+    o = oracle.critic_observe(e)
+    assert o.size == gold["critic_obs_dim"]["value"]
+    # hover at origin, zero disturbance -> (0^3, I, 0^3, 0^3, w_h 1^4, 0^3, 0^3)
+    exp = np.concatenate([np.zeros(3), np.eye(3).ravel(), np.zeros(6), np.full(4, hover_rpm()), np.zeros(6)])
+    assert np.allclose(o, exp, rtol=1e-15, atol=0)
+    e2 = oracle.reset(inputs.config_c2(), 4, 2)
+    o2 = oracle.critic_observe(e2)
+    assert np.array_equal(o2[18:22], e2["s"][13:17]) and np.array_equal(o2[22:28], e2["dist"])
+    assert np.allclose(o2[3:12].reshape(3, 3), oracle.rotation(e2["s"][3:7]))
+
+
+def test_recompute_reward_matches_step_reward_and_stages():
+    cfg = inputs.config_c2()
+    cfg["curriculum"]["interval"] = 10
+    e = oracle.reset_many(cfg, [3], 0)
+    a = np.array([0.1, 0.2, 0.3, 0.4])
+    so = oracle.env_step(cfg, e, 3, 25, a)
+    assert oracle.recompute_reward(cfg, 25, so.final_s, so.a_applied) == so.reward
+    # a later stage re-weights the same transition (P:231 recalculation after a curriculum change)
+    w2, _ = oracle.stage(cfg, 95)
+    assert oracle.recompute_reward(cfg, 95, so.final_s, so.a_applied) == oracle.reward(w2, so.final_s, so.a_applied)
+    bad = np.array(so.final_s)
+    bad[4] = np.nan
+    assert oracle.recompute_reward(cfg, 25, bad, so.a_applied) == 0.0
