@@ -50,7 +50,8 @@ def test_library_is_sm100a(L):
 
 
 def test_abi_version(L):
-    assert L.l2f_abi_version() == 1
+    from paper_2311_13081_b200.abi import ABI_VERSION
+    assert L.l2f_abi_version() == ABI_VERSION == 2
 
 
 def _size(L, cfg, n, off=0):
