@@ -38,10 +38,23 @@ DT = 0.01
 STEP_BYTES_DR = 68 + 16 + 24 + 20 + 8 + 68 + 8 + 16 + 72 + 4 + 1
 #  tensor-core FLOPs of the actor MLP 146 -> 64 -> 64 -> 4 per env-step
 MLP_FLOPS = 2 * (146 * 64 + 64 * 64 + 64 * 4)
-#  scalar (non-tensor) operations of one fused MLP env-step, counted from the method as
-#  written with a fused multiply-add counted once (DESIGN.md section 5 table)
-ALU_OPS_PER_ENV_STEP = 1372
+#  scalar (non-tensor) operations of one env-step, counted from the method's arithmetic with a
+#  fused multiply-add or a transcendental counted as one op (DESIGN.md section 5.5 table):
+#  fused MLP rollout (obs noise, obs, MLP epilogue, action noise, RK4, reward, amortised reset)
+ALU_OPS_PER_ENV_STEP = 1071
+#  open-loop rollout with Philox random actions (no observation, no MLP)
+ALU_OPS_PER_ENV_STEP_OPEN = 657
 SMS = 148
+
+
+def traffic(key):
+    """DRAM bytes per launch of a kernel from the last committed ncu --set full capture
+    (profiles/latest_traffic.json, written by scripts/summarize_profile.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "latest_traffic.json")) as f:
+            return json.load(f)[key]["dram_bytes"]
+    except Exception:
+        return None
 
 
 def peaks():
@@ -271,9 +284,13 @@ def main():
     f_clk = (clocks["sm_mhz"] or pk["sm_max_mhz"]) * 1e6
     k_rate = n * T / (k_ms / 1e3)
     alu_peak = SMS * 128 * f_clk / 1e12
+    ops = ALU_OPS_PER_ENV_STEP if args.mode == "mlp" else ALU_OPS_PER_ENV_STEP_OPEN
     roof = {"bound": "alu", "kernel": "rollout_mlp_kernel" if args.mode == "mlp" else "rollout_open_kernel",
-            "achieved": ALU_OPS_PER_ENV_STEP * k_rate / 1e12, "peak": alu_peak, "unit": "Tops/s",
-            "frac": ALU_OPS_PER_ENV_STEP * k_rate / 1e12 / alu_peak, "traffic": None,
+            "achieved": ops * k_rate / 1e12, "peak": alu_peak, "unit": "Tops/s",
+            "frac": ops * k_rate / 1e12 / alu_peak, "ops_per_env_step": ops,
+            "traffic": traffic("mlp" if args.mode == "mlp" else "open"),
+            "traffic_note": "DRAM read+write bytes per launch, ncu --set full (profiles/latest_traffic.json; "
+                            "captured at T=100: the rollout moves state once per tile, independent of T)",
             "peak_source": f"148 SMs x 128 lanes x {f_clk / 1e6:.0f} MHz (median SM clock sampled in the timed region)",
             "tensor": {"achieved": MLP_FLOPS * k_rate / 1e12, "peak": pk["bf16_tflops_sustained"],
                        "unit": "TFLOP/s", "frac": MLP_FLOPS * k_rate / 1e12 / pk["bf16_tflops_sustained"],
@@ -370,7 +387,7 @@ def secondary(pkg, inputs, torch, dev, pk, f_clk):
     out["C3_step_api"] = {"value": rate, "unit": "env-steps/s", "us_per_step": ms * 1e3,
                           "sim_seconds_per_wall_second": rate * DT,
                           "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                                       "frac": gbs / pk["hbm_gbs"], "traffic": None,
+                                       "frac": gbs / pk["hbm_gbs"], "traffic": traffic("step"),
                                        "bytes_per_env_step": STEP_BYTES_DR, "peak_source": pk["source"]}}
     # e2e of the step API through host buffers (pinned): H2D actions, D2H obs/reward/flags
     ha = acts[0].cpu().pin_memory()

@@ -140,9 +140,9 @@ __device__ __forceinline__ void epilogue_hidden(const TileCtx& c)
 }
 
 // The tile's 128 threads hand their freshly written A rows (and finished TMEM reads) to the
-// MMA issuer: proxy fence + tcgen05 fence + a 128-thread named barrier (id 1 + tile).  (An
-// mbarrier arrive/wait variant that lets early warps run ahead measured slower: the waiting
-// warps then spin instead of sleeping at the barrier.)
+// MMA issuer: proxy fence + tcgen05 fence + a 128-thread named barrier (id 1 + tile).  (Variants
+// where only the issuing warp waits -- mbarrier arrive/wait, or bar.arrive for the other three
+// warps -- measured no faster: the other tiles' warps already fill the barrier time.)
 __device__ __forceinline__ void handoff_to_mma(TileCtx& c)
 {
     tc::fence_proxy_async();

@@ -101,6 +101,11 @@ __device__ __forceinline__ void named_sync(uint32_t id, uint32_t count)
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+__device__ __forceinline__ void named_arrive(uint32_t id, uint32_t count)
+{
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // TMEM allocation by one full warp; the base address is written to smem.
 __device__ __forceinline__ void tmem_alloc(uint32_t dst_saddr, uint32_t ncols)
 {

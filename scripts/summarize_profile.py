@@ -46,6 +46,7 @@ METRICS = [
     "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
     "lts__t_sector_hit_rate.pct",
 ]
+traffic = {}
 for rep in sorted(f for f in os.listdir(src) if f.endswith(".ncu-rep")):
     path = os.path.join(src, rep)
     shutil.copy(path, os.path.join(dst, rep))
@@ -55,6 +56,15 @@ for rep in sorted(f for f in os.listdir(src) if f.endswith(".ncu-rep")):
         continue
     h, u, v = rr[0], rr[1], rr[2]
     name = v[h.index("Kernel Name")] if "Kernel Name" in h else rep
+    try:
+        rd = float(v[h.index("dram__bytes_read.sum")]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[
+            u[h.index("dram__bytes_read.sum")]]
+        wr = float(v[h.index("dram__bytes_write.sum")]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[
+            u[h.index("dram__bytes_write.sum")]]
+        traffic[rep.replace(".ncu-rep", "")] = {"kernel": name.split("(")[0], "dram_bytes": rd + wr,
+                                                "dram_read": rd, "dram_write": wr}
+    except (ValueError, KeyError):
+        pass
     out += [f"## `{rep}`: {name.split('(')[0]}", "", "| metric | value |", "|---|---|"]
     for m in METRICS:
         if m in h:
@@ -65,4 +75,9 @@ for rep in sorted(f for f in os.listdir(src) if f.endswith(".ncu-rep")):
                            capture_output=True, text=True).stdout
     out += ["Top CUDA source lines by executed warp-instructions:", "", "```", lines.rstrip(), "```", ""]
 open(os.path.join(dst, "SUMMARY.md"), "w").write("\n".join(out) + "\n")
+import json  # noqa: E402
+json.dump(traffic, open(os.path.join(dst, "traffic.json"), "w"), indent=1)
+# bench.py reports these per-launch DRAM bytes as roofline.traffic
+json.dump({"source": os.path.join(dst, "traffic.json"), **traffic},
+          open(os.path.join(os.path.dirname(dst.rstrip("/")), "latest_traffic.json"), "w"), indent=1)
 print("\n".join(out))
