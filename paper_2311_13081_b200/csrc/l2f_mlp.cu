@@ -16,7 +16,8 @@
 //    history block is rotated instead (MN-major copy with duplicated K rows, so a rotation
 //    by 4 K-rows is a 64-byte start-address offset).  Zero shared-memory traffic for the
 //    history beyond the one 8-byte slot write per env-step;
-//  * one elected thread per tile issues the MMAs after a 128-thread named barrier; MMA
+//  * one thread per tile and layer (lane 0 of warp l - 1 for layer l) issues the MMAs after a
+//    128-thread named barrier; MMA
 //    completion is signalled through tcgen05.commit -> mbarrier.  The other two tiles' warps
 //    keep the FP32/INT pipes busy while one tile waits on the tensor core.
 #include "l2f_device.cuh"
@@ -121,7 +122,7 @@ struct TileCtx {
     uint32_t a2_trow;         // ... of this thread's lane
     uint32_t bar_id;
     uint32_t phase;
-    bool leader;
+    uint32_t r;               // thread index within the tile
 };
 
 // Epilogue of L1 / L2: accumulator row -> relu -> fp16 -> this thread's A2 row in TMEM.
@@ -161,7 +162,8 @@ struct NoHook {
     __device__ __forceinline__ void operator()(int) const {}
 };
 
-// The three layers on the tensor core for one tile.  Precondition: A1 rows written by all 128
+// The three layers on the tensor core for one tile; layer l is issued by lane 0 of the tile's warp
+// l - 1 so the issue work is spread over three warps.  Precondition: A1 rows written by all 128
 // threads.  `rot` = rotation of the history ring (W1 history row offset in slots).  hook(l) runs
 // on every thread right after layer l's MMAs were issued, i.e. inside the MMA latency (used to
 // draw the next step's noise).
@@ -172,7 +174,7 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
     // descriptors = base descriptor + (byte offset >> 4) in the start-address field (addresses
     // stay below 256 KB, so the 14-bit field never carries)
     handoff_to_mma(c);
-    if (c.leader) {
+    if (c.r == 0) {
         tc::fence_after();
         const uint64_t dA1 = tc::make_desc(c.a1, kChunkA, 128);
         const uint64_t dW1o = tc::make_desc(sbase + OFF_W1O, kHid * 16, 128);
@@ -188,7 +190,7 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
     wait_mma(c);
     epilogue_hidden(c);
     handoff_to_mma(c);
-    if (c.leader) {
+    if (c.r == 32) {
         tc::fence_after();
         const uint64_t dW2 = tc::make_desc(sbase + OFF_W2, kHid * 16, 128);
 #pragma unroll
@@ -200,7 +202,7 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
     wait_mma(c);
     epilogue_hidden(c);
     handoff_to_mma(c);
-    if (c.leader) {
+    if (c.r == 64) {
         tc::fence_after();
         const uint64_t dW3 = tc::make_desc(sbase + OFF_W3, 256, 128);
 #pragma unroll
@@ -301,7 +303,7 @@ __device__ __forceinline__ TileCtx make_ctx(uint32_t sbase)
     tc::tmem_wait_st();
     c.bar_id = 1 + g;
     c.phase = 0;
-    c.leader = (r == 0);
+    c.r = r;
     tc::sts128(c.a1_row + 3 * kChunkA, 0u, 0u, 0u, 0u);  // K 24..31: constant zero pad
     return c;
 }

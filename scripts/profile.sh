@@ -17,6 +17,4 @@ ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 1
 ncu --set full --clock-control none --import-source on -k regex:rollout_open -c 1 -o $OUT/open \
     python scripts/run_open.py > $OUT/ncu_open.log 2>&1
 
-L2F_STEP_PATH=bulk ncu --set full --clock-control none --import-source on -k regex:step_tma -s 10 -c 1 -o $OUT/step_bulk \
-    python scripts/run_step.py > $OUT/ncu_step_bulk.log 2>&1
 echo done
