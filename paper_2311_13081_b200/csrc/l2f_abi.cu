@@ -189,6 +189,14 @@ DevParams make_base(const l2f_config& c)
     P.half_dt = (float)(0.5 * c.dt);
     P.dt_6 = (float)(c.dt / 6.0);
     P.dt2_6 = (float)(c.dt * c.dt / 6.0);
+    {  // RK4 of the rotor lag w' = (u - w)/T_m: stage factors and stability polynomial at z = dt/T_m
+        const double z = c.dt / c.params.motor_tau;
+        const double b2 = 1.0 - 0.5 * z, b3 = 1.0 - 0.5 * z * b2, b4 = 1.0 - z * b3;
+        P.m_beta2 = (float)b2;
+        P.m_beta3 = (float)b3;
+        P.m_beta4 = (float)b4;
+        P.m_R = (float)(1.0 - z / 6.0 * (1.0 + 2.0 * b2 + 2.0 * b3 + b4));
+    }
     const l2f_params& p = c.params;
     P.mass = (float)p.mass;
     for (int j = 0; j < 3; ++j) {

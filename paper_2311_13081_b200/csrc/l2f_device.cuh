@@ -49,6 +49,8 @@ struct DevParams {
     uint32_t t0;               // step counter at launch
     // integration
     float dt, half_dt, dt_6, dt2_6;
+    // RK4 of the linear rotor lag (rk4_step): stage values u + d beta_j, result u + d R
+    float m_beta2, m_beta3, m_beta4, m_R;
     // nominal parameters; DR factors scale mass, J, thrust coefficients (Q19)
     float mass, J[3], c[3], ctau, inv_tm, rpm_min, rpm_max, gravity, rpm_half_span, inv_rpm_span2;
     float rx[4], ry[4], spin[4];
@@ -169,6 +171,40 @@ __device__ __forceinline__ void box_muller(uint32_t xa, uint32_t xb, float& z0, 
     z1 = r * sn;
 }
 
+// Both Box-Muller pairs of one Philox block, (x.x, x.y) -> z0, z1 and (x.z, x.w) -> z2, z3, in
+// packed f32x2 arithmetic (FADD2 / FFMA2 / FMUL2): every element goes through the same
+// round-to-nearest operations as box_muller, so the results are identical to two calls.
+__device__ __forceinline__ void box_muller2(uint4 x, float z[4])
+{
+    const float c = -0.99999994039535522f;
+    const float2 u1 = __fadd2_rn(make_float2(__uint_as_float(0x3F800000u | (x.x >> 9)),
+                                             __uint_as_float(0x3F800000u | (x.z >> 9))), make_float2(c, c));
+    const float2 u2 = __fadd2_rn(make_float2(__uint_as_float(0x3F800000u | (x.y >> 9)),
+                                             __uint_as_float(0x3F800000u | (x.w >> 9))), make_float2(c, c));
+    const float2 xm = __fadd2_rn(u1, make_float2(-1.0f, -1.0f));
+    float2 p = __ffma2_rn(xm, make_float2(-1.0f / 6.0f, -1.0f / 6.0f), make_float2(0.2f, 0.2f));
+    p = __ffma2_rn(xm, p, make_float2(-0.25f, -0.25f));
+    p = __ffma2_rn(xm, p, make_float2(1.0f / 3.0f, 1.0f / 3.0f));
+    p = __ffma2_rn(xm, p, make_float2(-0.5f, -0.5f));
+    p = __ffma2_rn(xm, p, make_float2(1.0f, 1.0f));
+    const float2 series = __fmul2_rn(xm, p);
+    const float2 lg = __fmul2_rn(make_float2(__log2f(u1.x), __log2f(u1.y)),
+                                 make_float2(0.69314718055994531f, 0.69314718055994531f));
+    const float2 ln = make_float2(xm.x > -0.0625f ? series.x : lg.x, xm.y > -0.0625f ? series.y : lg.y);
+    const float2 y = __fmul2_rn(make_float2(-2.0f, -2.0f), ln);
+    const float2 r = __fmul2_rn(y, make_float2(rsqrtf(y.x), rsqrtf(y.y)));
+    const float2 th = __fmul2_rn(make_float2(6.28318530717958648f, 6.28318530717958648f), u2);
+    float s0, c0, s1, c1;
+    __sincosf(th.x, &s0, &c0);
+    __sincosf(th.y, &s1, &c1);
+    const float2 za = __fmul2_rn(make_float2(r.x, r.x), make_float2(c0, s0));
+    const float2 zb = __fmul2_rn(make_float2(r.y, r.y), make_float2(c1, s1));
+    z[0] = za.x;
+    z[1] = za.y;
+    z[2] = zb.x;
+    z[3] = zb.y;
+}
+
 __device__ __forceinline__ const StageW& stage_of(const DevParams& P, uint32_t t)
 {
     int k = 0;
@@ -190,11 +226,10 @@ struct Phys {
     float inv_m;
     float Jx, Jy, Jz, iJx, iJy, iJz;
     float dJzy, dJxz, dJyx; // Jz - Jy, Jx - Jz, Jy - Jx (gyroscopic term)
-    float u_tm[4];          // setpoint / T_m
 };
 
 template <bool kDR>
-__device__ __forceinline__ void make_phys(const DevParams& P, const EnvReg& e, const float u[4], Phys& ph)
+__device__ __forceinline__ void make_phys(const DevParams& P, const EnvReg& e, Phys& ph)
 {
     if constexpr (kDR) {
         ph.c0 = P.c[0] * e.dr[4];
@@ -225,22 +260,19 @@ __device__ __forceinline__ void make_phys(const DevParams& P, const EnvReg& e, c
         ph.iJy = P.iJ[1];
         ph.iJz = P.iJ[2];
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) ph.u_tm[i] = u[i] * P.inv_tm;
 }
 
-// Derivative of the non-position part x = s[3..16] = (q, v, w, w_m):
-// q' = 1/2 q (x) (0,w); v' = (R e_z T + f_r)/m - g e_z; w' = J^-1 (tau - w x J w);
-// w_m' = (u - w_m)/T_m.  The position never feeds back (p' = v), so RK4 integrates it in
-// closed form from the stage velocities (rk4_step).  dx[j] = d/dt s[3 + j].
-constexpr int kX = 14;
-__device__ __forceinline__ void deriv(const DevParams& P, const Phys& ph, const float* d,
-                                      const float* x, float* dx)
+// Derivative of the coupled part y = (q, w) of the state, given the rotor speeds m of the RK4
+// stage: q' = 1/2 q (x) (0,w); w' = J^-1 (tau - w x J w); plus the
+// linear acceleration av = v' = (R e_z T + f_r)/m - g e_z, which feeds nothing back.
+// y = (qw, qx, qy, qz, wx, wy, wz).
+constexpr int kY = 7;
+__device__ __forceinline__ void deriv(const DevParams& P, const Phys& ph, const float* d, const float* y,
+                                      const float m[4], float* dy, float av[3])
 {
-    const float* wm = x + 10;
     float f[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) f[i] = fmaf(fmaf(ph.c2, wm[i], ph.c1), wm[i], ph.c0);
+    for (int i = 0; i < 4; ++i) f[i] = fmaf(fmaf(ph.c2, m[i], ph.c1), m[i], ph.c0);
     const float T = (f[0] + f[1]) + (f[2] + f[3]);
     float tx = d[3], ty = d[4], tz = 0.0f;
 #pragma unroll
@@ -250,37 +282,29 @@ __device__ __forceinline__ void deriv(const DevParams& P, const Phys& ph, const 
         tz = fmaf(P.spin[i], f[i], tz);
     }
     tz = fmaf(P.ctau, tz, d[5]);
-    const float qw = x[0], qx = x[1], qy = x[2], qz = x[3];
-    const float wx = x[7], wy = x[8], wz = x[9];
+    const float qw = y[0], qx = y[1], qy = y[2], qz = y[3];
+    const float wx = y[4], wy = y[5], wz = y[6];
     const float hx = 0.5f * wx, hy = 0.5f * wy, hz = 0.5f * wz;
-    dx[0] = -(qx * hx + qy * hy + qz * hz);
-    dx[1] = qw * hx + qy * hz - qz * hy;
-    dx[2] = qw * hy - qx * hz + qz * hx;
-    dx[3] = qw * hz + qx * hy - qy * hx;
+    dy[0] = -(qx * hx + qy * hy + qz * hz);
+    dy[1] = qw * hx + qy * hz - qz * hy;
+    dy[2] = qw * hy - qx * hz + qz * hx;
+    dy[3] = qw * hz + qx * hy - qy * hx;
     // third column of R(q): body z-axis in world
     const float r02 = 2.0f * (qx * qz + qw * qy);
     const float r12 = 2.0f * (qy * qz - qw * qx);
     const float r22 = 1.0f - 2.0f * (qx * qx + qy * qy);
-    dx[4] = fmaf(r02, T, d[0]) * ph.inv_m;
-    dx[5] = fmaf(r12, T, d[1]) * ph.inv_m;
-    dx[6] = fmaf(fmaf(r22, T, d[2]), ph.inv_m, -P.gravity);
+    av[0] = fmaf(r02, T, d[0]) * ph.inv_m;
+    av[1] = fmaf(r12, T, d[1]) * ph.inv_m;
+    av[2] = fmaf(fmaf(r22, T, d[2]), ph.inv_m, -P.gravity);
     // Euler: J w' = tau - w x (J w)
     const float cx = ph.dJzy * (wy * wz);
     const float cy = ph.dJxz * (wz * wx);
     const float cz = ph.dJyx * (wx * wy);
-    dx[7] = (tx - cx) * ph.iJx;
-    dx[8] = (ty - cy) * ph.iJy;
-    dx[9] = (tz - cz) * ph.iJz;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) dx[10 + i] = fmaf(-wm[i], P.inv_tm, ph.u_tm[i]);
+    dy[4] = (tx - cx) * ph.iJx;
+    dy[5] = (ty - cy) * ph.iJy;
+    dy[6] = (tz - cz) * ph.iJz;
 }
 
-// Classical RK4 with zero-order-hold setpoints (Q1), then q renormalisation and rotor-speed
-// clamp (Q5).  Returns true if the result is non-finite.
-// The 14 non-position components use the sm_100 packed FP32 pipe (FFMA2/FADD2: each lane is
-// an IEEE fma/add like the scalar instruction) in 7 pairs.  Position: with p' = v and stage
-// velocities v1 = v, v2 = v + h/2 a1, v3 = v + h/2 a2, v4 = v + h a3, the RK4 combination
-// h/6 (v1 + 2 v2 + 2 v3 + v4) equals h v + h^2/6 (a1 + a2 + a3) exactly.
 // Any NaN/Inf component makes the sum non-finite (a finite overflow to inf also counts:
 // |x| > 1e38 is divergence in any sense).  Checked on the projected state s'.
 __device__ __forceinline__ bool state_finite(const float* s)
@@ -291,58 +315,91 @@ __device__ __forceinline__ bool state_finite(const float* s)
     return isfinite(sum);
 }
 
+// out = a * h + b over the 7 coupled components: 3 packed FFMA2 pairs + 1 scalar FFMA.
 __device__ __forceinline__ void pair_fma(const float* a, float h, const float* b, float* out)
 {
     const float2 hh = make_float2(h, h);
 #pragma unroll
-    for (int i = 0; i < kX; i += 2) {
+    for (int i = 0; i + 1 < kY; i += 2) {
         const float2 r = __ffma2_rn(make_float2(a[i], a[i + 1]), hh, make_float2(b[i], b[i + 1]));
         out[i] = r.x;
         out[i + 1] = r.y;
     }
+    out[kY - 1] = fmaf(a[kY - 1], h, b[kY - 1]);
 }
 
-__device__ __forceinline__ bool rk4_step(const DevParams& P, const Phys& ph, const float* d, float* s)
+// Classical RK4 at dt with zero-order-hold setpoints u (Q1), then q renormalisation and
+// rotor-speed clamp (Q5).  Returns true if the result is non-finite.  The RK4 is
+// evaluated in the algebraically identical form that exploits the structure of the ODE
+// (DESIGN.md section 5.6), so only the coupled part y = (q, w) carries stage vectors:
+//  * rotors: w_m' = (u - w_m)/T_m is linear with a constant input, so with d = w_m0 - u the
+//    RK4 stage values are u + d beta_j and the RK4 result is u + d R (R = the RK4 stability
+//    polynomial at -dt/T_m; beta_j, R precomputed in FP64 on the host);
+//  * velocity: v' = a(q, w_m) does not depend on v, so v_new = v + h/6 (a1 + 2 a2 + 2 a3 + a4)
+//    needs no stage velocities;
+//  * position: p' = v with stage velocities v, v + h/2 a1, v + h/2 a2, v + h a3 gives
+//    p_new = p + h v + h^2/6 (a1 + a2 + a3).
+__device__ __forceinline__ bool rk4_step(const DevParams& P, const Phys& ph, const float* d, const float u[4],
+                                         float* s)
 {
-    float* x = s + 3;
-    float acc[kX], tmp[kX], k[kX];
-    deriv(P, ph, d, x, k);
-    float asum0 = k[4], asum1 = k[5], asum2 = k[6];  // a1 + a2 + a3 (v' of stages 1-3)
+    float y0[kY] = {s[3], s[4], s[5], s[6], s[10], s[11], s[12]};
+    float dm[4], m[4];
 #pragma unroll
-    for (int i = 0; i < kX; ++i) acc[i] = k[i];
-    pair_fma(k, P.half_dt, x, tmp);
-    deriv(P, ph, d, tmp, k);
-    asum0 += k[4];
-    asum1 += k[5];
-    asum2 += k[6];
+    for (int i = 0; i < 4; ++i) dm[i] = s[13 + i] - u[i];
+    float acc[kY], tmp[kY], k[kY], a[3], asum[3], vacc[3];
+    deriv(P, ph, d, y0, s + 13, k, a);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) asum[i] = vacc[i] = a[i];
+#pragma unroll
+    for (int i = 0; i < kY; ++i) acc[i] = k[i];
+    pair_fma(k, P.half_dt, y0, tmp);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) m[i] = fmaf(dm[i], P.m_beta2, u[i]);
+    deriv(P, ph, d, tmp, m, k, a);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        asum[i] += a[i];
+        vacc[i] = fmaf(a[i], 2.0f, vacc[i]);
+    }
     pair_fma(k, 2.0f, acc, acc);
-    pair_fma(k, P.half_dt, x, tmp);
-    deriv(P, ph, d, tmp, k);
-    asum0 += k[4];
-    asum1 += k[5];
-    asum2 += k[6];
+    pair_fma(k, P.half_dt, y0, tmp);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) m[i] = fmaf(dm[i], P.m_beta3, u[i]);
+    deriv(P, ph, d, tmp, m, k, a);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        asum[i] += a[i];
+        vacc[i] = fmaf(a[i], 2.0f, vacc[i]);
+    }
     pair_fma(k, 2.0f, acc, acc);
-    pair_fma(k, P.dt, x, tmp);
-    deriv(P, ph, d, tmp, k);
-    // position first (uses the pre-step velocity)
-    s[0] = fmaf(P.dt2_6, asum0, fmaf(P.dt, s[7], s[0]));
-    s[1] = fmaf(P.dt2_6, asum1, fmaf(P.dt, s[8], s[1]));
-    s[2] = fmaf(P.dt2_6, asum2, fmaf(P.dt, s[9], s[2]));
+    pair_fma(k, P.dt, y0, tmp);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) m[i] = fmaf(dm[i], P.m_beta4, u[i]);
+    deriv(P, ph, d, tmp, m, k, a);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        s[i] = fmaf(P.dt2_6, asum[i], fmaf(P.dt, s[7 + i], s[i]));  // position (pre-step v)
+        s[7 + i] = fmaf(P.dt_6, vacc[i] + a[i], s[7 + i]);
+    }
     {
         const float2 h6 = make_float2(P.dt_6, P.dt_6);
 #pragma unroll
-        for (int i = 0; i < kX; i += 2) {
-            const float2 a = __fadd2_rn(make_float2(acc[i], acc[i + 1]), make_float2(k[i], k[i + 1]));
-            const float2 r = __ffma2_rn(h6, a, make_float2(x[i], x[i + 1]));
-            x[i] = r.x;
-            x[i + 1] = r.y;
+        for (int i = 0; i + 1 < kY; i += 2) {
+            const float2 sm = __fadd2_rn(make_float2(acc[i], acc[i + 1]), make_float2(k[i], k[i + 1]));
+            const float2 r = __ffma2_rn(h6, sm, make_float2(y0[i], y0[i + 1]));
+            y0[i] = r.x;
+            y0[i + 1] = r.y;
         }
-    }    const float n2 = (s[3] * s[3] + s[4] * s[4]) + (s[5] * s[5] + s[6] * s[6]);
+        y0[kY - 1] = fmaf(P.dt_6, acc[kY - 1] + k[kY - 1], y0[kY - 1]);
+    }
+    const float n2 = (y0[0] * y0[0] + y0[1] * y0[1]) + (y0[2] * y0[2] + y0[3] * y0[3]);
     const float inv = rsqrtf(n2);
 #pragma unroll
-    for (int i = 3; i < 7; ++i) s[i] *= inv;
+    for (int i = 0; i < 4; ++i) s[3 + i] = y0[i] * inv;
 #pragma unroll
-    for (int i = 13; i < 17; ++i) s[i] = fminf(fmaxf(s[i], P.rpm_min), P.rpm_max);
+    for (int i = 0; i < 3; ++i) s[10 + i] = y0[4 + i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[13 + i] = fminf(fmaxf(fmaf(dm[i], P.m_R, u[i]), P.rpm_min), P.rpm_max);
     return !state_finite(s);
 }
 
@@ -365,9 +422,7 @@ __device__ __forceinline__ void action_noise(const DevParams& P, uint32_t gid, u
 {
     z[0] = z[1] = z[2] = z[3] = 0.0f;
     if (P.flags & F_ACTION_NOISE) {
-        const uint4 x = draw(P, gid, t, S_ACT, 0);
-        box_muller(x.x, x.y, z[0], z[1]);
-        box_muller(x.z, x.w, z[2], z[3]);
+        box_muller2(draw(P, gid, t, S_ACT, 0), z);
     }
 }
 
@@ -437,8 +492,8 @@ __device__ __forceinline__ void transition(const DevParams& P, const StageW& W, 
         for (int i = 0; i < 4; ++i) e.s[13 + i] = u[i];
     }
     Phys ph;
-    make_phys<kDR>(P, e, u, ph);
-    const bool div = rk4_step(P, ph, e.dist, e.s);
+    make_phys<kDR>(P, e, ph);
+    const bool div = rk4_step(P, ph, e.dist, u, e.s);
 
     const float* s = e.s;
     const float vv = s[7] * s[7] + s[8] * s[8] + s[9] * s[9];
@@ -598,8 +653,10 @@ __device__ __forceinline__ void obs_noise_blocks(const DevParams& P, uint32_t gi
     for (int b = 0; b < 5; ++b) {
         if (b < b0 || b >= b1) continue;
         const uint4 x = draw(P, gid, t, S_OBS, (uint32_t)b);
-        box_muller(x.x, x.y, z[4 * b], z[4 * b + 1]);
-        if (b < 4) box_muller(x.z, x.w, z[4 * b + 2], z[4 * b + 3]);
+        if (b < 4)
+            box_muller2(x, z + 4 * b);
+        else
+            box_muller(x.x, x.y, z[4 * b], z[4 * b + 1]);
     }
 }
 
