@@ -230,6 +230,28 @@ DevParams make_base(const l2f_config& c)
     P.dist_torque = (float)c.dist_torque;
     P.dr_lo = (float)c.dr_lo;
     P.dr_hi = (float)c.dr_hi;
+    {  // reset sampling table (reset_values): lo and the fp32-rounded span hi - lo per value
+        auto rng = [](float lo, float hi, float4& L, float4& S, int k) {
+            (&L.x)[k] = lo;
+            (&S.x)[k] = hi - lo;  // fp32 subtraction, as a device-side hi - lo would round
+        };
+        const float pi2 = 6.28318530717958648f;
+        for (int b = 0; b < 8; ++b) P.rs_lo[b] = P.rs_span[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 0; k < 3; ++k) rng(-P.init_pos, P.init_pos, P.rs_lo[0], P.rs_span[0], k);
+        rng(-1.0f, 1.0f, P.rs_lo[0], P.rs_span[0], 3);                 // axis cos-polar
+        P.rs_lo[1].x = 0.0f, P.rs_span[1].x = pi2;                      // axis azimuth
+        P.rs_lo[1].y = 0.0f, P.rs_span[1].y = P.init_angle;             // rotation angle
+        rng(-P.init_vel, P.init_vel, P.rs_lo[1], P.rs_span[1], 2);
+        rng(-P.init_vel, P.init_vel, P.rs_lo[1], P.rs_span[1], 3);
+        rng(-P.init_vel, P.init_vel, P.rs_lo[2], P.rs_span[2], 0);
+        for (int k = 1; k < 4; ++k) rng(-P.init_angvel, P.init_angvel, P.rs_lo[2], P.rs_span[2], k);
+        for (int k = 0; k < 4; ++k) rng(P.init_rpm_lo, P.init_rpm_hi, P.rs_lo[3], P.rs_span[3], k);
+        for (int k = 0; k < 3; ++k) rng(-P.dist_force, P.dist_force, P.rs_lo[4], P.rs_span[4], k);
+        rng(-P.dist_torque, P.dist_torque, P.rs_lo[4], P.rs_span[4], 3);
+        for (int k = 0; k < 2; ++k) rng(-P.dist_torque, P.dist_torque, P.rs_lo[5], P.rs_span[5], k);
+        for (int k = 0; k < 4; ++k) rng(P.dr_lo, P.dr_hi, P.rs_lo[6], P.rs_span[6], k);
+        rng(P.dr_lo, P.dr_hi, P.rs_lo[7], P.rs_span[7], 0);
+    }
     for (int j = 0; j < 4; ++j) P.obs_sigma[j] = (float)c.obs_sigma[j];
     P.term_pos = (float)c.term_pos;
     P.term_vel2 = (float)(c.term_vel * c.term_vel);

@@ -58,6 +58,9 @@ struct DevParams {
     // reset distribution (Q17-Q19)
     float init_pos, init_angle, init_vel, init_angvel, init_rpm_lo, init_rpm_hi;
     float dist_force, dist_torque, dr_lo, dr_hi;
+    // reset sampling table: value (Philox slot b, component c) = rs_lo + rs_span * u (host-built
+    // from the ranges above with the span rounded in fp32; reset_values)
+    float4 rs_lo[8], rs_span[8];
     // observation noise (Q8), termination (Q14)
     float obs_sigma[4];
     float term_pos, term_vel2, term_angvel2;
@@ -516,7 +519,7 @@ __device__ __forceinline__ void transition(const DevParams& P, const StageW& W, 
 __device__ __forceinline__ float uab(float a, float b, uint32_t x) { return fmaf(b - a, unif(x), a); }
 
 // Philox blocks of one reset (Q20): RESET 0..3 at slots 0..3, DIST 0..1 at slots 4..5,
-// DR 0..1 at slots 6..7 (fixed slots keep the block array in registers).
+// DR 0..1 at slots 6..7.
 __device__ __forceinline__ int reset_nblocks(const DevParams& P)
 {
     return (P.flags & (F_DISTURBANCE | F_DOMAIN_RAND)) ? 8 : 4;
@@ -529,18 +532,26 @@ __device__ __forceinline__ uint4 reset_block(const DevParams& P, uint32_t gid, u
     return draw(P, gid, ctr, stream, blk);
 }
 
-// Reset sampling from the drawn blocks (Q17-Q19): state, disturbance, DR
-// factors, episode counters; the history fill value per rotor (Q10) in hfill.
-__device__ __forceinline__ void reset_from_blocks(const DevParams& P, const uint4 (&blk)[8], EnvReg& e,
-                                                  float hfill[4])
+// The four sampled values of reset slot b (Q17-Q19): lo + span * u per uniform
+// of the slot's Philox block.  Slot 0: p_x, p_y, p_z, axis cos-polar c_z; slot 1: axis azimuth
+// phi, rotation angle theta, v_x, v_y; slot 2: v_z, w; slot 3: rotor speeds; slots 4-5:
+// disturbance force, torque; slots 6-7: DR factors (m, J_xx, J_yy, J_zz, thrust scale).
+__device__ __forceinline__ float4 reset_values(const DevParams& P, int b, uint4 x)
 {
-    const uint4 b0 = blk[0], b1 = blk[1], b2 = blk[2], b3 = blk[3];
-    e.s[0] = uab(-P.init_pos, P.init_pos, b0.x);
-    e.s[1] = uab(-P.init_pos, P.init_pos, b0.y);
-    e.s[2] = uab(-P.init_pos, P.init_pos, b0.z);
-    const float cz = uab(-1.0f, 1.0f, b0.w);
-    const float phi = 6.28318530717958648f * unif(b1.x);
-    const float th = P.init_angle * unif(b1.y);
+    const float4 lo = P.rs_lo[b], sp = P.rs_span[b];
+    return make_float4(fmaf(sp.x, unif(x.x), lo.x), fmaf(sp.y, unif(x.y), lo.y), fmaf(sp.z, unif(x.z), lo.z),
+                       fmaf(sp.w, unif(x.w), lo.w));
+}
+
+// Assemble the new episode from the sampled values of its 8 slots: state (uniform axis-angle
+// quaternion, Q17), disturbance, DR factors, episode counters; the history fill value per
+// rotor (Q10) in hfill.
+__device__ __forceinline__ void reset_finish(const DevParams& P, const float4 (&v)[8], EnvReg& e, float hfill[4])
+{
+    e.s[0] = v[0].x;
+    e.s[1] = v[0].y;
+    e.s[2] = v[0].z;
+    const float cz = v[0].w, phi = v[1].x, th = v[1].y;
     const float sxy = sqrtf(fmaxf(fmaf(-cz, cz, 1.0f), 0.0f));
     float sp, cp, sh, ch;
     __sincosf(phi, &sp, &cp);
@@ -549,35 +560,33 @@ __device__ __forceinline__ void reset_from_blocks(const DevParams& P, const uint
     e.s[4] = sh * (sxy * cp);
     e.s[5] = sh * (sxy * sp);
     e.s[6] = sh * cz;
-    e.s[7] = uab(-P.init_vel, P.init_vel, b1.z);
-    e.s[8] = uab(-P.init_vel, P.init_vel, b1.w);
-    e.s[9] = uab(-P.init_vel, P.init_vel, b2.x);
-    e.s[10] = uab(-P.init_angvel, P.init_angvel, b2.y);
-    e.s[11] = uab(-P.init_angvel, P.init_angvel, b2.z);
-    e.s[12] = uab(-P.init_angvel, P.init_angvel, b2.w);
-    e.s[13] = uab(P.init_rpm_lo, P.init_rpm_hi, b3.x);
-    e.s[14] = uab(P.init_rpm_lo, P.init_rpm_hi, b3.y);
-    e.s[15] = uab(P.init_rpm_lo, P.init_rpm_hi, b3.z);
-    e.s[16] = uab(P.init_rpm_lo, P.init_rpm_hi, b3.w);
+    e.s[7] = v[1].z;
+    e.s[8] = v[1].w;
+    e.s[9] = v[2].x;
+    e.s[10] = v[2].y;
+    e.s[11] = v[2].z;
+    e.s[12] = v[2].w;
+    e.s[13] = v[3].x;
+    e.s[14] = v[3].y;
+    e.s[15] = v[3].z;
+    e.s[16] = v[3].w;
     if (P.flags & F_DISTURBANCE) {
-        const uint4 d0 = blk[4], d1 = blk[5];
-        e.dist[0] = uab(-P.dist_force, P.dist_force, d0.x);
-        e.dist[1] = uab(-P.dist_force, P.dist_force, d0.y);
-        e.dist[2] = uab(-P.dist_force, P.dist_force, d0.z);
-        e.dist[3] = uab(-P.dist_torque, P.dist_torque, d0.w);
-        e.dist[4] = uab(-P.dist_torque, P.dist_torque, d1.x);
-        e.dist[5] = uab(-P.dist_torque, P.dist_torque, d1.y);
+        e.dist[0] = v[4].x;
+        e.dist[1] = v[4].y;
+        e.dist[2] = v[4].z;
+        e.dist[3] = v[4].w;
+        e.dist[4] = v[5].x;
+        e.dist[5] = v[5].y;
     } else {
 #pragma unroll
         for (int j = 0; j < 6; ++j) e.dist[j] = 0.0f;
     }
     if (P.flags & F_DOMAIN_RAND) {
-        const uint4 r0 = blk[6], r1 = blk[7];
-        e.dr[0] = uab(P.dr_lo, P.dr_hi, r0.x);
-        e.dr[1] = uab(P.dr_lo, P.dr_hi, r0.y);
-        e.dr[2] = uab(P.dr_lo, P.dr_hi, r0.z);
-        e.dr[3] = uab(P.dr_lo, P.dr_hi, r0.w);
-        e.dr[4] = uab(P.dr_lo, P.dr_hi, r1.x);
+        e.dr[0] = v[6].x;
+        e.dr[1] = v[6].y;
+        e.dr[2] = v[6].z;
+        e.dr[3] = v[6].w;
+        e.dr[4] = v[7].x;
     } else {
 #pragma unroll
         for (int j = 0; j < 5; ++j) e.dr[j] = 1.0f;
@@ -591,20 +600,20 @@ __device__ __forceinline__ void reset_from_blocks(const DevParams& P, const uint
 // Reset of one env from Philox counter `ctr` (thread-local draws).
 __device__ __forceinline__ void reset_env(const DevParams& P, EnvReg& e, uint32_t gid, uint32_t ctr, float hfill[4])
 {
-    uint4 blk[8];
+    float4 v[8];
     const int nb = reset_nblocks(P);
 #pragma unroll
-    for (int b = 0; b < 8; ++b)
-        if (b < nb) blk[b] = reset_block(P, gid, ctr, b);
-    reset_from_blocks(P, blk, e, hfill);  // unused DIST/DR slots are ignored
+    for (int b = 0; b < 8; ++b) v[b] = b < nb ? reset_values(P, b, reset_block(P, gid, ctr, b)) : make_float4(0, 0, 0, 0);
+    reset_finish(P, v, e, hfill);  // unused DIST/DR slots are ignored
 }
 
-// Warp-cooperative reset (all 32 lanes must call; gids of a warp are consecutive): the Philox
-// blocks of every lane that needs a reset are drawn by all lanes in parallel and handed to
-// their owner through a shared-memory scratch of the warp (kResetScratch uint4: 32 blocks +
-// a 32-int rank->lane table), so a warp with k ending
-// episodes pays ceil(k * nb / 32) Philox rounds instead of nb serial ones.  Bitwise identical
-// to reset_env (integer Philox, owner-lane sampling).
+// Warp-cooperative reset (all 32 lanes must call; gids of a warp are consecutive): lane j of a
+// round draws Philox block (j mod nb) of the (j / nb)-th resetting lane and maps it to that
+// slot's four sampled values; the values reach their owner through the warp's shared-memory
+// scratch (kResetScratch uint4: 32 value slots + a 32-int rank->lane table).  A warp with k
+// ending episodes pays ceil(k nb / 32) Philox + sampling rounds instead of nb serial ones, and
+// the owners only assemble the quaternion.  Bitwise identical to reset_env (same integer
+// Philox, same per-value fma).
 __device__ __forceinline__ bool reset_env_warp(const DevParams& P, EnvReg& e, uint32_t gid, uint32_t ctr, bool need,
                                                float hfill[4], uint4* scratch)
 {
@@ -619,28 +628,28 @@ __device__ __forceinline__ bool reset_env_warp(const DevParams& P, EnvReg& e, ui
     int* tab = reinterpret_cast<int*>(scratch + 32);
     if (need) tab[rank] = lane;
     __syncwarp();
-    uint4 blk[8];
-    for (int base = 0; base < nr * nb; base += 32) {
-        const int j = base + lane;
-        uint4 x = make_uint4(0u, 0u, 0u, 0u);
+    float4 v[8];
+    const int per_round = 32 >> lnb;  // resets served per round
+    for (int round = 0; round * per_round < nr; ++round) {
+        const int j = round * 32 + lane;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
         if (j < nr * nb) {
             const int b = j & (nb - 1);
             const bool used = b < 4 || (b < 6 && (P.flags & F_DISTURBANCE)) || (b >= 6 && (P.flags & F_DOMAIN_RAND));
-            if (used) x = reset_block(P, gid - (uint32_t)lane + (uint32_t)tab[j >> lnb], ctr, b);
+            if (used) x = reset_values(P, b, reset_block(P, gid - (uint32_t)lane + (uint32_t)tab[j >> lnb], ctr, b));
         }
         __syncwarp();
-        scratch[lane] = x;
+        reinterpret_cast<float4*>(scratch)[lane] = x;
         __syncwarp();
-        if (need) {
+        if (need && rank / per_round == round) {
+            const float4* src = reinterpret_cast<const float4*>(scratch) + ((rank - round * per_round) << lnb);
 #pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const int sj = rank * nb + b - base;
-                if (b < nb && sj >= 0 && sj < 32) blk[b] = scratch[sj];
-            }
+            for (int b = 0; b < 8; ++b)
+                if (b < nb) v[b] = src[b];
         }
     }
     __syncwarp();
-    if (need) reset_from_blocks(P, blk, e, hfill);
+    if (need) reset_finish(P, v, e, hfill);
     return need;
 }
 

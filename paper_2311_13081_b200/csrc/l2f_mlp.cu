@@ -20,6 +20,8 @@
 //    128-thread named barrier; MMA
 //    completion is signalled through tcgen05.commit -> mbarrier.  The other two tiles' warps
 //    keep the FP32/INT pipes busy while one tile waits on the tensor core.
+#include <cstdio>
+
 #include "l2f_device.cuh"
 #include "l2f_internal.h"
 #include "l2f_tcgen05.cuh"
@@ -123,7 +125,26 @@ struct TileCtx {
     uint32_t bar_id;
     uint32_t phase;
     uint32_t r;               // thread index within the tile
+#ifdef L2F_PHASE_TIMING
+    uint32_t ph_last;         // debug build only: clock() at the last phase boundary
+#endif
 };
+
+// Debug build only (-DL2F_PHASE_TIMING): per-warp cycles spent in each phase of a tile-step,
+// accumulated in shared memory and printed by CTA 0 at exit (scripts/phase_timing.py).
+#ifdef L2F_PHASE_TIMING
+__shared__ unsigned long long g_ph[kThreads / 32][16];
+#define L2F_PHASE(c, k)                                                             \
+    do {                                                                            \
+        const uint32_t _n = (uint32_t)clock();                                      \
+        if ((threadIdx.x & 31) == 0) g_ph[threadIdx.x >> 5][k] += _n - (c).ph_last; \
+        (c).ph_last = _n;                                                           \
+    } while (0)
+#else
+#define L2F_PHASE(c, k) \
+    do {                \
+    } while (0)
+#endif
 
 // Epilogue of L1 / L2: accumulator row -> relu -> fp16 -> this thread's A2 row in TMEM.
 __device__ __forceinline__ void epilogue_hidden(const TileCtx& c)
@@ -173,7 +194,10 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
 {
     // descriptors = base descriptor + (byte offset >> 4) in the start-address field (addresses
     // stay below 256 KB, so the 14-bit field never carries)
+    L2F_PHASE(c, 0);
+    rot = __shfl_sync(0xffffffffu, rot, 0);  // warp-uniform for the compiler (uniform registers)
     handoff_to_mma(c);
+    L2F_PHASE(c, 1);
     if (c.r == 0) {
         tc::fence_after();
         const uint64_t dA1 = tc::make_desc(c.a1, kChunkA, 128);
@@ -187,9 +211,13 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
         tc::commit(c.mbar);
     }
     hook(1);
+    L2F_PHASE(c, 2);
     wait_mma(c);
+    L2F_PHASE(c, 3);
     epilogue_hidden(c);
+    L2F_PHASE(c, 4);
     handoff_to_mma(c);
+    L2F_PHASE(c, 5);
     if (c.r == 32) {
         tc::fence_after();
         const uint64_t dW2 = tc::make_desc(sbase + OFF_W2, kHid * 16, 128);
@@ -199,9 +227,13 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
         tc::commit(c.mbar);
     }
     hook(2);
+    L2F_PHASE(c, 6);
     wait_mma(c);
+    L2F_PHASE(c, 7);
     epilogue_hidden(c);
+    L2F_PHASE(c, 8);
     handoff_to_mma(c);
+    L2F_PHASE(c, 9);
     if (c.r == 64) {
         tc::fence_after();
         const uint64_t dW3 = tc::make_desc(sbase + OFF_W3, 256, 128);
@@ -211,6 +243,7 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
         tc::commit(c.mbar);
     }
     hook(3);
+    L2F_PHASE(c, 10);
     wait_mma(c);
     uint32_t v[4];
     tc::tmem_ld4(c.tmem_row, v);
@@ -218,6 +251,7 @@ __device__ __forceinline__ void mlp_tile(TileCtx& c, uint32_t sbase, int n_hist,
     tc::fence_before();
 #pragma unroll
     for (int j = 0; j < 4; ++j) a[j] = tanh_fast(__uint_as_float(v[j]));
+    L2F_PHASE(c, 11);
 }
 
 // Observation-noise normals of one step, stashed per thread in TMEM (columns 0..17 of the
@@ -287,8 +321,11 @@ __device__ void setup_cta(const PolicyDev& W, uint32_t sbase, int n_hist)
 __device__ __forceinline__ TileCtx make_ctx(uint32_t sbase)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int g = threadIdx.x / kM, r = threadIdx.x % kM;
-    const uint32_t tbase = *reinterpret_cast<const uint32_t*>(smem + OFF_TMEM);
+    // tile index and TMEM base broadcast from lane 0: the compiler then knows they are
+    // warp-uniform and keeps the MMA descriptors / TMEM addresses in uniform registers (no
+    // per-MMA R2UR waterfall loop in the issuing thread)
+    const int g = __shfl_sync(0xffffffffu, (int)(threadIdx.x / kM), 0), r = threadIdx.x % kM;
+    const uint32_t tbase = __shfl_sync(0xffffffffu, *reinterpret_cast<const uint32_t*>(smem + OFF_TMEM), 0);
     TileCtx c;
     c.a1 = sbase + OFF_A1 + g * kA1Bytes;
     c.a1_row = c.a1 + r * 16;
@@ -304,6 +341,11 @@ __device__ __forceinline__ TileCtx make_ctx(uint32_t sbase)
     c.bar_id = 1 + g;
     c.phase = 0;
     c.r = r;
+#ifdef L2F_PHASE_TIMING
+    if ((threadIdx.x & 31) == 0)
+        for (int k = 0; k < 16; ++k) g_ph[threadIdx.x >> 5][k] = 0ull;
+    c.ph_last = (uint32_t)clock();
+#endif
     tc::sts128(c.a1_row + 3 * kChunkA, 0u, 0u, 0u, 0u);  // K 24..31: constant zero pad
     return c;
 }
@@ -410,6 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             Trans o;
             transition<kDR>(P, W, e, gid, t, a, za, o);
+            L2F_PHASE(c, 12);
             uint32_t fl = o.flags;
             const bool ended = (fl & (D_TERM | D_TRUNC)) != 0;
             if (ended && active) stat_episode(st, o);
@@ -445,6 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            L2F_PHASE(c, 13);
             if (tr) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) tr[21 + q] = o.a[q];
@@ -479,6 +523,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             steps_done += (double)T;
         }
     }
+#ifdef L2F_PHASE_TIMING
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        for (int w = 0; w < kThreads / 32; ++w) {
+            printf("L2F_PHASE warp %d", w);
+            for (int k = 0; k < 14; ++k) printf(" %llu", g_ph[w][k]);
+            printf("\n");
+        }
+#endif
     // statistics: warp -> fixed-order block sum -> this CTA's slot
     double* srow = reinterpret_cast<double*>(smem + OFF_STAT);
     const int warp = threadIdx.x >> 5;
