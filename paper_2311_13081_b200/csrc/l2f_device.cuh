@@ -482,17 +482,18 @@ template <bool kDR>
 __device__ __forceinline__ void transition(const DevParams& P, const StageW& W, EnvReg& e, uint32_t gid,
                                            uint32_t t, const float a_in[4], const float z[4], Trans& o)
 {
+    // branch-free on the feature flags (selects), so several envs' transitions can share one
+    // basic block and interleave their dependency chains
     const bool act_noise = (P.flags & F_ACTION_NOISE) != 0;
+    const bool no_delay = (P.flags & F_NO_ROTOR_DELAY) != 0;
     float u[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const float v = act_noise ? fmaf(W.sigma_a, z[i], a_in[i]) : a_in[i];
         o.a[i] = fminf(fmaxf(v, -1.0f), 1.0f);
         u[i] = fmaf(o.a[i] + 1.0f, P.rpm_half_span, P.rpm_min);
-    }
-    if (P.flags & F_NO_ROTOR_DELAY) {  // ablation: rotors reach the setpoint instantly
-#pragma unroll
-        for (int i = 0; i < 4; ++i) e.s[13 + i] = u[i];
+        // ablation: rotors reach the setpoint instantly
+        e.s[13 + i] = no_delay ? u[i] : e.s[13 + i];
     }
     Phys ph;
     make_phys<kDR>(P, e, ph);
@@ -501,15 +502,14 @@ __device__ __forceinline__ void transition(const DevParams& P, const StageW& W, 
     const float* s = e.s;
     const float vv = s[7] * s[7] + s[8] * s[8] + s[9] * s[9];
     const float ww = s[10] * s[10] + s[11] * s[11] + s[12] * s[12];
-    const float r = div ? 0.0f : reward_of(W, s, o.a);  // Q26
-    bool term = div;
-    if (P.flags & F_TERMINATION) {
-        const float pinf = fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2])));
-        term |= (pinf > P.term_pos) | (vv > P.term_vel2) | (ww > P.term_angvel2);
-    }
+    const float rw = reward_of(W, s, o.a);
+    const float r = div ? 0.0f : rw;  // Q26
+    const float pinf = fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2])));
+    const bool out = (pinf > P.term_pos) | (vv > P.term_vel2) | (ww > P.term_angvel2);
+    const bool term = div | (((P.flags & F_TERMINATION) != 0) & out);
     e.ep_step += 1;
     e.ep_return += r;
-    const bool trunc = !term && P.max_ep > 0 && e.ep_step >= P.max_ep;
+    const bool trunc = (!term) & (P.max_ep > 0) & (e.ep_step >= P.max_ep);
     o.reward = r;
     o.flags = (term ? D_TERM : 0u) | (trunc ? D_TRUNC : 0u) | (div ? D_DIV : 0u);
     o.len = e.ep_step;
