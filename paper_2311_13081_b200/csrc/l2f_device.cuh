@@ -543,6 +543,22 @@ __device__ __forceinline__ float4 reset_values(const DevParams& P, int b, uint4 
                        fmaf(sp.w, unif(x.w), lo.w));
 }
 
+// The sampling table in shared memory (tab[b] = lo, tab[8 + b] = span of slot b): the
+// cooperative reset reads slot (lane mod nb), and a lane-divergent constant-bank index
+// serialises 8 ways.  Threads 0..15 copy; the caller synchronises before the first use.  (Kernels
+// without a barrier to spare pass tab = nullptr and index the constant bank instead.)
+__device__ __forceinline__ void reset_table_to_smem(const DevParams& P, float4* tab)
+{
+    if (threadIdx.x < 16) tab[threadIdx.x] = threadIdx.x < 8 ? P.rs_lo[threadIdx.x] : P.rs_span[threadIdx.x - 8];
+}
+
+__device__ __forceinline__ float4 reset_values_tab(const float4* tab, int b, uint4 x)
+{
+    const float4 lo = tab[b], sp = tab[8 + b];
+    return make_float4(fmaf(sp.x, unif(x.x), lo.x), fmaf(sp.y, unif(x.y), lo.y), fmaf(sp.z, unif(x.z), lo.z),
+                       fmaf(sp.w, unif(x.w), lo.w));
+}
+
 // Assemble the new episode from the sampled values of its 8 slots: state (uniform axis-angle
 // quaternion, Q17), disturbance, DR factors, episode counters; the history fill value per
 // rotor (Q10) in hfill.
@@ -614,8 +630,8 @@ __device__ __forceinline__ void reset_env(const DevParams& P, EnvReg& e, uint32_
 // ending episodes pays ceil(k nb / 32) Philox + sampling rounds instead of nb serial ones, and
 // the owners only assemble the quaternion.  Bitwise identical to reset_env (same integer
 // Philox, same per-value fma).
-__device__ __forceinline__ bool reset_env_warp(const DevParams& P, EnvReg& e, uint32_t gid, uint32_t ctr, bool need,
-                                               float hfill[4], uint4* scratch)
+__device__ __forceinline__ bool reset_env_warp(const DevParams& P, const float4* tab, EnvReg& e, uint32_t gid,
+                                               uint32_t ctr, bool need, float hfill[4], uint4* scratch)
 {
     const unsigned m = __ballot_sync(0xffffffffu, need);
     if (m == 0u) return false;
@@ -625,8 +641,8 @@ __device__ __forceinline__ bool reset_env_warp(const DevParams& P, EnvReg& e, ui
     const int nr = __popc(m);
     const int rank = __popc(m & ((1u << lane) - 1u));
     // rank -> lane table in the scratch's tail words (entries 32..39 hold 32 ints)
-    int* tab = reinterpret_cast<int*>(scratch + 32);
-    if (need) tab[rank] = lane;
+    int* rl = reinterpret_cast<int*>(scratch + 32);
+    if (need) rl[rank] = lane;
     __syncwarp();
     float4 v[8];
     const int per_round = 32 >> lnb;  // resets served per round
@@ -636,7 +652,10 @@ __device__ __forceinline__ bool reset_env_warp(const DevParams& P, EnvReg& e, ui
         if (j < nr * nb) {
             const int b = j & (nb - 1);
             const bool used = b < 4 || (b < 6 && (P.flags & F_DISTURBANCE)) || (b >= 6 && (P.flags & F_DOMAIN_RAND));
-            if (used) x = reset_values(P, b, reset_block(P, gid - (uint32_t)lane + (uint32_t)tab[j >> lnb], ctr, b));
+            if (used) {
+                const uint4 blk = reset_block(P, gid - (uint32_t)lane + (uint32_t)rl[j >> lnb], ctr, b);
+                x = tab ? reset_values_tab(tab, b, blk) : reset_values(P, b, blk);
+            }
         }
         __syncwarp();
         reinterpret_cast<float4*>(scratch)[lane] = x;

@@ -58,7 +58,8 @@ constexpr uint32_t OFF_W2 = OFF_W1H + kW1hBytes;
 constexpr uint32_t OFF_W3 = OFF_W2 + kW2Bytes;
 constexpr uint32_t OFF_BAR = OFF_W3 + kW3Bytes;       // kG MMA-done mbarriers (one per group)
 constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * kG;
-constexpr uint32_t OFF_STAT = (OFF_TMEM + 8 + 127) & ~127u;  // reset scratch (32 uint4 per warp); reused by stats
+constexpr uint32_t OFF_RTAB = (OFF_TMEM + 8 + 15) & ~15u;     // reset sampling table (16 float4)
+constexpr uint32_t OFF_STAT = (OFF_RTAB + 256 + 127) & ~127u;  // reset scratch (40 uint4 per warp); reused by stats
 constexpr uint32_t kScratchBytes = (kThreads / 32) * kResetScratch * 16;
 static_assert(kScratchBytes >= (kThreads / 32) * kStatsLen * 8, "stats rows fit in the scratch");
 constexpr uint32_t kSmemBytes = OFF_STAT + kScratchBytes;
@@ -331,9 +332,11 @@ __device__ __forceinline__ uint32_t hist_addr(const GroupCtx& c, int k, int p)
     return a1_row(c, k) + (4 + (p >> 1)) * kChunkA + (p & 1) * 8;
 }
 
-__device__ void setup_cta(const PolicyDev& W, uint32_t sbase, int n_hist)
+__device__ void setup_cta(const PolicyDev& W, uint32_t sbase, int n_hist, const DevParams* P = nullptr)
 {
+    extern __shared__ __align__(1024) uint8_t smem[];
     stage_weights(W, sbase, n_hist);
+    if (P) reset_table_to_smem(*P, reinterpret_cast<float4*>(smem + OFF_RTAB));
     if (threadIdx.x == 0) {
         for (int g = 0; g < kG; ++g) tc::mbar_init(sbase + OFF_BAR + 8 * g, 1);  // MMA done
         tc::fence_mbar_init();
@@ -403,11 +406,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sbase = tc::smem_u32(smem);
     const int NH = P.n_hist;
-    setup_cta(W, sbase, NH);
+    setup_cta(W, sbase, NH, &P);
     GroupCtx c = make_ctx(sbase);
     const int64_t N = P.n;
     const int r = threadIdx.x % kM;
     uint4* const rscratch = reinterpret_cast<uint4*>(smem + OFF_STAT) + (threadIdx.x >> 5) * kResetScratch;
+    const float4* const rtab = reinterpret_cast<const float4*>(smem + OFF_RTAB);
     StatAcc st;
     stat_zero(st);
     double steps_done = 0.0;
@@ -512,12 +516,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t fl = o[k].flags;
                 const bool ended = (fl & (D_TERM | D_TRUNC)) != 0;
                 if (ended && active[k]) stat_episode(st, o[k]);
+                L2F_PHASE(c, 14);
                 bool did_reset = false;
                 float hf[4];
                 if (P.flags & F_AUTO_RESET) {
-                    did_reset = reset_env_warp(P, e[k], gid[k], t + 1, ended && active[k], hf, rscratch);
+                    did_reset = reset_env_warp(P, rtab, e[k], gid[k], t + 1, ended && active[k], hf, rscratch);
                     if (did_reset) fl |= D_RESET;
                 }
+                L2F_PHASE(c, 15);
                 if (ended && !did_reset) {
                     e[k].ep_step = 0;
                     e[k].ep_return = 0.0f;
@@ -526,21 +532,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (!did_reset)
                         tc::sts64(hist_addr(c, k, wpos), tc::pack_h2(o[k].a[0], o[k].a[1]),
                                   tc::pack_h2(o[k].a[2], o[k].a[3]));
-                    // new episodes: the whole history row takes the fill value (Q10); the N_H/2
-                    // 16-byte chunks of each resetting lane's row are written by N_H/2 lanes at once
-                    unsigned rm = __ballot_sync(0xffffffffu, did_reset);
-                    if (rm) {
+                    // new episode: the lane's whole history row takes the fill value (Q10):
+                    // N_H/2 16-byte stores by the resetting lanes only
+                    if (did_reset) {
                         const uint32_t h01 = tc::pack_h2(hf[0], hf[1]), h23 = tc::pack_h2(hf[2], hf[3]);
-                        const int lane = threadIdx.x & 31;
-                        while (rm) {
-                            const int src = __ffs(rm) - 1;
-                            rm &= rm - 1u;
-                            const uint32_t v01 = __shfl_sync(0xffffffffu, h01, src);
-                            const uint32_t v23 = __shfl_sync(0xffffffffu, h23, src);
-                            if (lane < NH / 2)
-                                tc::sts128(a1_row(c, k) + (uint32_t)(src - lane) * 16u + (4 + lane) * kChunkA, v01,
-                                           v23, v01, v23);
-                        }
+#pragma unroll
+                        for (int q = 0; q < kMaxHist / 2; ++q)
+                            if (q < NH / 2) tc::sts128(a1_row(c, k) + (4 + q) * kChunkA, h01, h23, h01, h23);
                     }
                 }
                 float* tr = (tslot[k] >= 0) ? trace + ((int64_t)ks * K + tslot[k]) * kTraceFields : nullptr;
@@ -589,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (blockIdx.x == 0 && threadIdx.x == 0)
         for (int w = 0; w < kThreads / 32; ++w) {
             printf("L2F_PHASE warp %d", w);
-            for (int k = 0; k < 14; ++k) printf(" %llu", g_ph[w][k]);
+            for (int k = 0; k < 16; ++k) printf(" %llu", g_ph[w][k]);
             printf("\n");
         }
 #endif
