@@ -109,8 +109,15 @@ __device__ __forceinline__ void stats_block_end(const StatAcc& st, double* srow,
 #pragma unroll
         for (int j = 0; j < kStatsLen; ++j) srow[warp * kStatsLen + j] = 0.0;
     }
-    __syncthreads();
-    stat_rows_to_slot(srow, nw, steps, slot);
+    // producer/consumer named barrier: warps 1.. arrive and retire at once, warp 0 waits for
+    // the rows and writes the block's slot (the block's SM slot frees up sooner than with a
+    // full __syncthreads)
+    if (warp == 0) {
+        asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
+        stat_rows_to_slot(srow, nw, steps, slot);
+    } else {
+        asm volatile("bar.arrive 1, %0;" ::"r"(blockDim.x) : "memory");
+    }
 }
 
 // ---------------------------------------------------------------------------------------

@@ -206,7 +206,7 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
     rot = __shfl_sync(0xffffffffu, rot, 0);  // warp-uniform for the compiler (uniform registers)
     handoff_to_mma(c);
     L2F_PHASE(c, 1);
-    if (c.r == 0) {
+    if (c.r / 32 == 0) {  // the whole warp, converged; elect.sync picks the issuing lane
         tc::fence_after();
         const uint64_t dW1o = tc::make_desc(sbase + OFF_W1O, kHid * 16, 128);
         const uint64_t dW1h = tc::make_desc(sbase + OFF_W1H, 128, 2u * 4u * (uint32_t)n_hist * 16u) + 4u * rot;
@@ -215,12 +215,14 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
             // L1: obs part (K = 32) then history (K = 4 N_H) with the rotated W1 history block
             const uint64_t dA1 = tc::make_desc(c.a1 + k * kA1Bytes, kChunkA, 128);
             const uint32_t d = c.tmem_tile + 64 * k;
-            tc::mma_f16(d, dA1, dW1o, kIdescN64, 0);
-            tc::mma_f16(d, dA1 + 2 * kChunkA / 16, dW1o + 2 * (kHid * 16) / 16, kIdescN64, 1);
-            for (int j = 0; j < n_hist / 4; ++j)
-                tc::mma_f16(d, dA1 + (4 + 2 * j) * (kChunkA / 16), dW1h + 16u * j, kIdescN64BMN, 1);
+            tc::mma_f16_elect(d, dA1, dW1o, kIdescN64, 0);
+            tc::mma_f16_elect(d, dA1 + 2 * kChunkA / 16, dW1o + 2 * (kHid * 16) / 16, kIdescN64, 1);
+#pragma unroll
+            for (int j = 0; j < kMaxHist / 4; ++j)
+                if (j < n_hist / 4)
+                    tc::mma_f16_elect(d, dA1 + (4 + 2 * j) * (kChunkA / 16), dW1h + 16u * j, kIdescN64BMN, 1);
         }
-        tc::commit(c.mbar);
+        tc::commit_elect(c.mbar);
     }
     hook(1);
     L2F_PHASE(c, 2);
@@ -232,16 +234,16 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
     L2F_PHASE(c, 4);
     handoff_to_mma(c);
     L2F_PHASE(c, 5);
-    if (c.r == 32) {
+    if (c.r / 32 == 1) {
         tc::fence_after();
         const uint64_t dW2 = tc::make_desc(sbase + OFF_W2, kHid * 16, 128);
 #pragma unroll
         for (int k = 0; k < kE; ++k)
 #pragma unroll
             for (int j = 0; j < 5; ++j)  // A from TMEM; j = 4: the ones column (bias row of W2)
-                tc::mma_f16_ts(c.tmem_tile + 64 * k, c.a2_tmem + 40 * k + 8 * j, dW2 + j * (2 * kHid * 16 / 16),
+                tc::mma_f16_ts_elect(c.tmem_tile + 64 * k, c.a2_tmem + 40 * k + 8 * j, dW2 + j * (2 * kHid * 16 / 16),
                                kIdescN64, j);
-        tc::commit(c.mbar);
+        tc::commit_elect(c.mbar);
     }
     hook(2);
     L2F_PHASE(c, 6);
@@ -253,16 +255,16 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
     L2F_PHASE(c, 8);
     handoff_to_mma(c);
     L2F_PHASE(c, 9);
-    if (c.r == 64) {
+    if (c.r / 32 == 2) {
         tc::fence_after();
         const uint64_t dW3 = tc::make_desc(sbase + OFF_W3, 256, 128);
 #pragma unroll
         for (int k = 0; k < kE; ++k)
 #pragma unroll
             for (int j = 0; j < 5; ++j)
-                tc::mma_f16_ts(c.tmem_tile + 64 * k, c.a2_tmem + 40 * k + 8 * j, dW3 + j * (2 * 256 / 16),
+                tc::mma_f16_ts_elect(c.tmem_tile + 64 * k, c.a2_tmem + 40 * k + 8 * j, dW3 + j * (2 * 256 / 16),
                                kIdescN16, j);
-        tc::commit(c.mbar);
+        tc::commit_elect(c.mbar);
     }
     hook(3);
     L2F_PHASE(c, 10);
@@ -483,11 +485,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 write_obs_row(c, k, ob);
             }
             float a[kE][4], za[kE][4];
+            // noise draws inside the MMA latency, unconditionally (no flag branch splits the
+            // independent Philox chains into separate basic blocks; unused draws are discarded)
             mlp_group(c, sbase, NH, rot, a, [&](int l) {
 #pragma unroll
                 for (int k = 0; k < kE; ++k) {
-                    if (l == 1) action_noise(P, gid[k], t, za[k]);
-                    if (obs_noise) stash_obs_noise(P, c, k, gid[k], t + 1, l - 1);
+                    if (l == 1) {
+                        box_muller2(draw(P, gid[k], t, S_ACT, 0), za[k]);
+                        const bool an = (P.flags & F_ACTION_NOISE) != 0;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) za[k][q] = an ? za[k][q] : 0.0f;
+                    }
+                    stash_obs_noise(P, c, k, gid[k], t + 1, l - 1);
                 }
             });
             if (NH > 0 && ++rot == (uint32_t)NH) rot = 0;
