@@ -251,6 +251,15 @@ L2F_API l2f_status l2f_rollout_host(l2f_env* env, const l2f_policy* h_policy, in
 L2F_API l2f_status l2f_get_state(l2f_env* env, l2f_state_view* out);
 L2F_API l2f_status l2f_set_t(l2f_env* env, uint64_t t);
 
+/* Checkpoint restore (SURVEY 8(b) set_state): asynchronously copies every non-NULL
+ * array of `in` (caller-owned DEVICE buffers in the l2f_state_view layouts above) into the
+ * env's workspace on `stream`, then sets the step counter to in->t.  in->num_envs and
+ * in->action_history must equal the env's (INVALID_ARGUMENT otherwise; nothing copied).
+ * NULL arrays keep the current contents.  q is not re-normalised (precondition ||q|| = 1).
+ * Restoring a snapshot taken with l2f_get_state (copied out) resumes the run bitwise:
+ * the RNG is keyed by (env id, t), not by a stateful generator. */
+L2F_API l2f_status l2f_set_state(l2f_env* env, const l2f_state_view* in, void* stream);
+
 /* Actor MLP forward on explicit observations (the same tcgen05 tile code as the rollout):
  * d_obs [N][in_dim] fp32, d_act [N][4] fp32 (tanh output, before noise). */
 L2F_API l2f_status l2f_policy_forward(const l2f_policy* policy, const float* d_obs, float* d_act,

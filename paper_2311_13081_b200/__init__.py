@@ -125,6 +125,46 @@ class Env:
     def t(self, value: int):
         _check(lib().l2f_set_t(self.h, int(value)), "l2f_set_t")
 
+    def get_state(self) -> dict:
+        """Copy of the full env state (device tensors) for checkpointing; see set_state."""
+        return {"state": self.state.clone(), "dist": self.dist.clone(), "dr": self.dr.clone(),
+                "hist": self.hist.clone(), "hist_t0": self.hist_t0.clone(), "hist_fill": self.hist_fill.clone(),
+                "ep_step": self.ep_step.clone(), "ep_return": self.ep_return.clone(), "t": self.t}
+
+    def set_state(self, snap: dict, stream=None):
+        """l2f_set_state: restore (a subset of) a get_state() snapshot; missing keys stay."""
+        v = lib().StateView()
+        keep = []
+
+        def ptr(name, dtype):
+            x = snap.get(name)
+            if x is None:
+                return None
+            x = x.to(device=self.device, dtype=dtype).contiguous()
+            keep.append(x)
+            return C.c_void_p(x.data_ptr())
+
+        v.state = ptr("state", torch.float32)
+        v.dist = ptr("dist", torch.float32)
+        v.dr = ptr("dr", torch.float32)
+        v.hist = ptr("hist", torch.float32)
+        v.hist_t0 = ptr("hist_t0", torch.int32)
+        v.hist_fill = ptr("hist_fill", torch.float32)
+        v.ep_step = ptr("ep_step", torch.int32)
+        v.ep_return = ptr("ep_return", torch.float32)
+        v.t = int(snap.get("t", self.t))
+        # sizes as the snapshot has them (the library rejects a mismatch before copying)
+        ns = {int(snap[k].shape[-1]) for k in ("state", "dist", "dr", "hist", "hist_t0", "hist_fill", "ep_step",
+                                                "ep_return") if snap.get(k) is not None}
+        if len(ns) > 1:
+            raise L2FError(f"set_state: inconsistent env counts {sorted(ns)}")
+        v.num_envs = ns.pop() if ns else self.n
+        h = snap.get("hist")
+        v.action_history = (int(h.shape[0]) if self.n_hist > 0 else 0) if h is not None else self.n_hist
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(lib().l2f_set_state(self.h, C.byref(v), C.c_void_p(s.cuda_stream)), "l2f_set_state")
+        s.synchronize()  # the source tensors in `keep` must outlive the copies
+
     def make_out(self, obs_core=True, reward=True, flags=True, final_state=False, obs_dense=False,
                  obs_critic=False):
         d = self.device

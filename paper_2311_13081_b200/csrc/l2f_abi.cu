@@ -539,6 +539,39 @@ l2f_status l2f_set_t(l2f_env* env, uint64_t t)
     return L2F_OK;
 }
 
+l2f_status l2f_set_state(l2f_env* env, const l2f_state_view* in, void* stream)
+{
+    if (!env || !in) return fail(L2F_ERR_INVALID_ARGUMENT, "env/in is NULL");
+    const int64_t N = env->cfg.num_envs;
+    const int32_t NH = env->cfg.action_history;
+    if (in->num_envs != N || in->action_history != NH)
+        return fail(L2F_ERR_INVALID_ARGUMENT, "set_state: num_envs/action_history differ from the env's");
+    if (in->t >= (1ull << 31)) return fail(L2F_ERR_INVALID_ARGUMENT, "t must be < 2^31");
+    const cudaStream_t s = (cudaStream_t)stream;
+    const size_t n = (size_t)N;
+    struct Part {
+        void* dst;
+        const void* src;
+        size_t bytes;
+    } parts[] = {
+        {env->B.state, in->state, 4 * n * L2F_STATE_DIM},
+        {env->B.dist, in->dist, 4 * n * L2F_DIST_DIM},
+        {env->B.dr, in->dr, 4 * n * L2F_DR_DIM},
+        {env->B.hist, in->hist, 4 * n * 4 * (size_t)(NH > 0 ? NH : 1)},
+        {env->B.hist_t0, in->hist_t0, 4 * n},
+        {env->B.hist_fill, in->hist_fill, 4 * n * 4},
+        {env->B.ep_step, in->ep_step, 4 * n},
+        {env->B.ep_return, in->ep_return, 4 * n},
+    };
+    for (const Part& p : parts) {
+        if (!p.src || p.src == p.dst) continue;
+        const cudaError_t e = cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return fail(L2F_ERR_CUDA, cudaGetErrorString(e));
+    }
+    env->t = in->t;
+    return L2F_OK;
+}
+
 l2f_status l2f_policy_forward(const l2f_policy* policy, const float* d_obs, float* d_act, int64_t n, void* stream)
 {
     if (!policy || !d_obs || !d_act || n <= 0) return fail(L2F_ERR_INVALID_ARGUMENT, "bad policy_forward arguments");

@@ -229,3 +229,38 @@ def test_mlp_rollout_distribution_matches_oracle(pkg):
     assert abs(r_g - r_o) <= 4 * np.sqrt(2) * se_r, (r_g, r_o, se_r)
     assert abs(st[0] - ost[0]) <= 4 * np.sqrt(ost[0]) + 0.02 * ost[0]
     assert abs(m_g - m_o) <= 0.05 * m_o
+
+
+@pytest.mark.gpu
+def test_set_state_checkpoint_resume_bitwise(pkg):
+    """l2f_set_state: a snapshot taken mid-run (l2f_get_state, copied out) restored into a
+    fresh env resumes bitwise -- MLP rollout and single steps (the RNG is keyed by (id, t))."""
+    cfg = inputs.config_c5()
+    n = 3 * 128 + 45
+    W = inputs.policy_weights(146, 64, seed=5, out_bias=inputs.hover_policy_bias())
+    pol = pkg.Policy(W)
+    ref = pkg.Env(cfg, n)
+    ref.reset()
+    ref.rollout(40, policy=pol)
+    ckpt = ref.get_state()
+    assert ckpt["t"] == 40
+    ref.rollout(35, policy=pol)
+    acts = torch.rand(4, n, device="cuda") * 2 - 1
+    ref.step(acts)
+    want = snapshot(ref)
+    env = pkg.Env(cfg, n)
+    env.reset()
+    env.rollout(7, policy=pol)  # some other state, overwritten entirely
+    env.set_state(ckpt)
+    assert env.t == 40
+    env.rollout(35, policy=pol)
+    env.step(acts)
+    got = snapshot(env)
+    for k in want:
+        assert np.array_equal(want[k], got[k]), k
+    # partial restore keeps the other arrays; a mismatched view is rejected
+    env.set_state({"ep_step": torch.zeros(n, dtype=torch.int32, device="cuda"), "t": 3})
+    assert env.t == 3 and int(env.ep_step.abs().sum()) == 0
+    bad = pkg.Env(cfg, n + 1)
+    with pytest.raises(Exception):
+        bad.set_state(ckpt)
