@@ -124,6 +124,13 @@ def lib():
         L.or_rollout.argtypes = [C.POINTER(Config), C.c_void_p, C.c_void_p, C.c_int64, C.c_uint64,
                                  C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, dp,
                                  C.c_int32]
+        L.or_lissajous.argtypes = [C.c_double] * 5 + [dp, dp]
+        L.or_shift_observation.argtypes = [dp, dp, dp, C.c_double, C.c_double]
+        L.or_hover_rpm.restype = C.c_double
+        L.or_hover_rpm.argtypes = [C.POINTER(Params)]
+        L.or_track.argtypes = [C.POINTER(Config), C.c_void_p, C.c_uint64, C.c_uint64, C.c_double, C.c_double,
+                               C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32, dp, dp,
+                               C.POINTER(C.c_int32), C.c_void_p]
         for f in ("or_sizeof_config", "or_sizeof_env", "or_sizeof_step_out"):
             getattr(L, f).restype = C.c_int64
         assert L.or_sizeof_config() == C.sizeof(Config), "oracle Config mirror out of sync"
@@ -386,3 +393,39 @@ def rollout(cfg: dict, envs: np.ndarray, env_ids, t0: int, T: int, mode: int,
                      C.byref(policy.s) if policy is not None else None,
                      tr.ctypes.data if tr is not None else None, _dp(stats), int(nthreads))
     return stats, tr
+
+
+# ---- Lissajous tracking evaluation (f3) ------------------------------------------------
+def lissajous(t: float, Tc: float, ax: float = 1.0, ay: float = 0.5, z: float = 0.0):
+    """Reference position and velocity at time t (Q28)."""
+    p, v = np.zeros(3), np.zeros(3)
+    lib().or_lissajous(float(t), float(Tc), float(ax), float(ay), float(z), _dp(p), _dp(v))
+    return p, v
+
+
+def shift_observation(obs, p_ref, v_ref, clip_pos: float, clip_vel: float) -> np.ndarray:
+    """Setpoint shifting with clipping (Q29) applied to an observation vector."""
+    o = _d(obs).copy()
+    lib().or_shift_observation(_dp(o), _dp(_d(p_ref)), _dp(_d(v_ref)), float(clip_pos), float(clip_vel))
+    return o
+
+
+def hover_rpm(params: Params) -> float:
+    return lib().or_hover_rpm(C.byref(params))
+
+
+def track(cfg: dict, policy: PolicyHandle | None, env_id: int, t0: int, Tc: float, n_steps: int,
+          ax: float = 1.0, ay: float = 0.5, z: float = 0.0, clip_pos: float | None = None,
+          clip_vel: float | None = None, trace: bool = False):
+    """One env's Lissajous tracking run (Q28-Q31).  policy None = exact hover action.
+    Returns (rmse, rmse_xy, steps_ok, positions[n_steps][3] or None)."""
+    c = config(cfg)
+    cp = cfg["init_pos"] if clip_pos is None else clip_pos
+    cv = cfg["init_vel"] if clip_vel is None else clip_vel
+    r, rxy = C.c_double(), C.c_double()
+    ok = C.c_int32()
+    tr = np.zeros((n_steps, 3)) if trace else None
+    lib().or_track(C.byref(c), C.byref(policy.s) if policy is not None else None, int(env_id), int(t0),
+                   float(Tc), float(ax), float(ay), float(z), float(cp), float(cv), int(n_steps),
+                   C.byref(r), C.byref(rxy), C.byref(ok), tr.ctypes.data if tr is not None else None)
+    return r.value, rxy.value, ok.value, tr

@@ -20,7 +20,8 @@
  * free fall z = -g t^2/2, discrete motor-lag closed form and the 63 % step response,
  * single-axis roll/yaw torque closed forms, RK4 4th-order convergence, reward special cases
  * (P:148-151), termination edge cases, curriculum closed form, reset-distribution
- * bounds/moments, MLP vs numpy matmul on fp16-rounded operands.
+ * bounds/moments, MLP vs numpy matmul on fp16-rounded operands, Lissajous reference closed
+ * forms and the exact-hover tracking RMSE (sqrt(13/8) over whole cycles).
  * Parity unpinned: long free-running closed-loop MLP trajectories (checked teacher-forced and
  * by distribution only); absolute physical constants (P:21 - the paper's
  * parameter PDF is absent).
@@ -735,6 +736,119 @@ void or_rollout(const or_config* cfg, or_env* envs, const uint64_t* env_ids, int
         for (int j = 0; j < OR_ST_LEN; ++j) stats[j] += jobs[w].stats[j];
     free(jobs);
     free(th);
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Lissajous trajectory tracking evaluation (Table III analogue).         */
+/* ------------------------------------------------------------------------------------ */
+
+/* Figure-eight reference: p(t) = [A_x cos(2 pi t/T), A_y sin(4 pi t/T), z]
+ * with A_x = 1, A_y = 1/2 in the paper's formula; v(t) = dp/dt analytically (Q28). */
+void or_lissajous(double t, double Tc, double ax, double ay, double z, double p[3], double v[3])
+{
+    double w = 2.0 * M_PI / Tc;
+    p[0] = ax * cos(w * t);
+    p[1] = ay * sin(2.0 * w * t);
+    p[2] = z;
+    v[0] = -ax * w * sin(w * t);
+    v[1] = 2.0 * ay * w * cos(2.0 * w * t);
+    v[2] = 0.0;
+}
+
+/* Setpoint shifting with clipping (Q29): the actor observes p - p_ref and v - v_ref,
+ * each component clipped to +-clip; the rest of the observation is unchanged.  Applied to
+ * the (noisy) observation vector from or_observe. */
+void or_shift_observation(double* obs, const double p_ref[3], const double v_ref[3], double clip_pos,
+                          double clip_vel)
+{
+    for (int j = 0; j < 3; ++j) {
+        obs[j] = fmin(fmax(obs[j] - p_ref[j], -clip_pos), clip_pos);
+        obs[12 + j] = fmin(fmax(obs[12 + j] - v_ref[j], -clip_vel), clip_vel);
+    }
+}
+
+/* Hover rotor speed: 4 f(w) = m g with f(w) = c0 + c1 w + c2 w^2 (nominal parameters). */
+double or_hover_rpm(const or_params* P)
+{
+    double c0 = P->thrust_c[0] - P->mass * P->gravity / 4.0, c1 = P->thrust_c[1], c2 = P->thrust_c[2];
+    if (c2 == 0.0) return -c0 / c1;
+    return (-c1 + sqrt(c1 * c1 - 4.0 * c2 * c0)) / (2.0 * c2);
+}
+
+/* One env's tracking run (Q28-Q31): start at p_ref(0) at rest (q = identity, w = 0, rotors
+ * at hover, no disturbance, nominal parameters, history filled with the normalised hover
+ * speed), then n_steps steps of: shifted observation (noise per cfg) -> deterministic actor
+ * (pol; pol == NULL applies the exact hover action) -> env transition without exploration
+ * noise -> error e_k = p_k - p_ref(k dt).  Termination (cfg TERMINATION flag) is tested on
+ * the tracking-error state (p - p_ref, v - v_ref, w) with the training bounds, plus
+ * divergence; the run stops accumulating at the first termination.  Outputs RMSE over the
+ * completed steps (3-D and x-y) and the number of completed steps.  The Philox counter of
+ * step k is t0 + k (as in a rollout). */
+void or_track(const or_config* cfg_in, const or_policy* pol, uint64_t env_id, uint64_t t0, double Tc,
+              double ax, double ay, double z, double clip_pos, double clip_vel, int32_t n_steps,
+              double* rmse, double* rmse_xy, int32_t* steps_ok, double* pos_trace)
+{
+    or_config cfg = *cfg_in;
+    cfg.flags &= ~(uint32_t)(OR_ACTION_NOISE | OR_AUTO_RESET | OR_DISTURBANCE | OR_DOMAIN_RAND);
+    or_env e;
+    memset(&e, 0, sizeof(e));
+    double pr[3], vr[3];
+    or_lissajous(0.0, Tc, ax, ay, z, pr, vr);
+    e.s[0] = pr[0];
+    e.s[1] = pr[1];
+    e.s[2] = pr[2];
+    e.s[3] = 1.0;
+    double w_h = or_hover_rpm(&cfg.nominal);
+    double a_h = 2.0 * (w_h - cfg.nominal.rpm_min) / (cfg.nominal.rpm_max - cfg.nominal.rpm_min) - 1.0;
+    for (int i = 0; i < 4; ++i) e.s[13 + i] = w_h;
+    for (int i = 0; i < 5; ++i) e.dr[i] = 1.0;
+    for (int k = 0; k < 32; ++k)
+        for (int i = 0; i < 4; ++i) e.hist[k][i] = a_h;
+    int obs_dim = 18 + 4 * cfg.n_hist;
+    double* obs = (double*)malloc(sizeof(double) * (size_t)obs_dim);
+    double se = 0.0, sexy = 0.0;
+    int32_t ok = 0;
+    for (int32_t k = 0; k < n_steps; ++k) {
+        uint64_t t = t0 + (uint64_t)k;
+        double a[4];
+        if (pol) {
+            or_observe(&cfg, &e, env_id, t, obs);
+            or_lissajous((double)k * cfg.dt, Tc, ax, ay, z, pr, vr);
+            or_shift_observation(obs, pr, vr, clip_pos, clip_vel);
+            or_mlp(pol, obs, a);
+        } else {
+            for (int i = 0; i < 4; ++i) a[i] = a_h;
+        }
+        or_step_out so;
+        uint32_t flags_saved = cfg.flags;
+        cfg.flags &= ~(uint32_t)OR_TERMINATION; /* tested on the error state below */
+        or_env_step(&cfg, &e, env_id, t, a, &so, NULL);
+        cfg.flags = flags_saved;
+        or_lissajous((double)(k + 1) * cfg.dt, Tc, ax, ay, z, pr, vr);
+        double ex = e.s[0] - pr[0], ey = e.s[1] - pr[1], ez = e.s[2] - pr[2];
+        double dvx = e.s[7] - vr[0], dvy = e.s[8] - vr[1], dvz = e.s[9] - vr[2];
+        double ww = e.s[10] * e.s[10] + e.s[11] * e.s[11] + e.s[12] * e.s[12];
+        int term = (so.flags & OR_FLAG_DIVERGED) != 0;
+        if (cfg.flags & OR_TERMINATION) {
+            double einf = fmax(fabs(ex), fmax(fabs(ey), fabs(ez)));
+            if (einf > cfg.term_pos || dvx * dvx + dvy * dvy + dvz * dvz > cfg.term_vel * cfg.term_vel ||
+                ww > cfg.term_angvel * cfg.term_angvel)
+                term = 1;
+        }
+        if (pos_trace) {
+            pos_trace[3 * k + 0] = e.s[0];
+            pos_trace[3 * k + 1] = e.s[1];
+            pos_trace[3 * k + 2] = e.s[2];
+        }
+        if (term) break;
+        se += ex * ex + ey * ey + ez * ez;
+        sexy += ex * ex + ey * ey;
+        ok = k + 1;
+    }
+    free(obs);
+    *rmse = ok > 0 ? sqrt(se / ok) : 0.0;
+    *rmse_xy = ok > 0 ? sqrt(sexy / ok) : 0.0;
+    *steps_ok = ok;
 }
 
 /* Size checks for the Python mirror. */

@@ -632,3 +632,71 @@ def test_recompute_reward_matches_step_reward_and_stages():
     bad = np.array(so.final_s)
     bad[4] = np.nan
     assert oracle.recompute_reward(cfg, 25, bad, so.a_applied) == 0.0
+
+
+# ---- f3: Lissajous tracking evaluation (Table III; Q28-Q31) -------------
+
+def test_lissajous_reference_closed_forms():
+    """p(t) = [cos(2 pi t/T), sin(4 pi t/T)/2, z]: the paper's special points, and the
+    velocity pinned as the numerical derivative of the position (not a retyped formula)."""
+    T, z = 5.5, 1.25
+    p, v = oracle.lissajous(0.0, T, 1.0, 0.5, z)
+    assert np.allclose(p, [1, 0, z], atol=1e-15) and np.allclose(v, [0, 2 * math.pi / T, 0], atol=1e-15)
+    p, _ = oracle.lissajous(T / 2, T, 1.0, 0.5, z)
+    assert np.allclose(p, [-1, 0, z], atol=1e-14)
+    p, _ = oracle.lissajous(T / 4, T, 1.0, 0.5, z)
+    assert np.allclose(p, [0, 0, z], atol=1e-14)  # the figure-eight crossing
+    p, _ = oracle.lissajous(T / 8, T, 1.0, 0.5, z)
+    assert np.isclose(p[1], 0.5, atol=1e-14)      # maximal y excursion = the amplitude 1/2
+    rng = np.random.default_rng(3)
+    for t in rng.uniform(0, 3 * T, 5):
+        h = 1e-6
+        pp, v = oracle.lissajous(t, T)
+        fd = (oracle.lissajous(t + h, T)[0] - oracle.lissajous(t - h, T)[0]) / (2 * h)
+        assert np.allclose(v, fd, atol=1e-8)
+    # peak speed of the fast (3.5 s) trajectory: order of the paper's "up to 3 m/s" (P:307)
+    sp = max(np.linalg.norm(oracle.lissajous(t, 3.5)[1]) for t in np.linspace(0, 3.5, 701))
+    assert 2.0 < sp < 3.5
+
+
+def test_setpoint_shift_identity_and_clipping():
+    cfg = inputs.config_c4()
+    e = oracle.reset(cfg, 7, 0)
+    o = oracle.observe(cfg, e, 7, 5)
+    # zero reference: identity (as long as the observation is inside the bounds)
+    z3 = np.zeros(3)
+    big = 1e9
+    assert np.array_equal(oracle.shift_observation(o, z3, z3, big, big), o)
+    # shift + clip, exactly at the bound; every other component untouched
+    pr, vr = np.array([5.0, -5.0, o[2]]), np.array([0.0, 0.0, -7.0])
+    s = oracle.shift_observation(o, pr, vr, 0.3, 1.0)
+    assert s[0] == -0.3 and s[1] == 0.3 and s[2] == 0.0
+    assert s[12] == min(max(o[12], -1.0), 1.0) and s[14] == 1.0
+    keep = np.r_[3:12, 15:len(o)]
+    assert np.array_equal(s[keep], o[keep])
+
+
+def test_tracking_rmse_exact_hover_closed_form():
+    """A vehicle that holds its start point (exact hover action, no termination) tracking the
+    unit figure-eight from p_ref(0) = (1, 0, z): e^2 = (cos th - 1)^2 + sin^2(2 th)/4, whose mean
+    over whole cycles is 3/2 + 1/8, so RMSE = RMSE_xy = sqrt(13/8) (z error 0)."""
+    cfg = inputs.config_c4()
+    cfg["flags"] &= ~4  # no termination: the full run is scored
+    for T, cycles in ((5.5, 1), (3.5, 2), (15.0, 1)):
+        n = int(round(T / cfg["dt"])) * cycles
+        r, rxy, ok, pos = oracle.track(cfg, None, 0, 0, T, n, z=1.0, trace=True)
+        assert ok == n
+        assert abs(r - math.sqrt(13 / 8)) < 1e-9 and abs(rxy - r) < 1e-12
+        assert np.abs(pos - [1.0, 0.0, 1.0]).max() < 1e-9  # hover: the vehicle does not move
+
+
+def test_tracking_terminates_on_error_state():
+    """With termination on, the hovering vehicle fails when |x error| = 1 - cos(th) first
+    exceeds term_pos (|y error| <= 1/2 < 0.6 and the speed error stays < 10 m/s)."""
+    cfg = inputs.config_c4()
+    T = 5.5
+    n = int(round(T / cfg["dt"]))
+    _, _, ok, _ = oracle.track(cfg, None, 0, 0, T, n)
+    th = math.acos(1.0 - cfg["term_pos"])
+    k_fail = math.floor(th * n / (2 * math.pi)) + 1  # first k with 1 - cos(2 pi k / n) > term_pos
+    assert ok == k_fail - 1
