@@ -246,6 +246,37 @@ L2F_API l2f_status l2f_step_host(l2f_env* env, const float* h_actions, float* h_
 L2F_API l2f_status l2f_rollout_host(l2f_env* env, const l2f_policy* h_policy, int32_t T,
                             double* h_stats, int32_t reset_accumulators, void* stream);
 
+/* ---- Lissajous tracking evaluation (Table III) ------ */
+
+/* Figure-eight reference p_ref(t) = [amp_x cos(2 pi t/T_c), amp_y sin(4 pi t/T_c), altitude]
+ * (the paper's [cos(2 pi t/T), sin(4 pi t/T)/2, const] is amp_x = 1, amp_y = 0.5), v_ref its
+ * analytic derivative, t = k dt for tracking step k (Q28). */
+typedef struct {
+    const float* cycle_time;  /* [N] device: cycle time T_c of each env (s, > 0); a batch can
+                                 sweep T_c (Table III: 15, 5.5, 3.5 s)                      */
+    double amp_x, amp_y, altitude;
+    double clip_pos, clip_vel; /* setpoint-shift clipping bounds (Q29), > 0          */
+    int32_t n_steps;           /* steps simulated, >= 1                                     */
+    float* rmse;               /* [N] out: RMSE of p - p_ref over x, y, z (m), completed steps */
+    float* rmse_xy;            /* [N] out: the same over x, y                                */
+    int32_t* steps_ok;         /* [N] out: steps completed before the first termination (Q31);
+                                  n_steps = the run succeeded                               */
+} l2f_tracking;
+
+/* Batched tracking of the reference by the actor with setpoint shifting: every env
+ * starts at p_ref(0) at rest (q = identity, w = 0, rotors at the hover speed, history filled
+ * with the hover action, no disturbance, nominal parameters; Q30); each step the actor sees
+ * its observation (noise per cfg.flags) with p and v replaced by clip(p - p_ref) and
+ * clip(v - v_ref) (Q29), acts deterministically (no exploration noise), the env transitions
+ * (RK4), and the error p - p_ref at the new time accumulates (FP64) until the first
+ * termination, which (with L2F_TERMINATION) is tested on the tracking-error state
+ * (|p - p_ref|_inf, |v - v_ref|, |w| against the training bounds) or on divergence (Q31).
+ * Overwrites the env state (it ends in the final tracking state with a valid history ring;
+ * call l2f_reset before training again) and advances t by n_steps.  Needs a policy
+ * (in_dim 18 + 4 N_H, N_H % 4 == 0).  INVALID_ARGUMENT for NULL pointers, n_steps < 1 or
+ * clip bounds <= 0. */
+L2F_API l2f_status l2f_track(l2f_env* env, const l2f_policy* policy, const l2f_tracking* spec, void* stream);
+
 /* ---- state access --------------------------------------------------------------------- */
 
 L2F_API l2f_status l2f_get_state(l2f_env* env, l2f_state_view* out);

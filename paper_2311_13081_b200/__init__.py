@@ -215,6 +215,30 @@ class Env:
                                  _ptr(trace), _ptr(trace_ids), K, _stream(stream)), "l2f_rollout")
         return trace
 
+    def track(self, policy: Policy, cycle_time, n_steps: int, amp_x: float = 1.0, amp_y: float = 0.5,
+              altitude: float = 0.0, clip_pos: float | None = None, clip_vel: float | None = None, stream=None):
+        """l2f_track: batched Lissajous tracking with setpoint shifting (f3).  cycle_time: a
+        float or a [N] tensor of per-env cycle times (s).  Clip bounds default to the training
+        initial-state bounds (init_pos, init_vel).  Returns {rmse, rmse_xy, steps_ok} ([N])."""
+        from .abi import Tracking
+        d = self.device
+        ct = torch.as_tensor(cycle_time, dtype=torch.float32, device=d)
+        if ct.dim() == 0:
+            ct = ct.expand(self.n)
+        ct = ct.contiguous()
+        assert ct.shape == (self.n,)
+        out = {"rmse": torch.empty(self.n, device=d), "rmse_xy": torch.empty(self.n, device=d),
+               "steps_ok": torch.empty(self.n, dtype=torch.int32, device=d)}
+        sp = Tracking()
+        sp.cycle_time = ct.data_ptr()
+        sp.amp_x, sp.amp_y, sp.altitude = float(amp_x), float(amp_y), float(altitude)
+        sp.clip_pos = float(self.cfg.init_pos if clip_pos is None else clip_pos)
+        sp.clip_vel = float(self.cfg.init_vel if clip_vel is None else clip_vel)
+        sp.n_steps = int(n_steps)
+        sp.rmse, sp.rmse_xy, sp.steps_ok = (out[k].data_ptr() for k in ("rmse", "rmse_xy", "steps_ok"))
+        _check(lib().l2f_track(self.h, C.byref(policy.s), C.byref(sp), _stream(stream)), "l2f_track")
+        return out
+
     def recompute_rewards(self, t: int, next_state: torch.Tensor, actions: torch.Tensor, stream=None):
         """Rewards of stored transitions (s' [17][M], a' [4][M]) under the curriculum stage of
         step t (P:231 reward recalculation)."""

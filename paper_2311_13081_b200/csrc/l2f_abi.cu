@@ -437,6 +437,52 @@ l2f_status l2f_rollout(l2f_env* env, const l2f_policy* policy, const float* d_ac
     return L2F_OK;
 }
 
+l2f_status l2f_track(l2f_env* env, const l2f_policy* policy, const l2f_tracking* spec, void* stream)
+{
+    if (!env || !policy || !spec) return fail(L2F_ERR_INVALID_ARGUMENT, "env/policy/spec is NULL");
+    if (!spec->cycle_time || !spec->rmse || !spec->rmse_xy || !spec->steps_ok)
+        return fail(L2F_ERR_INVALID_ARGUMENT, "tracking buffers must not be NULL");
+    if (spec->n_steps < 1 || !(spec->clip_pos > 0) || !(spec->clip_vel > 0))
+        return fail(L2F_ERR_INVALID_ARGUMENT, "tracking needs n_steps >= 1 and positive clip bounds");
+    const int32_t nh = env->cfg.action_history;
+    if (policy->in_dim != 18 + 4 * nh || policy->hidden != 64)
+        return fail(L2F_ERR_INVALID_ARGUMENT, "policy must be (18 + 4 N_H) -> 64 -> 64 -> 4");
+    if (nh % 4 != 0) return fail(L2F_ERR_NOT_SUPPORTED, "tracking needs N_H % 4 == 0");
+    if (!policy->W1 || !policy->b1 || !policy->W2 || !policy->b2 || !policy->W3 || !policy->b3)
+        return fail(L2F_ERR_INVALID_ARGUMENT, "policy pointer is NULL");
+    if (env->t + (uint64_t)spec->n_steps >= (1ull << 31)) return fail(L2F_ERR_INVALID_ARGUMENT, "t overflow");
+    DevParams P;
+    params_for(env, env->t, 1, P);  // stage weights are irrelevant here (no reward output)
+    const uint32_t keep = F_OBS_NOISE | F_NO_ROTOR_DELAY;  // deterministic actor, no resets / DR / disturbance
+    const bool terminate = (P.flags & F_TERMINATION) != 0;
+    P.flags &= keep;
+    // hover rotor speed of the nominal parameters: 4 (c0 + c1 w + c2 w^2) = m g
+    const l2f_params& pp = env->cfg.params;
+    const double c0 = pp.thrust_c[0] - pp.mass * pp.gravity / 4.0, c1 = pp.thrust_c[1], c2 = pp.thrust_c[2];
+    const double wh = c2 != 0.0 ? (-c1 + std::sqrt(c1 * c1 - 4.0 * c2 * c0)) / (2.0 * c2) : -c0 / c1;
+    TrackDev S;
+    S.cycle_time = spec->cycle_time;
+    S.ax = (float)spec->amp_x;
+    S.ay = (float)spec->amp_y;
+    S.z = (float)spec->altitude;
+    S.clip_pos = (float)spec->clip_pos;
+    S.clip_vel = (float)spec->clip_vel;
+    S.hover_rpm = (float)wh;
+    S.hover_a = (float)(2.0 * (wh - pp.rpm_min) / (pp.rpm_max - pp.rpm_min) - 1.0);
+    S.n_steps = spec->n_steps;
+    S.terminate = terminate ? 1 : 0;
+    S.rmse = spec->rmse;
+    S.rmse_xy = spec->rmse_xy;
+    S.steps_ok = spec->steps_ok;
+    PolicyDev W{policy->W1, policy->b1, policy->W2, policy->b2, policy->W3, policy->b3, policy->in_dim,
+                policy->hidden};
+    const cudaError_t e = launch_track_mlp(P, env->B, W, S, (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported) return fail(L2F_ERR_NOT_SUPPORTED, "tracking configuration not supported");
+    const l2f_status st = launched(e, "l2f_track");
+    if (st == L2F_OK) env->t += (uint64_t)spec->n_steps;
+    return st;
+}
+
 l2f_status l2f_episode_stats(l2f_env* env, double* d_out, int32_t reset_accumulators, void* stream)
 {
     if (!env || !d_out) return fail(L2F_ERR_INVALID_ARGUMENT, "env/out is NULL");

@@ -45,4 +45,16 @@ cudaError_t launch_rollout_mlp(const DevParams& P, const DevBufs& B, const Polic
                                const int64_t* trace_ids, int32_t K, cudaStream_t s);
 cudaError_t launch_policy_forward(const PolicyDev& W, const float* obs, float* act, int64_t n, cudaStream_t s);
 
+// Lissajous tracking evaluation (l2f_track): per-env cycle times in, per-env RMSE out.
+struct TrackDev {
+    const float* cycle_time;               // [N]
+    float ax, ay, z, clip_pos, clip_vel;   // reference and setpoint-shift clipping
+    float hover_rpm, hover_a;              // start rotor speed and history fill
+    int32_t n_steps, terminate;            // steps; termination test on the error state (Q31)
+    float *rmse, *rmse_xy;                 // [N]
+    int32_t* steps_ok;                     // [N]
+};
+cudaError_t launch_track_mlp(const DevParams& P, const DevBufs& B, const PolicyDev& W, const TrackDev& S,
+                             cudaStream_t s);
+
 }  // namespace l2f

@@ -660,6 +660,165 @@ __global__ void __launch_bounds__(kThreads, 1)
     teardown_cta();
 }
 
+// -------------------------------------------------------------------------------------------
+// Lissajous tracking evaluation (Table III analogue; Q28-Q31).  Same group /
+// MMA machinery as the rollout; per env: start at p_ref(0) at rest, the actor observes the
+// clipped setpoint shift, the error to p_ref(k dt) is accumulated in FP64 until the
+// first termination on the error state.  No exploration noise, resets, disturbance or DR.
+// -------------------------------------------------------------------------------------------
+__device__ __forceinline__ void lissajous_ref(const TrackDev& S, double dt_over_T, float w, int32_t k, float p[3],
+                                              float v[3])
+{
+    const double ph = (double)k * dt_over_T;  // cycles
+    const float f = (float)(ph - floor(ph));
+    float s1, c1, s2, c2;
+    sincospif(2.0f * f, &s1, &c1);
+    sincospif(4.0f * f, &s2, &c2);
+    p[0] = S.ax * c1;
+    p[1] = S.ay * s2;
+    p[2] = S.z;
+    v[0] = -S.ax * w * s1;
+    v[1] = 2.0f * S.ay * w * c2;
+    v[2] = 0.0f;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    track_mlp_kernel(const DevParams P, const DevBufs B, const PolicyDev W, const TrackDev S, int32_t n_units)
+{
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t sbase = tc::smem_u32(smem);
+    const int NH = P.n_hist;
+    setup_cta(W, sbase, NH, &P);
+    GroupCtx c = make_ctx(sbase);
+    const int64_t N = P.n;
+    const int r = threadIdx.x % kM;
+    const bool obs_noise = (P.flags & F_OBS_NOISE) != 0;
+    const StageW& SW = P.stage[0];
+    for (int u = blockIdx.x * kG + (int)(threadIdx.x / kM); u < n_units; u += gridDim.x * kG) {
+        int64_t i[kE];
+        bool active[kE];
+        uint32_t gid[kE];
+        EnvReg e[kE];
+        double dtT[kE], se[kE], sexy[kE];
+        float w[kE];
+        int32_t ok[kE];
+        bool alive[kE];
+#pragma unroll
+        for (int k = 0; k < kE; ++k) {
+            i[k] = ((int64_t)u * kE + k) * kM + r;
+            active[k] = i[k] < N;
+            gid[k] = P.id_offset + (uint32_t)i[k];
+            const float Tc = active[k] ? S.cycle_time[i[k]] : 1.0f;
+            dtT[k] = (double)P.dt / (double)Tc;
+            w[k] = 6.28318530717958648f / Tc;
+            // start: p_ref(0) = (A_x, 0, z) at rest, level, rotors at hover (Q30)
+#pragma unroll
+            for (int q = 0; q < kStateDim; ++q) e[k].s[q] = 0.0f;
+            e[k].s[0] = S.ax;
+            e[k].s[2] = S.z;
+            e[k].s[3] = 1.0f;
+#pragma unroll
+            for (int q = 13; q < 17; ++q) e[k].s[q] = S.hover_rpm;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) e[k].dist[q] = 0.0f;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) e[k].dr[q] = 1.0f;
+            e[k].ep_step = 0;
+            e[k].ep_return = 0.0f;
+            const uint32_t hh = tc::pack_h2(S.hover_a, S.hover_a);
+            for (int j = 0; j < NH; ++j) tc::sts64(hist_addr(c, k, j), hh, hh);
+            se[k] = sexy[k] = 0.0;
+            ok[k] = 0;
+            alive[k] = true;
+            stash_obs_noise(P, c, k, gid[k], P.t0, 3);
+        }
+        uint32_t rot = NH > 0 ? (P.t0 + (uint32_t)NH - 1u) % (uint32_t)NH : 0u;
+        int wpos = NH > 0 ? (int)(((uint32_t)NH - P.t0 % (uint32_t)NH) % (uint32_t)NH) : 0;
+        for (int32_t ks = 0; ks < S.n_steps; ++ks) {
+            const uint32_t t = P.t0 + (uint32_t)ks;
+            tc::tmem_wait_st();
+#pragma unroll
+            for (int k = 0; k < kE; ++k) {
+                float ob[kObsCore], z[20], pr[3], vr[3];
+                if (obs_noise) load_obs_noise(c, k, z);
+                observe_core_z(P, e[k].s, z, ob);
+                lissajous_ref(S, dtT[k], w[k], ks, pr, vr);
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {  // setpoint shift with clipping (Q29)
+                    ob[j] = fminf(fmaxf(ob[j] - pr[j], -S.clip_pos), S.clip_pos);
+                    ob[12 + j] = fminf(fmaxf(ob[12 + j] - vr[j], -S.clip_vel), S.clip_vel);
+                }
+                write_obs_row(c, k, ob);
+            }
+            float a[kE][4];
+            mlp_group(c, sbase, NH, rot, a, [&](int l) {
+#pragma unroll
+                for (int k = 0; k < kE; ++k) stash_obs_noise(P, c, k, gid[k], t + 1, l - 1);
+            });
+            if (NH > 0 && ++rot == (uint32_t)NH) rot = 0;
+#pragma unroll
+            for (int k = 0; k < kE; ++k) {
+                const float za[4] = {0.f, 0.f, 0.f, 0.f};
+                Trans o;
+                transition<false>(P, SW, e[k], gid[k], t, a[k], za, o);
+                if (NH > 0)
+                    tc::sts64(hist_addr(c, k, wpos), tc::pack_h2(o.a[0], o.a[1]), tc::pack_h2(o.a[2], o.a[3]));
+                float pr[3], vr[3];
+                lissajous_ref(S, dtT[k], w[k], ks + 1, pr, vr);
+                const float* s1 = e[k].s;
+                const float ex = s1[0] - pr[0], ey = s1[1] - pr[1], ez = s1[2] - pr[2];
+                const float dvx = s1[7] - vr[0], dvy = s1[8] - vr[1], dvz = s1[9] - vr[2];
+                const float ww = s1[10] * s1[10] + s1[11] * s1[11] + s1[12] * s1[12];
+                const float einf = fmaxf(fabsf(ex), fmaxf(fabsf(ey), fabsf(ez)));
+                const bool out = (einf > P.term_pos) | (dvx * dvx + dvy * dvy + dvz * dvz > P.term_vel2) |
+                                 (ww > P.term_angvel2);
+                const bool term = ((o.flags & D_DIV) != 0) | (S.terminate != 0 && out);
+                alive[k] = alive[k] && !term;
+                if (alive[k]) {
+                    const double dx = ex, dy = ey, dz = ez;
+                    sexy[k] += dx * dx + dy * dy;
+                    se[k] += dx * dx + dy * dy + dz * dz;
+                    ok[k] = ks + 1;
+                }
+            }
+            if (NH > 0 && --wpos < 0) wpos = NH - 1;
+        }
+#pragma unroll
+        for (int k = 0; k < kE; ++k) {
+            if (!active[k]) continue;
+            const int64_t ik = i[k];
+            S.rmse[ik] = ok[k] > 0 ? (float)sqrt(se[k] / ok[k]) : 0.0f;
+            S.rmse_xy[ik] = ok[k] > 0 ? (float)sqrt(sexy[k] / ok[k]) : 0.0f;
+            S.steps_ok[ik] = ok[k];
+            // the env is left in the final tracking state (history ring complete, as after a rollout)
+#pragma unroll
+            for (int q = 0; q < kStateDim; ++q) B.state[q * N + ik] = e[k].s[q];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) B.dist[q * N + ik] = 0.0f;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) B.dr[q * N + ik] = 1.0f;
+            B.ep_step[ik] = ok[k];
+            B.ep_return[ik] = 0.0f;
+            if (NH > 0) {
+                const int32_t t_end = (int32_t)(P.t0 + (uint32_t)S.n_steps);
+                B.hist_t0[ik] = t_end - NH;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) B.hist_fill[(int64_t)q * N + ik] = S.hover_a;
+            }
+            for (int sl = 0; sl < NH; ++sl) {
+                uint32_t h01, h23;
+                tc::lds64(hist_addr(c, k, (NH - sl) % NH), h01, h23);
+                const __half2 x = *reinterpret_cast<__half2*>(&h01), y = *reinterpret_cast<__half2*>(&h23);
+                B.hist[((int64_t)sl * 4 + 0) * N + ik] = __low2float(x);
+                B.hist[((int64_t)sl * 4 + 1) * N + ik] = __high2float(x);
+                B.hist[((int64_t)sl * 4 + 2) * N + ik] = __low2float(y);
+                B.hist[((int64_t)sl * 4 + 3) * N + ik] = __high2float(y);
+            }
+        }
+    }
+    teardown_cta();
+}
+
 int sm_count()
 {
     static int n = 0;
@@ -708,6 +867,20 @@ cudaError_t launch_rollout_mlp(const DevParams& P, const DevBufs& B, const Polic
         rollout_mlp_kernel<true><<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, n_units);
     else
         rollout_mlp_kernel<false><<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, n_units);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_track_mlp(const DevParams& P, const DevBufs& B, const PolicyDev& W, const TrackDev& S,
+                             cudaStream_t s)
+{
+    if (P.n_hist % 4 != 0 || W.hidden != kHid || W.in_dim != 18 + 4 * P.n_hist) return cudaErrorNotSupported;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(track_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    track_mlp_kernel<<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, S, (int32_t)units_for(P.n));
     return cudaGetLastError();
 }
 
