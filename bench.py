@@ -453,6 +453,26 @@ def secondary(pkg, inputs, torch, dev, pk, f_clk):
                                     "workload": "2^21 envs x 200 steps, C5 features, Philox random actions"}
     del env
     torch.cuda.empty_cache()
+    # f3: batched Lissajous tracking (l2f_track), 2^20 envs sweeping the Table III cycle times
+    n, steps = 1 << 20, 550
+    cfg = inputs.config_c4()
+    env = pkg.Env(cfg, n, device=dev)
+    pol = pkg.Policy(inputs.policy_weights(146, 64, seed=7, out_bias=inputs.hover_policy_bias()), device=dev)
+    ct = torch.tensor([15.0, 5.5, 3.5], device=dev).repeat(n // 3 + 1)[:n].contiguous()
+    env.track(pol, ct, 20)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    r = env.track(pol, ct, steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ok = (r["steps_ok"] == steps)
+    out["lissajous_tracking"] = {"value": n * steps / (ms / 1e3), "unit": "env-steps/s", "ms": ms,
+                                 "workload": "2^20 envs x 550 steps (5.5 s), cycle times 15/5.5/3.5 s, random "
+                                             "hover-biased C4 actor (untrained: RMSE values are not Table III's)",
+                                 "success_fraction": float(ok.float().mean())}
+    del env, pol, ct, r
+    torch.cuda.empty_cache()
     return out
 
 
