@@ -219,6 +219,7 @@ DevParams make_base(const l2f_config& c)
         P.rx[i] = (float)p.rotor_pos[i][0];
         P.ry[i] = (float)p.rotor_pos[i][1];
         P.spin[i] = (float)p.spin_dir[i];
+        P.rxy[i] = make_float2(P.ry[i], -P.rx[i]);
     }
     P.init_pos = (float)c.init_pos;
     P.init_angle = (float)c.init_angle;

@@ -54,6 +54,7 @@ struct DevParams {
     // nominal parameters; DR factors scale mass, J, thrust coefficients (Q19)
     float mass, J[3], c[3], ctau, inv_tm, rpm_min, rpm_max, gravity, rpm_half_span, inv_rpm_span2;
     float rx[4], ry[4], spin[4];
+    float2 rxy[4];                 // (ry_i, -rx_i): roll/pitch torque arms per rotor, packed
     float inv_mass, iJ[3], dJ[3];  // nominal 1/m, 1/J_ii, (Jz-Jy, Jx-Jz, Jy-Jx): DR-free fast path
     // reset distribution (Q17-Q19)
     float init_pos, init_angle, init_vel, init_angvel, init_rpm_lo, init_rpm_hi;
@@ -271,19 +272,24 @@ __device__ __forceinline__ void make_phys(const DevParams& P, const EnvReg& e, P
 // y = (qw, qx, qy, qz, wx, wy, wz).
 constexpr int kY = 7;
 __device__ __forceinline__ void deriv(const DevParams& P, const Phys& ph, const float* d, const float* y,
-                                      const float m[4], float* dy, float av[3])
+                                      float2 mA, float2 mB, float* dy, float av[3])
 {
-    float f[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) f[i] = fmaf(fmaf(ph.c2, m[i], ph.c1), m[i], ph.c0);
-    const float T = (f[0] + f[1]) + (f[2] + f[3]);
-    float tx = d[3], ty = d[4], tz = 0.0f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        tx = fmaf(P.ry[i], f[i], tx);
-        ty = fmaf(-P.rx[i], f[i], ty);
-        tz = fmaf(P.spin[i], f[i], tz);
-    }
+    // rotor thrusts packed as (f0, f2) and (f1, f3) from the rotor speeds (m0, m2), (m1, m3)
+    const float2 c2 = make_float2(ph.c2, ph.c2), c1 = make_float2(ph.c1, ph.c1), c0 = make_float2(ph.c0, ph.c0);
+    const float2 fA = __ffma2_rn(__ffma2_rn(c2, mA, c1), mA, c0);
+    const float2 fB = __ffma2_rn(__ffma2_rn(c2, mB, c1), mB, c0);
+    const float2 sp = __fadd2_rn(fA, fB);  // (f0 + f1, f2 + f3)
+    const float T = sp.x + sp.y;
+    // (tau_x, tau_y) = (d3, d4) + sum_i (ry_i, -rx_i) f_i, rotor order 0..3 as in the scalar sum
+    float2 txy = make_float2(d[3], d[4]);
+    txy = __ffma2_rn(P.rxy[0], make_float2(fA.x, fA.x), txy);
+    txy = __ffma2_rn(P.rxy[1], make_float2(fB.x, fB.x), txy);
+    txy = __ffma2_rn(P.rxy[2], make_float2(fA.y, fA.y), txy);
+    txy = __ffma2_rn(P.rxy[3], make_float2(fB.y, fB.y), txy);
+    float tz = fmaf(P.spin[0], fA.x, 0.0f);
+    tz = fmaf(P.spin[1], fB.x, tz);
+    tz = fmaf(P.spin[2], fA.y, tz);
+    tz = fmaf(P.spin[3], fB.y, tz);
     tz = fmaf(P.ctau, tz, d[5]);
     const float qw = y[0], qx = y[1], qy = y[2], qz = y[3];
     const float wx = y[4], wy = y[5], wz = y[6];
@@ -296,16 +302,52 @@ __device__ __forceinline__ void deriv(const DevParams& P, const Phys& ph, const 
     const float r02 = 2.0f * (qx * qz + qw * qy);
     const float r12 = 2.0f * (qy * qz - qw * qx);
     const float r22 = 1.0f - 2.0f * (qx * qx + qy * qy);
-    av[0] = fmaf(r02, T, d[0]) * ph.inv_m;
-    av[1] = fmaf(r12, T, d[1]) * ph.inv_m;
+    const float2 a01 = __fmul2_rn(__ffma2_rn(make_float2(r02, r12), make_float2(T, T), make_float2(d[0], d[1])),
+                                  make_float2(ph.inv_m, ph.inv_m));
+    av[0] = a01.x;
+    av[1] = a01.y;
     av[2] = fmaf(fmaf(r22, T, d[2]), ph.inv_m, -P.gravity);
     // Euler: J w' = tau - w x (J w)
     const float cx = ph.dJzy * (wy * wz);
     const float cy = ph.dJxz * (wz * wx);
     const float cz = ph.dJyx * (wx * wy);
-    dy[4] = (tx - cx) * ph.iJx;
-    dy[5] = (ty - cy) * ph.iJy;
+    dy[4] = (txy.x - cx) * ph.iJx;
+    dy[5] = (txy.y - cy) * ph.iJy;
     dy[6] = (tz - cz) * ph.iJz;
+}
+
+// SoA walkers: rows c = 0..C-1 of column i of a [C][N] array, visited in order with one
+// 32-bit-stride IMAD.WIDE per access (the indexed form c * N + i with a 64-bit N costs two to
+// three integer instructions per access).  N < 2^32.
+template <int C, class T>
+__device__ __forceinline__ void soa_load(const T* base, int64_t i, uint32_t n, T* out)
+{
+    const T* q = base + i;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        out[c] = *q;
+        q += n;
+    }
+}
+template <int C, class T>
+__device__ __forceinline__ void soa_load_ro(const T* __restrict__ base, int64_t i, uint32_t n, T* out)
+{
+    const T* q = base + i;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        out[c] = __ldg(q);
+        q += n;
+    }
+}
+template <int C, class T>
+__device__ __forceinline__ void soa_store(T* base, int64_t i, uint32_t n, const T* v)
+{
+    T* q = base + i;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        *q = v[c];
+        q += n;
+    }
 }
 
 // Any NaN/Inf component makes the sum non-finite (a finite overflow to inf also counts:
@@ -346,19 +388,18 @@ __device__ __forceinline__ bool rk4_step(const DevParams& P, const Phys& ph, con
                                          float* s)
 {
     float y0[kY] = {s[3], s[4], s[5], s[6], s[10], s[11], s[12]};
-    float dm[4], m[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) dm[i] = s[13 + i] - u[i];
+    // rotors packed as (0, 2) and (1, 3): d = w_m0 - u, stage speeds u + d beta_j
+    const float2 uA = make_float2(u[0], u[2]), uB = make_float2(u[1], u[3]);
+    const float2 dA = make_float2(s[13] - u[0], s[15] - u[2]), dB = make_float2(s[14] - u[1], s[16] - u[3]);
     float acc[kY], tmp[kY], k[kY], a[3], asum[3], vacc[3];
-    deriv(P, ph, d, y0, s + 13, k, a);
+    deriv(P, ph, d, y0, make_float2(s[13], s[15]), make_float2(s[14], s[16]), k, a);
 #pragma unroll
     for (int i = 0; i < 3; ++i) asum[i] = vacc[i] = a[i];
 #pragma unroll
     for (int i = 0; i < kY; ++i) acc[i] = k[i];
     pair_fma(k, P.half_dt, y0, tmp);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) m[i] = fmaf(dm[i], P.m_beta2, u[i]);
-    deriv(P, ph, d, tmp, m, k, a);
+    float2 b = make_float2(P.m_beta2, P.m_beta2);
+    deriv(P, ph, d, tmp, __ffma2_rn(dA, b, uA), __ffma2_rn(dB, b, uB), k, a);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         asum[i] += a[i];
@@ -366,9 +407,8 @@ __device__ __forceinline__ bool rk4_step(const DevParams& P, const Phys& ph, con
     }
     pair_fma(k, 2.0f, acc, acc);
     pair_fma(k, P.half_dt, y0, tmp);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) m[i] = fmaf(dm[i], P.m_beta3, u[i]);
-    deriv(P, ph, d, tmp, m, k, a);
+    b = make_float2(P.m_beta3, P.m_beta3);
+    deriv(P, ph, d, tmp, __ffma2_rn(dA, b, uA), __ffma2_rn(dB, b, uB), k, a);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         asum[i] += a[i];
@@ -376,9 +416,8 @@ __device__ __forceinline__ bool rk4_step(const DevParams& P, const Phys& ph, con
     }
     pair_fma(k, 2.0f, acc, acc);
     pair_fma(k, P.dt, y0, tmp);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) m[i] = fmaf(dm[i], P.m_beta4, u[i]);
-    deriv(P, ph, d, tmp, m, k, a);
+    b = make_float2(P.m_beta4, P.m_beta4);
+    deriv(P, ph, d, tmp, __ffma2_rn(dA, b, uA), __ffma2_rn(dB, b, uB), k, a);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         s[i] = fmaf(P.dt2_6, asum[i], fmaf(P.dt, s[7 + i], s[i]));  // position (pre-step v)
@@ -395,6 +434,12 @@ __device__ __forceinline__ bool rk4_step(const DevParams& P, const Phys& ph, con
         }
         y0[kY - 1] = fmaf(P.dt_6, acc[kY - 1] + k[kY - 1], y0[kY - 1]);
     }
+    const float2 R = make_float2(P.m_R, P.m_R);
+    const float2 wA = __ffma2_rn(dA, R, uA), wB = __ffma2_rn(dB, R, uB);
+    s[13] = wA.x;
+    s[14] = wB.x;
+    s[15] = wA.y;
+    s[16] = wB.y;
     const float n2 = (y0[0] * y0[0] + y0[1] * y0[1]) + (y0[2] * y0[2] + y0[3] * y0[3]);
     const float inv = rsqrtf(n2);
 #pragma unroll
@@ -402,7 +447,7 @@ __device__ __forceinline__ bool rk4_step(const DevParams& P, const Phys& ph, con
 #pragma unroll
     for (int i = 0; i < 3; ++i) s[10 + i] = y0[4 + i];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) s[13 + i] = fminf(fmaxf(fmaf(dm[i], P.m_R, u[i]), P.rpm_min), P.rpm_max);
+    for (int i = 13; i < 17; ++i) s[i] = fminf(fmaxf(s[i], P.rpm_min), P.rpm_max);
     return !state_finite(s);
 }
 

@@ -19,14 +19,11 @@ namespace l2f {
 template <bool kDR>
 __device__ __forceinline__ void load_env(const DevParams& P, const DevBufs& B, int64_t i, EnvReg& e)
 {
-    const int64_t N = P.n;
-#pragma unroll
-    for (int c = 0; c < kStateDim; ++c) e.s[c] = B.state[c * N + i];
-#pragma unroll
-    for (int c = 0; c < 6; ++c) e.dist[c] = B.dist[c * N + i];
+    const uint32_t n = (uint32_t)P.n;
+    soa_load<kStateDim>(B.state, i, n, e.s);
+    soa_load<6>(B.dist, i, n, e.dist);
     if (kDR) {
-#pragma unroll
-        for (int c = 0; c < 5; ++c) e.dr[c] = B.dr[c * N + i];
+        soa_load<5>(B.dr, i, n, e.dr);
     } else {
 #pragma unroll
         for (int c = 0; c < 5; ++c) e.dr[c] = 1.0f;
@@ -51,9 +48,7 @@ __device__ __forceinline__ void dummy_env(EnvReg& e)
 
 __device__ __forceinline__ void store_state(const DevParams& P, const DevBufs& B, int64_t i, const EnvReg& e)
 {
-    const int64_t N = P.n;
-#pragma unroll
-    for (int c = 0; c < kStateDim; ++c) B.state[c * N + i] = e.s[c];
+    soa_store<kStateDim>(B.state, i, (uint32_t)P.n, e.s);
     B.ep_step[i] = e.ep_step;
     B.ep_return[i] = e.ep_return;
 }
@@ -62,13 +57,9 @@ __device__ __forceinline__ void store_state(const DevParams& P, const DevBufs& B
 __device__ __forceinline__ void store_episode_consts(const DevParams& P, const DevBufs& B, int64_t i,
                                                      const EnvReg& e)
 {
-    const int64_t N = P.n;
-#pragma unroll
-    for (int c = 0; c < 6; ++c) B.dist[c * N + i] = e.dist[c];
-    if (P.flags & F_DOMAIN_RAND) {
-#pragma unroll
-        for (int c = 0; c < 5; ++c) B.dr[c * N + i] = e.dr[c];
-    }
+    const uint32_t n = (uint32_t)P.n;
+    soa_store<6>(B.dist, i, n, e.dist);
+    if (P.flags & F_DOMAIN_RAND) soa_store<5>(B.dr, i, n, e.dr);
 }
 
 // A new episode starting at step t0: O(1) bytes (marker + fill value), the ring itself is
@@ -76,10 +67,8 @@ __device__ __forceinline__ void store_episode_consts(const DevParams& P, const D
 __device__ __forceinline__ void hist_restart(const DevParams& P, const DevBufs& B, int64_t i, uint32_t t0,
                                              const float h[4])
 {
-    const int64_t N = P.n;
     B.hist_t0[i] = (int32_t)t0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) B.hist_fill[(int64_t)c * N + i] = h[c];
+    soa_store<4>(B.hist_fill, i, (uint32_t)P.n, h);
 }
 
 // Dense actor observation row [18 + 4 N_H]: obs_core then H most-recent-first at
@@ -140,8 +129,7 @@ __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const D
     float a[4] = {0.f, 0.f, 0.f, 0.f};
     if (active) {
         load_env<kDR>(P, B, i, e);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) a[c] = __ldg(act + c * N + i);
+        soa_load_ro<4>(act, i, (uint32_t)N, a);
     } else {
         dummy_env(e);
     }
@@ -151,8 +139,7 @@ __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const D
     transition<kDR>(P, stage_of(P, t), e, gid, t, a, za, o);
     uint32_t fl = o.flags;
     if (active && O.final_state) {
-#pragma unroll
-        for (int c = 0; c < kStateDim; ++c) O.final_state[c * N + i] = e.s[c];
+        soa_store<kStateDim>(O.final_state, i, (uint32_t)N, e.s);
     }
     const bool ended = active && (fl & (D_TERM | D_TRUNC));
     if (ended) stat_episode(st, o);
@@ -168,8 +155,7 @@ __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const D
     if (active) {
         if (P.n_hist > 0) {
             const int slot = P.hist_slot0;  // t0 mod N_H (written for every env: deterministic ring)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) B.hist[((int64_t)slot * 4 + c) * N + i] = o.a[c];
+            soa_store<4>(B.hist + (int64_t)slot * 4 * N, i, (uint32_t)N, o.a);
             if (did_reset) hist_restart(P, B, i, t + 1, hf);
         }
         store_state(P, B, i, e);
@@ -178,16 +164,14 @@ __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const D
             float ob[kObsCore];
             observe_core(P, e.s, gid, t + 1, ob);
             if (O.obs_core) {
-#pragma unroll
-                for (int j = 0; j < kObsCore; ++j) O.obs_core[j * N + i] = ob[j];
+                soa_store<kObsCore>(O.obs_core, i, (uint32_t)N, ob);
             }
             if (O.obs_dense) write_dense(P, B, i, ob, t + 1, O.obs_dense + i * (kObsCore + 4 * P.n_hist));
         }
         if (O.obs_critic) {
             float oc[kObsCritic];
             observe_critic(e.s, e.dist, oc);
-#pragma unroll
-            for (int j = 0; j < kObsCritic; ++j) O.obs_critic[j * N + i] = oc[j];
+            soa_store<kObsCritic>(O.obs_critic, i, (uint32_t)N, oc);
         }
         if (O.reward) O.reward[i] = o.reward;
         if (O.flags) O.flags[i] = (uint8_t)fl;
