@@ -503,8 +503,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             Trans o[kE];
 #pragma unroll
             for (int k = 0; k < kE; ++k) {
-                float* tr = (tslot[k] >= 0) ? trace + ((int64_t)ks * K + tslot[k]) * kTraceFields : nullptr;
-                if (tr) {
+                if (tslot[k] >= 0) {  // (traced envs only: the address is not formed otherwise)
+                    float* tr = trace + ((int64_t)ks * K + tslot[k]) * kTraceFields;
 #pragma unroll
                     for (int q = 0; q < kStateDim; ++q) tr[q] = e[k].s[q];
 #pragma unroll
@@ -550,8 +550,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if (q < NH / 2) tc::sts128(a1_row(c, k) + (4 + q) * kChunkA, h01, h23, h01, h23);
                     }
                 }
-                float* tr = (tslot[k] >= 0) ? trace + ((int64_t)ks * K + tslot[k]) * kTraceFields : nullptr;
-                if (tr) {
+                if (tslot[k] >= 0) {
+                    float* tr = trace + ((int64_t)ks * K + tslot[k]) * kTraceFields;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) tr[21 + q] = o[k].a[q];
                     tr[25] = o[k].reward;
