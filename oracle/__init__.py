@@ -84,6 +84,11 @@ class Policy(C.Structure):
 ENV_DTYPE = np.dtype([("s", "<f8", (17,)), ("dist", "<f8", (6,)), ("dr", "<f8", (5,)),
                       ("hist", "<f8", (32, 4)), ("ep_step", "<i8"), ("ep_return", "<f8")])
 
+class TD3Hyper(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("gamma", "tau", "sigma_t", "clip_t", "lr_actor", "lr_critic", "beta1",
+                                          "beta2", "eps")]
+
+
 _lib = None
 
 
@@ -131,6 +136,10 @@ def lib():
         L.or_track.argtypes = [C.POINTER(Config), C.c_void_p, C.c_uint64, C.c_uint64, C.c_double, C.c_double,
                                C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32, dp, dp,
                                C.POINTER(C.c_int32), C.c_void_p]
+        L.or_net_size.restype = C.c_int64
+        L.or_net_size.argtypes = [C.c_int32, C.c_int32, C.c_int32]
+        L.or_td3_update.argtypes = [dp, C.c_int32, C.c_int32, dp, dp, dp, dp, dp, dp, dp, dp,
+                                    C.POINTER(TD3Hyper), C.c_int64, C.c_int64, C.c_int32, dp, C.c_void_p]
         for f in ("or_sizeof_config", "or_sizeof_env", "or_sizeof_step_out"):
             getattr(L, f).restype = C.c_int64
         assert L.or_sizeof_config() == C.sizeof(Config), "oracle Config mirror out of sync"
@@ -429,3 +438,36 @@ def track(cfg: dict, policy: PolicyHandle | None, env_id: int, t0: int, Tc: floa
                    float(Tc), float(ax), float(ay), float(z), float(cp), float(cv), int(n_steps),
                    C.byref(r), C.byref(rxy), C.byref(ok), tr.ctypes.data if tr is not None else None)
     return r.value, rxy.value, ok.value, tr
+
+
+# ---- TD3 update (f4) ---------------------------------------------------------------------
+TD3_DEFAULTS = {"gamma": 0.99, "tau": 0.005, "sigma_t": 0.2, "clip_t": 0.5, "lr_actor": 3e-4, "lr_critic": 3e-4,
+                "beta1": 0.9, "beta2": 0.999, "eps": 1e-8}  # SPEC S:436 (the cited algorithm's defaults)
+
+
+def net_size(n_in: int, hid: int, n_out: int) -> int:
+    return int(lib().or_net_size(n_in, hid, n_out))
+
+
+def td3_block_size(in_dim: int) -> int:
+    na, nc = net_size(in_dim, 64, 4), net_size(32, 64, 1)
+    return 2 * na + 4 * nc + 2 * na + 4 * nc
+
+
+def td3_update(P: np.ndarray, in_dim: int, batch: dict, hyper: dict | None = None, t_critic: int = 1,
+               t_actor: int = 1, update_actor: bool = True, want_grads: bool = False):
+    """One TD3 update of one agent in place on the FP64 parameter block P (Q32-Q35).
+    batch: o_a [B][I], o_c [B][28], a [B][4], r [B], o_a2, o_c2, done [B], eps [B][4].
+    Returns (losses[3], grads or None)."""
+    assert P.dtype == np.float64 and P.flags.c_contiguous and P.size == td3_block_size(in_dim)
+    h = TD3Hyper(**{**TD3_DEFAULTS, **(hyper or {})})
+    B = len(batch["r"])
+    arr = {k: _d(batch[k]) for k in ("o_a", "o_c", "a", "r", "o_a2", "o_c2", "done", "eps")}
+    losses = np.zeros(3)
+    na, nc = net_size(in_dim, 64, 4), net_size(32, 64, 1)
+    g = np.zeros(2 * nc + na) if want_grads else None
+    lib().or_td3_update(_dp(P), int(in_dim), int(B), *(_dp(arr[k]) for k in
+                                                       ("o_a", "o_c", "a", "r", "o_a2", "o_c2", "done", "eps")),
+                        C.byref(h), int(t_critic), int(t_actor), int(bool(update_actor)), _dp(losses),
+                        g.ctypes.data if g is not None else None)
+    return losses, g

@@ -851,6 +851,203 @@ void or_track(const or_config* cfg_in, const or_policy* pol, uint64_t env_id, ui
     *steps_ok = ok;
 }
 
+/* ------------------------------------------------------------------------------------ */
+/* TD3 update ("we use TD3" citing Fujimoto et al. 2018; */
+/* DESIGN.md Q32-Q35).  Dense nets with a flat FP64 parameter layout per net:              */
+/*   W1[hid][in], b1[hid], W2[hid][hid], b2[hid], W3[out][hid], b3[out];                   */
+/* actor in_dim -> 64 -> 64 -> 4 (ReLU, ReLU, tanh); critics 32 -> 64 -> 64 -> 1 (ReLU,    */
+/* ReLU, linear) on concat(o_c, a) with o_c the 28-D privileged observation.               */
+/* ------------------------------------------------------------------------------------ */
+int64_t or_net_size(int32_t in, int32_t hid, int32_t out)
+{
+    return (int64_t)hid * in + hid + (int64_t)hid * hid + hid + (int64_t)out * hid + out;
+}
+
+typedef struct {
+    int32_t in, hid, out;
+    double *W1, *b1, *W2, *b2, *W3, *b3;
+} or_net;
+
+static or_net net_view(double* p, int32_t in, int32_t hid, int32_t out)
+{
+    or_net n;
+    n.in = in; n.hid = hid; n.out = out;
+    n.W1 = p; p += (size_t)hid * in;
+    n.b1 = p; p += hid;
+    n.W2 = p; p += (size_t)hid * hid;
+    n.b2 = p; p += hid;
+    n.W3 = p; p += (size_t)out * hid;
+    n.b3 = p;
+    return n;
+}
+
+/* y = f3(W3 relu(W2 relu(W1 x + b1) + b2) + b3), f3 = tanh or identity; caches h1, h2 */
+static void net_forward(const or_net* n, const double* x, double* h1, double* h2, double* y, int tanh_out)
+{
+    for (int j = 0; j < n->hid; ++j) {
+        double acc = n->b1[j];
+        for (int i = 0; i < n->in; ++i) acc += n->W1[(size_t)j * n->in + i] * x[i];
+        h1[j] = acc > 0.0 ? acc : 0.0;
+    }
+    for (int j = 0; j < n->hid; ++j) {
+        double acc = n->b2[j];
+        for (int i = 0; i < n->hid; ++i) acc += n->W2[(size_t)j * n->hid + i] * h1[i];
+        h2[j] = acc > 0.0 ? acc : 0.0;
+    }
+    for (int o = 0; o < n->out; ++o) {
+        double acc = n->b3[o];
+        for (int i = 0; i < n->hid; ++i) acc += n->W3[(size_t)o * n->hid + i] * h2[i];
+        y[o] = tanh_out ? tanh(acc) : acc;
+    }
+}
+
+/* Backpropagation of dL/dy through the net: accumulates dL/dtheta into g (same layout) and
+ * writes dL/dx (if dx != NULL).  ReLU'(0) = 0. */
+static void net_backward(const or_net* n, const double* x, const double* h1, const double* h2, const double* y,
+                         int tanh_out, const double* dy, or_net* g, double* dx)
+{
+    double d3[8], d2[256], d1[256];
+    for (int o = 0; o < n->out; ++o) d3[o] = tanh_out ? dy[o] * (1.0 - y[o] * y[o]) : dy[o];
+    for (int o = 0; o < n->out; ++o) {
+        g->b3[o] += d3[o];
+        for (int i = 0; i < n->hid; ++i) g->W3[(size_t)o * n->hid + i] += d3[o] * h2[i];
+    }
+    for (int j = 0; j < n->hid; ++j) {
+        double acc = 0.0;
+        for (int o = 0; o < n->out; ++o) acc += n->W3[(size_t)o * n->hid + j] * d3[o];
+        d2[j] = h2[j] > 0.0 ? acc : 0.0;
+    }
+    for (int j = 0; j < n->hid; ++j) {
+        g->b2[j] += d2[j];
+        for (int i = 0; i < n->hid; ++i) g->W2[(size_t)j * n->hid + i] += d2[j] * h1[i];
+    }
+    for (int i = 0; i < n->hid; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j < n->hid; ++j) acc += n->W2[(size_t)j * n->hid + i] * d2[j];
+        d1[i] = h1[i] > 0.0 ? acc : 0.0;
+    }
+    for (int j = 0; j < n->hid; ++j) {
+        g->b1[j] += d1[j];
+        for (int i = 0; i < n->in; ++i) g->W1[(size_t)j * n->in + i] += d1[j] * x[i];
+    }
+    if (dx)
+        for (int i = 0; i < n->in; ++i) {
+            double acc = 0.0;
+            for (int j = 0; j < n->hid; ++j) acc += n->W1[(size_t)j * n->in + i] * d1[j];
+            dx[i] = acc;
+        }
+}
+
+typedef struct {
+    double gamma, tau, sigma_t, clip_t, lr_actor, lr_critic, beta1, beta2, eps;
+} or_td3_hyper;
+
+/* Adam (Kingma & Ba 2015) step t >= 1 on n parameters. */
+static void adam(double* th, double* m, double* v, const double* g, int64_t n, int64_t t, double lr,
+                 const or_td3_hyper* h)
+{
+    double c1 = 1.0 - pow(h->beta1, (double)t), c2 = 1.0 - pow(h->beta2, (double)t);
+    for (int64_t k = 0; k < n; ++k) {
+        m[k] = h->beta1 * m[k] + (1.0 - h->beta1) * g[k];
+        v[k] = h->beta2 * v[k] + (1.0 - h->beta2) * g[k] * g[k];
+        th[k] -= lr * (m[k] / c1) / (sqrt(v[k] / c2) + h->eps);
+    }
+}
+
+/* One TD3 update of one agent (Q32-Q35).  P = [actor, actor', Q1, Q2, Q1', Q2', m_actor,
+ * v_actor, m_Q1, v_Q1, m_Q2, v_Q2] (flat FP64).  Batch arrays are [B][...]; eps [B][4] are
+ * the standard normals of the target-policy smoothing noise (drawn by the caller).  t_critic
+ * / t_actor: the Adam step numbers of this update (>= 1).  losses[3] = critic 1, critic 2,
+ * actor (0 when the actor is not updated).  grads (optional, for tests): the raw gradients
+ * [Q1, Q2, actor] before Adam. */
+void or_td3_update(double* P, int32_t in_dim, int32_t B, const double* o_a, const double* o_c, const double* a,
+                   const double* r, const double* o_a2, const double* o_c2, const double* done,
+                   const double* eps, const or_td3_hyper* h, int64_t t_critic, int64_t t_actor,
+                   int32_t update_actor, double* losses, double* grads)
+{
+    const int32_t H = 64, CI = 32;
+    const int64_t na = or_net_size(in_dim, H, 4), nc = or_net_size(CI, H, 1);
+    double* pa = P;
+    double* pa_t = pa + na;
+    double* pc[2] = {pa_t + na, pa_t + na + nc};
+    double* pc_t[2] = {pc[1] + nc, pc[1] + 2 * nc};
+    double* m_a = pc_t[1] + nc;
+    double* v_a = m_a + na;
+    double* m_c[2] = {v_a + na, v_a + na + 2 * nc};
+    double* v_c[2] = {v_a + na + nc, v_a + na + 3 * nc};
+    or_net actor = net_view(pa, in_dim, H, 4), actor_t = net_view(pa_t, in_dim, H, 4);
+    or_net Q[2] = {net_view(pc[0], CI, H, 1), net_view(pc[1], CI, H, 1)};
+    or_net Qt[2] = {net_view(pc_t[0], CI, H, 1), net_view(pc_t[1], CI, H, 1)};
+    double h1[64], h2[64], out[4], x[CI];
+    double* y = (double*)malloc(sizeof(double) * (size_t)B);
+    /* 1. target: smoothed target action, clipped double-Q */
+    for (int32_t s = 0; s < B; ++s) {
+        double at[4];
+        net_forward(&actor_t, o_a2 + (size_t)s * in_dim, h1, h2, at, 1);
+        for (int k = 0; k < 4; ++k) {
+            double nz = h->sigma_t * eps[(size_t)s * 4 + k];
+            nz = fmin(fmax(nz, -h->clip_t), h->clip_t);
+            at[k] = fmin(fmax(at[k] + nz, -1.0), 1.0);
+        }
+        for (int k = 0; k < 28; ++k) x[k] = o_c2[(size_t)s * 28 + k];
+        for (int k = 0; k < 4; ++k) x[28 + k] = at[k];
+        double q1, q2;
+        net_forward(&Qt[0], x, h1, h2, &q1, 0);
+        net_forward(&Qt[1], x, h1, h2, &q2, 0);
+        y[s] = r[s] + h->gamma * (1.0 - done[s]) * fmin(q1, q2);
+    }
+    /* 2. critics: mean squared error to y, one Adam step each */
+    double* g = (double*)calloc((size_t)(na > nc ? na : nc), sizeof(double));
+    for (int c = 0; c < 2; ++c) {
+        memset(g, 0, sizeof(double) * (size_t)nc);
+        or_net gn = net_view(g, CI, H, 1);
+        double loss = 0.0;
+        for (int32_t s = 0; s < B; ++s) {
+            for (int k = 0; k < 28; ++k) x[k] = o_c[(size_t)s * 28 + k];
+            for (int k = 0; k < 4; ++k) x[28 + k] = a[(size_t)s * 4 + k];
+            double q;
+            net_forward(&Q[c], x, h1, h2, &q, 0);
+            loss += (q - y[s]) * (q - y[s]) / B;
+            double dq = 2.0 * (q - y[s]) / B;
+            net_backward(&Q[c], x, h1, h2, &q, 0, &dq, &gn, NULL);
+        }
+        if (grads) memcpy(grads + (size_t)c * nc, g, sizeof(double) * (size_t)nc);
+        adam(pc[c], m_c[c], v_c[c], g, nc, t_critic, h->lr_critic, h);
+        losses[c] = loss;
+    }
+    losses[2] = 0.0;
+    if (update_actor) {
+        /* 3. actor: maximise Q1(o_c, pi(o_a)) with the updated Q1 (deterministic policy
+         *    gradient through the critic's action input), one Adam step */
+        memset(g, 0, sizeof(double) * (size_t)na);
+        or_net gn = net_view(g, in_dim, H, 4);
+        double* gq = (double*)calloc((size_t)nc, sizeof(double));
+        or_net gqn = net_view(gq, CI, H, 1);  /* scratch: Q1's own gradient is discarded */
+        double ah1[64], ah2[64], loss = 0.0;
+        for (int32_t s = 0; s < B; ++s) {
+            const double* xa = o_a + (size_t)s * in_dim;
+            net_forward(&actor, xa, ah1, ah2, out, 1);
+            for (int k = 0; k < 28; ++k) x[k] = o_c[(size_t)s * 28 + k];
+            for (int k = 0; k < 4; ++k) x[28 + k] = out[k];
+            double q, dq = -1.0 / B, dx[CI];
+            net_forward(&Q[0], x, h1, h2, &q, 0);
+            loss += -q / B;
+            net_backward(&Q[0], x, h1, h2, &q, 0, &dq, &gqn, dx);
+            net_backward(&actor, xa, ah1, ah2, out, 1, dx + 28, &gn, NULL);
+        }
+        free(gq);
+        if (grads) memcpy(grads + 2 * (size_t)nc, g, sizeof(double) * (size_t)na);
+        adam(pa, m_a, v_a, g, na, t_actor, h->lr_actor, h);
+        losses[2] = loss;
+        /* 4. Polyak averaging of all three targets (on the delayed step, as TD3 does) */
+        for (int64_t k = 0; k < na; ++k) pa_t[k] = h->tau * pa[k] + (1.0 - h->tau) * pa_t[k];
+        for (int c = 0; c < 2; ++c)
+            for (int64_t k = 0; k < nc; ++k) pc_t[c][k] = h->tau * pc[c][k] + (1.0 - h->tau) * pc_t[c][k];
+    }
+    free(g);
+    free(y);
+}
+
 /* Size checks for the Python mirror. */
 int64_t or_sizeof_config(void) { return (int64_t)sizeof(or_config); }
 int64_t or_sizeof_env(void) { return (int64_t)sizeof(or_env); }
