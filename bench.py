@@ -473,6 +473,40 @@ def secondary(pkg, inputs, torch, dev, pk, f_clk):
                                  "success_fraction": float(ok.float().mean())}
     del env, pol, ct, r
     torch.cuda.empty_cache()
+    # f4: batched TD3 update (l2f_td3_update), one agent per SM, B = 256, actor 146-64-64-4,
+    # twin critics 32-64-64-1; a delayed (actor) step every second update (S:436 d = 2)
+    A, B, I = SMS, 256, 146
+    td3 = pkg.TD3(A, I, B, device=dev)
+    g = torch.Generator(device=dev).manual_seed(3)
+    td3.params.uniform_(-0.1, 0.1, generator=g)
+    o = td3.offsets()
+    td3.params[:, o["m_actor"]:].zero_()
+    bt = {"o_a": torch.randn(A, B, I, device=dev, generator=g) * 0.5, "o_c": torch.randn(A, B, 28, device=dev, generator=g) * 0.5,
+          "a": torch.rand(A, B, 4, device=dev, generator=g) * 2 - 1, "r": torch.randn(A, B, device=dev, generator=g),
+          "o_a2": torch.randn(A, B, I, device=dev, generator=g) * 0.5, "o_c2": torch.randn(A, B, 28, device=dev, generator=g) * 0.5,
+          "done": (torch.rand(A, B, device=dev, generator=g) < 0.1).float(), "eps": torch.randn(A, B, 4, device=dev, generator=g)}
+    for k in range(4):
+        td3.update(bt, update_actor=(k % 2 == 1))
+    torch.cuda.synchronize()
+    reps = 20
+    e0.record(stream)
+    for k in range(reps):
+        td3.update(bt, update_actor=(k % 2 == 1))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    # algorithmic FP32 work per sample (MAC = 2 flops): target actor + 2 target critics 26 112,
+    # 2 x critic (forward 6 208 + deltas 4 160 + weight gradients 6 208) 33 152, and on the delayed
+    # step actor forward 13 696 + Q1 forward/backward 12 416 + actor deltas 4 352 + gradients 13 696
+    macs = B * (26112 + 33152 + 0.5 * (13696 + 12416 + 4352 + 13696))
+    tf = A * 2 * macs / (ms / 1e3) / 1e12
+    fp32_peak = SMS * 128 * 2 * f_clk / 1e12
+    out["td3_update"] = {"value": A / (ms / 1e3), "unit": "agent-updates/s", "ms_per_call": ms,
+                         "workload": f"{A} agents x batch {B}, actor {I}-64-64-4, twin critics 32-64-64-1, actor every 2nd",
+                         "roofline": {"bound": "fp32", "achieved": tf, "peak": fp32_peak, "unit": "TFLOP/s",
+                                      "frac": tf / fp32_peak, "peak_source": "148 SMs x 128 FP32 lanes x 2 x sampled clock"}}
+    del td3, bt
+    torch.cuda.empty_cache()
     return out
 
 

@@ -277,6 +277,44 @@ typedef struct {
  * clip bounds <= 0. */
 L2F_API l2f_status l2f_track(l2f_env* env, const l2f_policy* policy, const l2f_tracking* spec, void* stream);
 
+/* ---- batched TD3 update (Q32-Q35) ---------- */
+
+/* TD3 hyper-parameters (S:436 defaults: gamma 0.99, tau 0.005, sigma_t 0.2, clip_t 0.5,
+ * lr 3e-4 / 3e-4, Adam beta1 0.9, beta2 0.999, eps 1e-8). */
+typedef struct {
+    double gamma, tau, sigma_t, clip_t, lr_actor, lr_critic, beta1, beta2, eps;
+} l2f_td3_hyper;
+
+/* One replay batch per agent, device FP32, [A][B][...] row-major: actor observations o_a /
+ * o_a2 [in_dim], critic observations o_c / o_c2 [28] (l2f_step_out.obs_critic layout per
+ * sample), actions a [4] (as applied), rewards r, done (1 = terminal, 0 otherwise; truncation
+ * is not terminal), eps [4]: standard normals of the target-policy smoothing noise (drawn
+ * by the caller, e.g. torch.randn). */
+typedef struct {
+    const float *o_a, *o_c, *a, *r, *o_a2, *o_c2, *done, *eps;
+} l2f_td3_batch;
+
+/* Sizes: floats of one agent's parameter block and bytes of its scratch.  Block layout
+ * (FP32): [actor, actor', Q1, Q2, Q1', Q2', m_actor, v_actor, m_Q1, v_Q1, m_Q2, v_Q2]; each
+ * net is W1[64][in], b1[64], W2[64][64], b2[64], W3[out][64], b3[out] with the actor
+ * in_dim -> 4 (ReLU, ReLU, tanh) and the critics 32 -> 1 (ReLU, ReLU, linear) on
+ * concat(o_c, a).  INVALID_ARGUMENT unless 1 <= batch <= 256 and 1 <= in_dim <= 256. */
+L2F_API l2f_status l2f_td3_sizes(int32_t in_dim, int32_t batch, int64_t* block_floats,
+                                 int64_t* scratch_bytes_per_agent);
+
+/* One TD3 update of each of n_agents independent agents (one CTA each): clipped double-Q
+ * target with clipped smoothing noise, both critics regressed by MSE (one Adam step each,
+ * Adam step number t_critic >= 1), and if update_actor (the delayed step, every d-th call):
+ * the deterministic policy gradient through the updated Q1's action input (Adam step
+ * t_actor >= 1) and Polyak averaging of the three targets with tau.  d_losses [A][3] out:
+ * critic 1, critic 2, actor (0 when not updated).  d_scratch: n_agents x scratch bytes,
+ * caller-owned; after the call it holds the raw gradients (documented for tests: see
+ * l2f_td3.cu).  All pointers device, asynchronous on `stream`. */
+L2F_API l2f_status l2f_td3_update(float* d_params, int32_t n_agents, int32_t in_dim, int32_t batch,
+                                  const l2f_td3_batch* b, const l2f_td3_hyper* h, int64_t t_critic,
+                                  int64_t t_actor, int32_t update_actor, float* d_losses, void* d_scratch,
+                                  void* stream);
+
 /* ---- state access --------------------------------------------------------------------- */
 
 L2F_API l2f_status l2f_get_state(l2f_env* env, l2f_state_view* out);

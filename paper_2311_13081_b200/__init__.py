@@ -15,7 +15,7 @@ import torch
 from .abi import (ABI_VERSION, DONE_DIVERGED, DONE_RESET, DONE_TERMINATED, DONE_TRUNCATED,  # noqa: F401
                   OBS_CORE, STATE_DIM, STATS, STATS_LEN, TRACE_FIELDS, L2FError, lib, make_config)
 
-__all__ = ["Env", "Policy", "policy_forward", "lib", "L2FError", "launch_count"]
+__all__ = ["Env", "Policy", "policy_forward", "TD3", "lib", "L2FError", "launch_count"]
 
 
 def _stream(stream=None) -> C.c_void_p:
@@ -268,3 +268,67 @@ class Env:
         _check(lib().l2f_rollout_host(self.h, C.byref(policy.s), int(T), _ptr(h_stats), int(reset_stats),
                                       _stream(stream)), "l2f_rollout_host")
         return h_stats
+
+
+class TD3:
+    """Batched TD3 learner of n_agents independent agents (l2f_td3_update).
+    params [A][block] FP32: [actor, actor', Q1, Q2, Q1', Q2', m/v of actor, Q1, Q2] (include/l2f.h)."""
+
+    DEFAULTS = {"gamma": 0.99, "tau": 0.005, "sigma_t": 0.2, "clip_t": 0.5, "lr_actor": 3e-4, "lr_critic": 3e-4,
+                "beta1": 0.9, "beta2": 0.999, "eps": 1e-8}
+
+    def __init__(self, n_agents: int, in_dim: int, batch: int = 256, hyper: dict | None = None, device="cuda"):
+        from .abi import TD3Hyper
+        blk, sb = C.c_int64(), C.c_int64()
+        _check(lib().l2f_td3_sizes(int(in_dim), int(batch), C.byref(blk), C.byref(sb)), "l2f_td3_sizes")
+        self.A, self.in_dim, self.B, self.device = int(n_agents), int(in_dim), int(batch), device
+        self.block, self.scratch_bytes = int(blk.value), int(sb.value)
+        self.params = torch.zeros(self.A, self.block, device=device)
+        self.scratch = torch.zeros(self.A * self.scratch_bytes, dtype=torch.uint8, device=device)
+        self.losses = torch.zeros(self.A, 3, device=device)
+        self.hyper = {**self.DEFAULTS, **(hyper or {})}
+        self.h = TD3Hyper(**self.hyper)
+        self.t_critic = self.t_actor = 0
+        self.na = 64 * in_dim + 64 + 64 * 64 + 64 + 4 * 64 + 4
+        self.nc = 64 * 32 + 64 + 64 * 64 + 64 + 64 + 1
+
+    def offsets(self) -> dict:
+        na, nc = self.na, self.nc
+        o = {"actor": 0, "actor_t": na, "q1": 2 * na, "q2": 2 * na + nc, "q1_t": 2 * na + 2 * nc,
+             "q2_t": 2 * na + 3 * nc, "m_actor": 2 * na + 4 * nc, "v_actor": 3 * na + 4 * nc,
+             "m_q1": 4 * na + 4 * nc, "v_q1": 4 * na + 5 * nc, "m_q2": 4 * na + 6 * nc, "v_q2": 4 * na + 7 * nc}
+        return o
+
+    def update(self, batch: dict, update_actor: bool, stream=None):
+        """One update of every agent; batch tensors [A][B][...] fp32 on the device."""
+        from .abi import TD3Batch
+        keep = {k: batch[k].to(device=self.device, dtype=torch.float32).contiguous()
+                for k in ("o_a", "o_c", "a", "r", "o_a2", "o_c2", "done", "eps")}
+        b = TD3Batch(**{k: v.data_ptr() for k, v in keep.items()})
+        self.t_critic += 1
+        if update_actor:
+            self.t_actor += 1
+        _check(lib().l2f_td3_update(_ptr(self.params), self.A, self.in_dim, self.B, C.byref(b), C.byref(self.h),
+                                    self.t_critic, max(self.t_actor, 1), int(bool(update_actor)), _ptr(self.losses),
+                                    _ptr(self.scratch), _stream(stream)), "l2f_td3_update")
+        return self.losses
+
+    def grads(self) -> dict:
+        """Raw gradients of the last update (per agent views into the scratch): q1, q2, actor."""
+        f = self.scratch.view(torch.float32).view(self.A, self.scratch_bytes // 4)
+        g0 = self.B * (1 + 32 + 4 * 64 + 1 + 2 * 64 + 4 + 2 * 64 + 4)
+        return {"q1": f[:, g0:g0 + self.nc], "q2": f[:, g0 + self.nc:g0 + 2 * self.nc],
+                "actor": f[:, g0 + 2 * self.nc:g0 + 2 * self.nc + self.na]}
+
+    def actor_policy_weights(self, agent: int = 0) -> dict:
+        """The agent's actor as fp16 bit patterns in the l2f_policy layout (for Policy / rollouts)."""
+        import numpy as np
+        p = self.params[agent, :self.na].cpu().numpy()
+        I, o = self.in_dim, 0
+        out = {}
+        for k, n in (("W1", 64 * I), ("b1", 64), ("W2", 64 * 64), ("b2", 64), ("W3", 4 * 64), ("b3", 4)):
+            a = p[o:o + n].astype(np.float16).view(np.uint16)
+            out[k] = a.reshape(64, I) if k == "W1" else (a.reshape(64, 64) if k == "W2" else
+                                                          (a.reshape(4, 64) if k == "W3" else a))
+            o += n
+        return out

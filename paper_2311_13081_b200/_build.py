@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libl2f.so")
-SOURCES = ["l2f_abi.cu", "l2f_kernels.cu", "l2f_mlp.cu"]
+SOURCES = ["l2f_abi.cu", "l2f_kernels.cu", "l2f_mlp.cu", "l2f_td3.cu"]
 HEADERS = ["l2f_device.cuh", "l2f_internal.h", "l2f_tcgen05.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -12,7 +12,7 @@ STATE_DIM, OBS_CORE, MAX_HIST, STATS_LEN, TRACE_FIELDS = 17, 18, 32, 8, 32
 DONE_TERMINATED, DONE_TRUNCATED, DONE_DIVERGED, DONE_RESET = 1, 2, 4, 8
 STATS = ["episodes", "terminated", "truncated", "diverged", "sum_len", "sum_ret", "sum_ret_sq", "env_steps"]
 EXPORTS = ["l2f_workspace_size", "l2f_create", "l2f_destroy", "l2f_reset", "l2f_step", "l2f_rollout",
-           "l2f_episode_stats", "l2f_step_host", "l2f_rollout_host", "l2f_get_state", "l2f_set_t", "l2f_set_state", "l2f_track",
+           "l2f_episode_stats", "l2f_step_host", "l2f_rollout_host", "l2f_get_state", "l2f_set_t", "l2f_set_state", "l2f_track", "l2f_td3_sizes", "l2f_td3_update",
            "l2f_policy_forward", "l2f_recompute_rewards", "l2f_selftest_philox", "l2f_launch_count", "l2f_last_error", "l2f_abi_version"]
 
 
@@ -63,6 +63,15 @@ class Tracking(C.Structure):
     _fields_ = [("cycle_time", C.c_void_p), ("amp_x", C.c_double), ("amp_y", C.c_double),
                 ("altitude", C.c_double), ("clip_pos", C.c_double), ("clip_vel", C.c_double),
                 ("n_steps", C.c_int32), ("rmse", C.c_void_p), ("rmse_xy", C.c_void_p), ("steps_ok", C.c_void_p)]
+
+
+class TD3Hyper(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("gamma", "tau", "sigma_t", "clip_t", "lr_actor", "lr_critic", "beta1",
+                                          "beta2", "eps")]
+
+
+class TD3Batch(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("o_a", "o_c", "a", "r", "o_a2", "o_c2", "done", "eps")]
 
 
 class StateView(C.Structure):
@@ -147,6 +156,9 @@ def lib():
         L.l2f_set_t.argtypes = [vp, C.c_uint64]
         L.l2f_set_state.argtypes = [vp, C.POINTER(StateView), vp]
         L.l2f_track.argtypes = [vp, vp, C.POINTER(Tracking), vp]
+        L.l2f_td3_sizes.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.l2f_td3_update.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.POINTER(TD3Batch), C.POINTER(TD3Hyper),
+                                     C.c_int64, C.c_int64, C.c_int32, vp, vp, vp]
         L.l2f_policy_forward.argtypes = [C.POINTER(PolicyS), vp, vp, C.c_int64, vp]
         L.l2f_recompute_rewards.argtypes = [vp, C.c_uint64, vp, vp, C.c_int64, vp, vp]
         L.l2f_selftest_philox.argtypes = [C.c_int64, C.c_uint64, C.c_uint32, vp, vp, vp]

@@ -484,6 +484,66 @@ l2f_status l2f_track(l2f_env* env, const l2f_policy* policy, const l2f_tracking*
     return st;
 }
 
+l2f_status l2f_td3_sizes(int32_t in_dim, int32_t batch, int64_t* block_floats, int64_t* scratch_bytes_per_agent)
+{
+    if (in_dim < 1 || in_dim > 256 || batch < 1 || batch > 256)
+        return fail(L2F_ERR_INVALID_ARGUMENT, "TD3 needs 1 <= in_dim <= 256 and 1 <= batch <= 256");
+    if (block_floats) *block_floats = td3_block_floats(in_dim);
+    if (scratch_bytes_per_agent) *scratch_bytes_per_agent = td3_scratch_bytes(in_dim, batch);
+    return L2F_OK;
+}
+
+l2f_status l2f_td3_update(float* d_params, int32_t n_agents, int32_t in_dim, int32_t batch, const l2f_td3_batch* b,
+                          const l2f_td3_hyper* h, int64_t t_critic, int64_t t_actor, int32_t update_actor,
+                          float* d_losses, void* d_scratch, void* stream)
+{
+    int64_t blk = 0, sb = 0;
+    l2f_status st = l2f_td3_sizes(in_dim, batch, &blk, &sb);
+    if (st != L2F_OK) return st;
+    if (!d_params || !b || !h || !d_losses || !d_scratch || n_agents < 1)
+        return fail(L2F_ERR_INVALID_ARGUMENT, "bad TD3 arguments");
+    if (!b->o_a || !b->o_c || !b->a || !b->r || !b->o_a2 || !b->o_c2 || !b->done || !b->eps)
+        return fail(L2F_ERR_INVALID_ARGUMENT, "TD3 batch pointer is NULL");
+    if (t_critic < 1 || (update_actor && t_actor < 1)) return fail(L2F_ERR_INVALID_ARGUMENT, "Adam steps start at 1");
+    if (!(h->gamma >= 0 && h->gamma <= 1) || !(h->tau >= 0 && h->tau <= 1) || !(h->beta1 >= 0 && h->beta1 < 1) ||
+        !(h->beta2 >= 0 && h->beta2 < 1) || !(h->eps > 0))
+        return fail(L2F_ERR_INVALID_ARGUMENT, "bad TD3 hyper-parameters");
+    TD3Dev A;
+    A.params = d_params;
+    A.scratch = (float*)d_scratch;
+    A.losses = d_losses;
+    A.o_a = b->o_a;
+    A.o_c = b->o_c;
+    A.a = b->a;
+    A.r = b->r;
+    A.o_a2 = b->o_a2;
+    A.o_c2 = b->o_c2;
+    A.done = b->done;
+    A.eps = b->eps;
+    A.block = blk;
+    A.scratch_floats = sb / 4;
+    A.n_agents = n_agents;
+    A.B = batch;
+    A.in_dim = in_dim;
+    A.update_actor = update_actor ? 1 : 0;
+    A.gamma = (float)h->gamma;
+    A.tau = (float)h->tau;
+    A.sigma_t = (float)h->sigma_t;
+    A.clip_t = (float)h->clip_t;
+    A.lr_actor = (float)h->lr_actor;
+    A.lr_critic = (float)h->lr_critic;
+    A.beta1 = (float)h->beta1;
+    A.beta2 = (float)h->beta2;
+    A.adam_eps = (float)h->eps;
+    A.c1_critic = (float)(1.0 - std::pow(h->beta1, (double)t_critic));
+    A.c2_critic = (float)(1.0 - std::pow(h->beta2, (double)t_critic));
+    A.c1_actor = (float)(1.0 - std::pow(h->beta1, (double)(t_actor > 0 ? t_actor : 1)));
+    A.c2_actor = (float)(1.0 - std::pow(h->beta2, (double)(t_actor > 0 ? t_actor : 1)));
+    const cudaError_t e = launch_td3_update(A, (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported) return fail(L2F_ERR_NOT_SUPPORTED, "TD3 configuration not supported");
+    return launched(e, "l2f_td3_update");
+}
+
 l2f_status l2f_episode_stats(l2f_env* env, double* d_out, int32_t reset_accumulators, void* stream)
 {
     if (!env || !d_out) return fail(L2F_ERR_INVALID_ARGUMENT, "env/out is NULL");

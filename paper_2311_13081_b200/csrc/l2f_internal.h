@@ -57,4 +57,19 @@ struct TrackDev {
 cudaError_t launch_track_mlp(const DevParams& P, const DevBufs& B, const PolicyDev& W, const TrackDev& S,
                              cudaStream_t s);
 
+// Batched TD3 update (l2f_td3.cu): one CTA per agent, one thread per sample.
+struct TD3Dev {
+    float* params;          // [A][block] flat FP32 blocks (td3_block_floats)
+    float* scratch;         // [A][scratch_floats]
+    float* losses;          // [A][3]
+    const float *o_a, *o_c, *a, *r, *o_a2, *o_c2, *done, *eps;  // [A][B][...]
+    int64_t block, scratch_floats;
+    int32_t n_agents, B, in_dim, update_actor;
+    float gamma, tau, sigma_t, clip_t, lr_actor, lr_critic, beta1, beta2, adam_eps;
+    float c1_critic, c2_critic, c1_actor, c2_actor;  // Adam bias corrections 1 - beta^t
+};
+int64_t td3_block_floats(int in_dim);
+int64_t td3_scratch_bytes(int in_dim, int B);
+cudaError_t launch_td3_update(const TD3Dev& A, cudaStream_t s);
+
 }  // namespace l2f

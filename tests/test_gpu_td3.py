@@ -1,0 +1,134 @@
+"""GPU <-> oracle parity of the batched TD3 update, l2f_td3_update (DESIGN.md
+Q32-Q35).  The GPU runs FP32, the oracle FP64 on the same (FP32-representable) inputs.
+
+Compared: losses, raw gradients (before Adam), and the updated parameters.  Adam divides by
+sqrt(v) + eps, so a gradient entry within FP32 noise of zero can legitimately move its
+parameter by anything in [-lr, lr]; updated parameters are therefore compared tightly only
+where the oracle's gradient is well above that noise, and elsewhere checked to stay within
+Adam's step bound."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2311_13081_b200 as p
+    p.lib()
+    return p
+
+
+def init_block(td3, seed):
+    """Online nets U(+-1/sqrt(fan_in)), targets different nets, zero moments; FP32 values."""
+    g = np.random.default_rng(seed)
+    o = td3.offsets()
+
+    def net(n_in, n_out):
+        parts = []
+        for (m, i) in ((64, n_in), (64, 64), (n_out, 64)):
+            b = 1.0 / np.sqrt(i)
+            parts += [g.uniform(-b, b, m * i), g.uniform(-b, b, m)]
+        return np.concatenate(parts)
+
+    P = np.zeros(td3.block)
+    P[o["actor"]:o["actor"] + td3.na] = net(td3.in_dim, 4)
+    P[o["actor_t"]:o["actor_t"] + td3.na] = net(td3.in_dim, 4)
+    for k in ("q1", "q2", "q1_t", "q2_t"):
+        P[o[k]:o[k] + td3.nc] = net(32, 1)
+    return P.astype(np.float32)
+
+
+def make_batch(A, B, I, seed):
+    g = np.random.default_rng(seed)
+    f = lambda *s: g.normal(0, 0.5, s).astype(np.float32)  # noqa: E731
+    return {"o_a": f(A, B, I), "o_c": f(A, B, 28), "a": g.uniform(-1, 1, (A, B, 4)).astype(np.float32),
+            "r": g.normal(-1, 1, (A, B)).astype(np.float32), "o_a2": f(A, B, I), "o_c2": f(A, B, 28),
+            "done": (g.uniform(0, 1, (A, B)) < 0.2).astype(np.float32), "eps": g.normal(0, 1, (A, B, 4)).astype(np.float32)}
+
+
+def run_both(pkg, A, B, I, steps, hyper=None, seed=0):
+    td3 = pkg.TD3(A, I, B, hyper=hyper)
+    blocks = [init_block(td3, seed + a) for a in range(A)]
+    td3.params.copy_(torch.as_tensor(np.stack(blocks)))
+    P_or = [b.astype(np.float64) for b in blocks]
+    res = []
+    for k, upd in enumerate(steps):
+        bt = make_batch(A, B, I, 100 + k)
+        losses = td3.update({kk: torch.as_tensor(v) for kk, v in bt.items()}, update_actor=upd).cpu().numpy()
+        gg = {kk: v.cpu().numpy().copy() for kk, v in td3.grads().items()}
+        ref = []
+        for a in range(A):
+            ba = {kk: v[a].astype(np.float64) for kk, v in bt.items()}
+            lo, go = oracle.td3_update(P_or[a], I, ba, td3.hyper, t_critic=td3.t_critic, t_actor=max(td3.t_actor, 1),
+                                       update_actor=upd, want_grads=True)
+            ref.append((lo, go))
+        res.append((losses, gg, ref))
+    return td3, P_or, res
+
+
+@pytest.mark.parametrize("I,B", [(146, 256), (34, 100)])
+def test_td3_update_matches_oracle(pkg, I, B):
+    A = 3
+    td3, P_or, res = run_both(pkg, A, B, I, [True, False, True])
+    nc, na = td3.nc, td3.na
+    for (losses, gg, ref) in res:
+        for a in range(A):
+            lo, go = ref[a]
+            assert np.allclose(losses[a], lo, rtol=2e-4, atol=1e-6), (a, losses[a], lo)
+            for name, sl, n in (("q1", slice(0, nc), nc), ("q2", slice(nc, 2 * nc), nc), ("actor", slice(2 * nc, 2 * nc + na), na)):
+                if name == "actor" and lo[2] == 0.0:
+                    continue
+                want = go[sl]
+                scale = np.abs(want).max()
+                assert np.abs(gg[name][a] - want).max() <= 1e-4 * scale + 1e-7, (name, a)
+    # parameters after the three updates
+    P_gpu = td3.params.cpu().numpy().astype(np.float64)
+    lr = td3.hyper["lr_critic"]
+    for a in range(A):
+        d = np.abs(P_gpu[a] - P_or[a])
+        assert d.max() <= 3 * lr + 1e-6  # never more than Adam's step bound apart
+        assert np.median(d) <= 1e-3 * lr + 1e-7  # and almost everywhere FP32-close
+
+
+def test_td3_special_cases(pkg):
+    """tau = 1 copies the online nets into the targets exactly; done = 1 with zero critics
+    gives the critic loss mean(r^2); no actor step leaves actor and targets untouched."""
+    A, B, I = 2, 64, 34
+    td3 = pkg.TD3(A, I, B, hyper={"tau": 1.0})
+    blocks = [init_block(td3, 7 + a) for a in range(A)]
+    o = td3.offsets()
+    for b in blocks:
+        b[o["q1"]:o["q1"] + td3.nc] = 0.0
+        b[o["q2"]:o["q2"] + td3.nc] = 0.0
+    td3.params.copy_(torch.as_tensor(np.stack(blocks)))
+    bt = make_batch(A, B, I, 5)
+    bt["done"][:] = 1.0
+    before = td3.params.clone()
+    losses = td3.update({k: torch.as_tensor(v) for k, v in bt.items()}, update_actor=False).cpu().numpy()
+    for a in range(A):
+        assert np.isclose(losses[a, 0], np.mean(bt["r"][a].astype(np.float64) ** 2), rtol=1e-5)
+        assert losses[a, 2] == 0.0
+    P = td3.params
+    assert torch.equal(P[:, :2 * td3.na], before[:, :2 * td3.na])  # actor + actor' untouched
+    td3.update({k: torch.as_tensor(v) for k, v in bt.items()}, update_actor=True)
+    P = td3.params
+    assert torch.equal(P[:, o["actor_t"]:o["actor_t"] + td3.na], P[:, :td3.na])
+    assert torch.equal(P[:, o["q1_t"]:o["q1_t"] + td3.nc], P[:, o["q1"]:o["q1"] + td3.nc])
+    assert torch.equal(P[:, o["q2_t"]:o["q2_t"] + td3.nc], P[:, o["q2"]:o["q2"] + td3.nc])
+
+
+def test_td3_actor_exports_to_the_rollout(pkg):
+    """The learner's actor (fp16-rounded) drives the tcgen05 policy path."""
+    import inputs
+    td3 = pkg.TD3(1, 146, 32)
+    td3.params.copy_(torch.as_tensor(init_block(td3, 3))[None])
+    W = td3.actor_policy_weights(0)
+    env = pkg.Env(inputs.config_c4(), 256)
+    env.reset()
+    env.rollout(5, policy=pkg.Policy(W))
+    assert torch.isfinite(env.state).all()
