@@ -16,5 +16,8 @@ ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 1
     python scripts/run_step.py > $OUT/ncu_step.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:rollout_open -c 1 -o $OUT/open \
     python scripts/run_open.py > $OUT/ncu_open.log 2>&1
-
+ncu --set full --clock-control none --import-source on -k regex:track_mlp -c 1 -o $OUT/track \
+    python scripts/run_track.py > $OUT/ncu_track.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:td3_update -s 1 -c 1 -o $OUT/td3 \
+    python scripts/run_td3.py > $OUT/ncu_td3.log 2>&1
 echo done
