@@ -115,14 +115,17 @@ __device__ __forceinline__ void mbar_arrive(uint32_t mbar_saddr)
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(mbar_saddr) : "memory");
 }
 
+#ifndef L2F_MBAR_SUSPEND_NS
+#define L2F_MBAR_SUSPEND_NS 100000  // try_wait suspend-time hint (ns): sleep until the phase flips instead of polling
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t mbar_saddr, uint32_t parity)
 {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(mbar_saddr),
-        "r"(parity)
+        "r"(parity), "n"(L2F_MBAR_SUSPEND_NS)
         : "memory");
 }
 
