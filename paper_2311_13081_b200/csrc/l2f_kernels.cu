@@ -8,7 +8,7 @@
 #include <curand_philox4x32_x.h>
 
 #ifndef L2F_STEP_MINB
-#define L2F_STEP_MINB 5  // resident 128-thread blocks per SM the register budget targets
+#define L2F_STEP_MINB 6  // resident 128-thread blocks per SM the register budget targets (4: 96 us, 5: 88, 6: 87, 7: 91, 8: 97 at C3)
 #endif
 
 #include "l2f_device.cuh"
