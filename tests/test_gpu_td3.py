@@ -1,11 +1,11 @@
 """GPU <-> oracle parity of the batched TD3 update, l2f_td3_update (DESIGN.md
 Q32-Q35).  The GPU runs FP32, the oracle FP64 on the same (FP32-representable) inputs.
 
-Compared: losses, raw gradients (before Adam), and the updated parameters.  Adam divides by
-sqrt(v) + eps, so a gradient entry within FP32 noise of zero can legitimately move its
-parameter by anything in [-lr, lr]; updated parameters are therefore compared tightly only
-where the oracle's gradient is well above that noise, and elsewhere checked to stay within
-Adam's step bound."""
+Compared: losses, raw gradients (before Adam; max error <= 1e-4 of the largest entry), and the
+updated parameters.  Adam divides by sqrt(v) + eps, so a gradient entry within FP32 noise of
+zero can legitimately move its parameter by anything in [-lr, lr]; the updated parameters are
+therefore required to stay within Adam's step bound of the oracle everywhere and to agree to
+1e-3 lr for the median entry."""
 import numpy as np
 import pytest
 import torch
@@ -132,3 +132,22 @@ def test_td3_actor_exports_to_the_rollout(pkg):
     env.reset()
     env.rollout(5, policy=pkg.Policy(W))
     assert torch.isfinite(env.state).all()
+
+
+@pytest.mark.parametrize("A,B,I", [(1, 1, 18), (5, 33, 18), (2, 256, 146)])
+def test_td3_edge_shapes_match_oracle(pkg, A, B, I):
+    """Single-sample batch, N_H = 0 actor input (in_dim 18), ragged batch, full batch."""
+    td3, P_or, res = run_both(pkg, A, B, I, [True], seed=11)
+    losses, gg, ref = res[0]
+    for a in range(A):
+        assert np.allclose(losses[a], ref[a][0], rtol=2e-4, atol=1e-6)
+        go = ref[a][1]
+        scale = np.abs(go[:td3.nc]).max()
+        assert np.abs(gg["q1"][a] - go[:td3.nc]).max() <= 1e-4 * scale + 1e-7
+
+
+def test_td3_invalid_arguments(pkg):
+    with pytest.raises(Exception):
+        pkg.TD3(1, 146, 0)
+    with pytest.raises(Exception):
+        pkg.TD3(1, 146, 257)

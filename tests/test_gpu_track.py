@@ -116,3 +116,17 @@ def test_track_invalid_arguments(pkg):
     bad = pkg.Policy(inputs.policy_weights(18 + 16, 64))
     with pytest.raises(Exception):
         env.track(bad, 5.5, 10)
+
+
+@pytest.mark.parametrize("n,steps", [(1, 1), (129, 3)])
+def test_track_tiny_runs_match_oracle(pkg, n, steps):
+    cfg = inputs.config_c4()
+    W = inputs.policy_weights(146, 64, seed=5, out_bias=inputs.hover_policy_bias())
+    env = pkg.Env(cfg, n)
+    env.reset()
+    out = env.track(pkg.Policy(W), 5.5, steps)
+    r, ok = out["rmse"].cpu().numpy(), out["steps_ok"].cpu().numpy()
+    ph = oracle.PolicyHandle(W)
+    for i in (0, n - 1):
+        orr, _, ook, _ = oracle.track(cfg, ph, i, 0, 5.5, steps)
+        assert ok[i] == ook and abs(r[i] - orr) <= 1e-4 + 1e-3 * orr
