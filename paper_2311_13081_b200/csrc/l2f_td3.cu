@@ -14,10 +14,13 @@
 // gradient through the updated Q1's action input, Adam, Polyak averaging of the targets.
 //
 // Layout of the work: the weights of the net in use are staged in shared memory (rows padded
-// to a multiple of 4 floats), the actor input rows too; each thread keeps its sample's
-// hidden vectors in registers (fully unrolled 64-wide loops, float4 weight reads that every
-// lane of a warp takes from the same address -- one shared-memory wavefront), and writes the
-// per-sample rows the weight gradients need to a per-agent global scratch (L2-resident).
+// to a multiple of 4 floats), the actor input rows too.  Two adjacent threads (lanes 2s,
+// 2s + 1) own sample s: each computes one half (32) of every hidden layer's outputs from the
+// full input vector, which the pair exchanges with warp shuffles; backward deltas are formed as
+// partial sums over the thread's half and pair-summed.  So every thread needs at most ~128
+// registers and a CTA runs 512 threads (16 warps) -- twice the latency hiding of one thread
+// per sample.  Per-sample rows the weight gradients need go to a per-agent global scratch
+// (L2-resident).
 #include <cmath>
 
 #include "l2f_internal.h"
@@ -25,7 +28,9 @@
 namespace l2f {
 namespace {
 
-constexpr int kT = 256;   // threads = max batch
+constexpr int kB = 256;   // max batch
+constexpr int kT = 2 * kB;  // two threads per sample
+constexpr int kHH = 32;   // half of the hidden width
 constexpr int kH = 64;    // hidden width
 constexpr int kCI = 32;   // critic input: o_c (28) + a (4)
 
@@ -110,114 +115,160 @@ __device__ __forceinline__ void fma4(float& acc, float4 w, float4 x)
     acc = fmaf(w.w, x.w, acc);
 }
 
-// h = relu(W1 x + b1) with x a shared-memory row of S.ld1 floats (padded with zeros); 16
-// outputs per pass over the row (x re-read 4 times, 16 accumulators live).
-__device__ __forceinline__ void layer1_smem(const NetS& S, const float* x, float (&h)[kH])
+// ---- half-layer helpers: thread hf in {0, 1} of a sample's pair owns outputs 32 hf .. 32 hf + 31
+
+// out = relu(W1 x + b1) for my 32 outputs, x a shared-memory row of S.ld1 floats (zero padded);
+// 16 outputs per pass over the row.
+__device__ __forceinline__ void l1_smem_half(const NetS& S, const float* x, int hf, float (&out)[kHH])
 {
+    const float* Wm = S.W1 + kHH * hf * S.ld1;
+    const float* bm = S.b1 + kHH * hf;
 #pragma unroll
-    for (int jb = 0; jb < kH; jb += 16) {
+    for (int jb = 0; jb < kHH; jb += 16) {
         float acc[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = S.b1[jb + j];
+        for (int j = 0; j < 16; ++j) acc[j] = bm[jb + j];
 #pragma unroll 1
         for (int c = 0; c < S.ld1; c += 4) {
             const float4 xv = ld4(x + c);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) fma4(acc[j], ld4(S.W1 + (jb + j) * S.ld1 + c), xv);
+            for (int j = 0; j < 16; ++j) fma4(acc[j], ld4(Wm + (jb + j) * S.ld1 + c), xv);
         }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) h[jb + j] = fmaxf(acc[j], 0.0f);
+        for (int j = 0; j < 16; ++j) out[jb + j] = fmaxf(acc[j], 0.0f);
     }
 }
 
-// h = relu(W1 x + b1) with x the 32-float critic input in registers (ld1 = 32).
-__device__ __forceinline__ void layer1_reg(const NetS& S, const float (&x)[kCI], float (&h)[kH])
+// out = relu(W1 x + b1) for my 32 outputs, x the sample's 32-float critic-input row (scratch).
+__device__ __forceinline__ void l1_row_half(const NetS& S, const float* xrow, int hf, float (&out)[kHH])
 {
+    float x[kCI];
 #pragma unroll
-    for (int j = 0; j < kH; ++j) {
-        float acc = S.b1[j];
+    for (int c = 0; c < kCI; c += 4) {
+        const float4 v = ld4(xrow + c);
+        x[c] = v.x;
+        x[c + 1] = v.y;
+        x[c + 2] = v.z;
+        x[c + 3] = v.w;
+    }
+    const float* Wm = S.W1 + kHH * hf * kCI;
+    const float* bm = S.b1 + kHH * hf;
+#pragma unroll
+    for (int j = 0; j < kHH; ++j) {
+        float acc = bm[j];
 #pragma unroll
         for (int c = 0; c < kCI; c += 4)
-            fma4(acc, ld4(S.W1 + j * kCI + c), make_float4(x[c], x[c + 1], x[c + 2], x[c + 3]));
-        h[j] = fmaxf(acc, 0.0f);
+            fma4(acc, ld4(Wm + j * kCI + c), make_float4(x[c], x[c + 1], x[c + 2], x[c + 3]));
+        out[j] = fmaxf(acc, 0.0f);
         if (j % 8 == 7) sched_fence();
     }
 }
 
-// h2 = relu(W2 h1 + b2)
-__device__ __forceinline__ void layer2(const NetS& S, const float (&h1)[kH], float (&h2)[kH])
+// The full 64-vector of a pair from the two halves: lo = outputs 0..31, hi = 32..63.
+__device__ __forceinline__ void gather(const float (&mine)[kHH], int hf, float (&lo)[kHH], float (&hi)[kHH])
 {
 #pragma unroll
-    for (int j = 0; j < kH; ++j) {
-        float acc = S.b2[j];
+    for (int j = 0; j < kHH; ++j) {
+        const float o = __shfl_xor_sync(0xffffffffu, mine[j], 1);
+        lo[j] = hf ? o : mine[j];
+        hi[j] = hf ? mine[j] : o;
+    }
+}
+
+// out = relu(W2 (lo, hi) + b2) for my 32 outputs.
+__device__ __forceinline__ void l2_half(const NetS& S, const float (&lo)[kHH], const float (&hi)[kHH], int hf,
+                                        float (&out)[kHH])
+{
+    const float* Wm = S.W2 + kHH * hf * kH;
+    const float* bm = S.b2 + kHH * hf;
 #pragma unroll
-        for (int c = 0; c < kH; c += 4)
-            fma4(acc, ld4(S.W2 + j * kH + c), make_float4(h1[c], h1[c + 1], h1[c + 2], h1[c + 3]));
-        h2[j] = fmaxf(acc, 0.0f);
+    for (int j = 0; j < kHH; ++j) {
+        float acc = bm[j];
+#pragma unroll
+        for (int c = 0; c < kHH; c += 4)
+            fma4(acc, ld4(Wm + j * kH + c), make_float4(lo[c], lo[c + 1], lo[c + 2], lo[c + 3]));
+#pragma unroll
+        for (int c = 0; c < kHH; c += 4)
+            fma4(acc, ld4(Wm + j * kH + kHH + c), make_float4(hi[c], hi[c + 1], hi[c + 2], hi[c + 3]));
+        out[j] = fmaxf(acc, 0.0f);
         if (j % 4 == 3) sched_fence();
     }
 }
 
-// y = W3 h2 + b3 (OUT outputs), tanh optional
+// y = W3 (lo, hi) + b3, all OUT outputs (both threads of the pair), tanh optional.
 template <int OUT>
-__device__ __forceinline__ void layer3(const NetS& S, const float (&h2)[kH], float (&y)[OUT], bool tanh_out)
+__device__ __forceinline__ void l3_full(const NetS& S, const float (&lo)[kHH], const float (&hi)[kHH], float (&y)[OUT],
+                                        bool tanh_out)
 {
 #pragma unroll
     for (int o = 0; o < OUT; ++o) {
         float acc = S.b3[o];
 #pragma unroll
-        for (int c = 0; c < kH; c += 4)
-            fma4(acc, ld4(S.W3 + o * kH + c), make_float4(h2[c], h2[c + 1], h2[c + 2], h2[c + 3]));
+        for (int c = 0; c < kHH; c += 4)
+            fma4(acc, ld4(S.W3 + o * kH + c), make_float4(lo[c], lo[c + 1], lo[c + 2], lo[c + 3]));
+#pragma unroll
+        for (int c = 0; c < kHH; c += 4)
+            fma4(acc, ld4(S.W3 + o * kH + kHH + c), make_float4(hi[c], hi[c + 1], hi[c + 2], hi[c + 3]));
         y[o] = tanh_out ? tanhf(acc) : acc;
     }
 }
 
-// d2 = (W3^T d3) o relu'(h2)
+// d2 = (W3^T d3) o relu'(h2) for my 32 outputs.
 template <int OUT>
-__device__ __forceinline__ void delta2(const NetS& S, const float (&d3)[OUT], const float (&h2)[kH], float (&d2)[kH])
+__device__ __forceinline__ void d2_half(const NetS& S, const float (&d3)[OUT], const float (&h2m)[kHH], int hf,
+                                        float (&d2m)[kHH])
 {
 #pragma unroll
-    for (int j = 0; j < kH; ++j) {
+    for (int j = 0; j < kHH; ++j) {
         float acc = 0.0f;
 #pragma unroll
-        for (int o = 0; o < OUT; ++o) acc = fmaf(S.W3[o * kH + j], d3[o], acc);
-        d2[j] = h2[j] > 0.0f ? acc : 0.0f;
+        for (int o = 0; o < OUT; ++o) acc = fmaf(S.W3[o * kH + kHH * hf + j], d3[o], acc);
+        d2m[j] = h2m[j] > 0.0f ? acc : 0.0f;
     }
 }
 
-// d1 = (W2^T d2) o relu'(h1), four outputs at a time (float4 column slices of the W2 rows),
-// so only d2 and four accumulators are live.  d1 may alias h1.
-__device__ __forceinline__ void delta1(const NetS& S, const float (&d2)[kH], float (&h1_d1)[kH])
+// d1 = (W2^T d2) o relu'(h1), my 32 entries, in place of h1 (h1d1m: h1 in, d1 out): partial
+// sums over my 32 rows of W2 for each half of the 64 outputs, pair-summed with one shuffle per
+// entry (the partner's partial of my half).
+__device__ __forceinline__ void d1_half(const NetS& S, const float (&d2m)[kHH], int hf, float (&h1d1m)[kHH])
 {
+    const float* Wm = S.W2 + kHH * hf * kH;
 #pragma unroll
-    for (int c = 0; c < kH; c += 4) {
-        float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    for (int half = 0; half < 2; ++half) {
+        float acc[kHH];
 #pragma unroll
-        for (int j = 0; j < kH; ++j) {
-            const float4 w = ld4(S.W2 + j * kH + c);
-            a0 = fmaf(w.x, d2[j], a0);
-            a1 = fmaf(w.y, d2[j], a1);
-            a2 = fmaf(w.z, d2[j], a2);
-            a3 = fmaf(w.w, d2[j], a3);
+        for (int i = 0; i < kHH; ++i) acc[i] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < kHH; ++j) {
+#pragma unroll
+            for (int c = 0; c < kHH; c += 4) {
+                const float4 w = ld4(Wm + j * kH + kHH * half + c);
+                acc[c] = fmaf(w.x, d2m[j], acc[c]);
+                acc[c + 1] = fmaf(w.y, d2m[j], acc[c + 1]);
+                acc[c + 2] = fmaf(w.z, d2m[j], acc[c + 2]);
+                acc[c + 3] = fmaf(w.w, d2m[j], acc[c + 3]);
+            }
+            if (j % 8 == 7) sched_fence();
         }
-        h1_d1[c] = h1_d1[c] > 0.0f ? a0 : 0.0f;
-        h1_d1[c + 1] = h1_d1[c + 1] > 0.0f ? a1 : 0.0f;
-        h1_d1[c + 2] = h1_d1[c + 2] > 0.0f ? a2 : 0.0f;
-        h1_d1[c + 3] = h1_d1[c + 3] > 0.0f ? a3 : 0.0f;
-        sched_fence();
+#pragma unroll
+        for (int i = 0; i < kHH; ++i) {
+            const float other = __shfl_xor_sync(0xffffffffu, acc[i], 1);
+            if (half == hf) h1d1m[i] = h1d1m[i] > 0.0f ? acc[i] + other : 0.0f;
+        }
     }
 }
 
-__device__ __forceinline__ void store_row(float* dst, const float (&v)[kH])
+__device__ __forceinline__ void store_half(float* row, int hf, const float (&v)[kHH])
 {
 #pragma unroll
-    for (int c = 0; c < kH; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+    for (int c = 0; c < kHH; c += 4)
+        *reinterpret_cast<float4*>(row + kHH * hf + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
 }
-__device__ __forceinline__ void load_row(const float* src, float (&v)[kH])
+__device__ __forceinline__ void load_half(const float* row, int hf, float (&v)[kHH])
 {
 #pragma unroll
-    for (int c = 0; c < kH; c += 4) {
-        const float4 x = ld4(src + c);
+    for (int c = 0; c < kHH; c += 4) {
+        const float4 x = ld4(row + kHH * hf + c);
         v[c] = x.x;
         v[c + 1] = x.y;
         v[c + 2] = x.z;
@@ -354,8 +405,10 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
 {
     extern __shared__ __align__(16) float sm[];
     __shared__ float red[kT / 32];
-    const int ag = blockIdx.x, B = A.B, I = A.in_dim, s = threadIdx.x, LI = pad4(A.in_dim);
-    const bool act = s < B;
+    const int ag = blockIdx.x, B = A.B, I = A.in_dim, LI = pad4(A.in_dim);
+    const int s = threadIdx.x >> 1, hf = threadIdx.x & 1;  // sample, half of the pair
+    const bool act = s < B;                                // (inactive pairs still shuffle)
+    const bool lead = act && hf == 0;                      // writes the per-sample scalars
     const int na = net_size(I, 4), nc = net_size(kCI, 1);
     float* P = A.params + (int64_t)ag * A.block;
     NetP actor = net_at(P, I, 4), actor_t = net_at(P + na, I, 4);
@@ -366,11 +419,14 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     float* m_c[2] = {v_a + na, v_a + na + 2 * nc};
     float* v_c[2] = {v_a + na + nc, v_a + na + 3 * nc};
     TD3Scratch S = scratch_at(A.scratch + (int64_t)ag * A.scratch_floats, B);
-    const int64_t rb = (int64_t)ag * B + s;  // this sample's row in the [A][B][...] batch arrays
+    const int sc = act ? s : 0;  // clamped sample index for inactive lanes' (discarded) loads
+    const int64_t rb = (int64_t)ag * B + sc;
     // shared memory: input rows xs [B][LI], then one staged net
     float* xs = sm;
     float* wsm = sm + pad4(B * LI);
-    float h1[kH], h2[kH], x[kCI];
+    float h1m[kHH], h2m[kHH], lo[kHH], hi[kHH];
+    float* const xt = S.d1 + sc * kH;  // target-critic input row (o_c', a'): S.d1 is free until phase 2
+    float* const xcr = S.xc + sc * kCI;  // critic input row (o_c, a)
 
     // ---- 1. target: a' = clip(pi'(o_a') + clip(sigma eps, -c, c), -1, 1); y = r + g (1-d) min Q'
 #pragma unroll 4
@@ -380,46 +436,51 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     }
     NetS W = stage(actor_t, wsm);
     __syncthreads();
-    if (act) {
+    {
         float at[4];
-        layer1_smem(W, xs + s * LI, h1);
-        layer2(W, h1, h2);
-        layer3<4>(W, h2, at, true);
+        l1_smem_half(W, xs + sc * LI, hf, h1m);
+        gather(h1m, hf, lo, hi);
+        l2_half(W, lo, hi, hf, h2m);
+        gather(h2m, hf, lo, hi);
+        l3_full<4>(W, lo, hi, at, true);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const float nz = fminf(fmaxf(A.sigma_t * A.eps[rb * 4 + k], -A.clip_t), A.clip_t);
             at[k] = fminf(fmaxf(at[k] + nz, -1.0f), 1.0f);
         }
+        // the pair writes the target-critic input row: lane hf the 16 floats [16 hf, 16 hf + 16)
+        if (act) {
 #pragma unroll
-        for (int k = 0; k < 28; ++k) x[k] = A.o_c2[rb * 28 + k];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) x[28 + k] = at[k];
+            for (int k = 0; k < 16; ++k) {
+                const int q = 16 * hf + k;
+                xt[q] = q < 28 ? A.o_c2[rb * 28 + q] : at[q - 28];
+            }
+        }
     }
+    __syncwarp();
     float qmin = 0.0f;
     for (int c = 0; c < 2; ++c) {
         __syncthreads();
         W = stage(Qt[c], wsm);
         __syncthreads();
-        if (act) {
-            float q[1];
-            layer1_reg(W, x, h1);
-            layer2(W, h1, h2);
-            layer3<1>(W, h2, q, false);
-            qmin = c == 0 ? q[0] : fminf(qmin, q[0]);
+        float q[1];
+        l1_row_half(W, xt, hf, h1m);
+        gather(h1m, hf, lo, hi);
+        l2_half(W, lo, hi, hf, h2m);
+        gather(h2m, hf, lo, hi);
+        l3_full<1>(W, lo, hi, q, false);
+        qmin = c == 0 ? q[0] : fminf(qmin, q[0]);
+    }
+    const float y = A.r[rb] + A.gamma * (1.0f - A.done[rb]) * qmin;
+    // the critic input row (o_c, a), shared by both critics
+    if (act) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int q = 16 * hf + k;
+            xcr[q] = q < 28 ? A.o_c[rb * 28 + q] : A.a[rb * 4 + (q - 28)];
         }
     }
-    float y = 0.0f;
-    if (act) {
-        y = A.r[rb] + A.gamma * (1.0f - A.done[rb]) * qmin;
-        // the critic input (o_c, a) of this sample, shared by both critics
-#pragma unroll
-        for (int k = 0; k < 28; ++k) x[k] = A.o_c[rb * 28 + k];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) x[28 + k] = A.a[rb * 4 + k];
-#pragma unroll
-        for (int k = 0; k < kCI; k += 4)
-            *reinterpret_cast<float4*>(S.xc + s * kCI + k) = make_float4(x[k], x[k + 1], x[k + 2], x[k + 3]);
-    }
+    __syncwarp();
 
     // ---- 2. critics: MSE to y, Adam
     const AdamC Ac{A.lr_critic, A.beta1, A.beta2, A.c1_critic, A.c2_critic, A.adam_eps};
@@ -427,24 +488,23 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         __syncthreads();
         W = stage(Q[c], wsm);
         __syncthreads();
-        float lossc = 0.0f;
-        if (act) {
-            float q[1], d2[kH];
-            layer1_reg(W, x, h1);
-            store_row(S.h1 + s * kH, h1);
-            layer2(W, h1, h2);
-            store_row(S.h2 + s * kH, h2);
-            layer3<1>(W, h2, q, false);
-            const float e = q[0] - y;
-            lossc = e * e / (float)B;
-            const float d3[1] = {2.0f * e / (float)B};
-            delta2<1>(W, d3, h2, d2);
-            store_row(S.d2 + s * kH, d2);
-            delta1(W, d2, h1);  // h1 <- d1
-            store_row(S.d1 + s * kH, h1);
-            S.d3[s] = d3[0];
-        }
-        const float loss = block_sum(lossc, red);
+        float q[1], d2m[kHH];
+        l1_row_half(W, xcr, hf, h1m);
+        if (act) store_half(S.h1 + s * kH, hf, h1m);
+        gather(h1m, hf, lo, hi);
+        l2_half(W, lo, hi, hf, h2m);
+        if (act) store_half(S.h2 + s * kH, hf, h2m);
+        gather(h2m, hf, lo, hi);
+        l3_full<1>(W, lo, hi, q, false);
+        const float e = q[0] - y;
+        const float d3[1] = {2.0f * e / (float)B};
+        d2_half<1>(W, d3, h2m, hf, d2m);
+        if (act) store_half(S.d2 + s * kH, hf, d2m);
+        load_half(S.h1 + sc * kH, hf, h1m);  // (reloaded: not kept live across layer 2)
+        d1_half(W, d2m, hf, h1m);  // h1m <- my half of d1
+        if (act) store_half(S.d1 + s * kH, hf, h1m);
+        if (lead) S.d3[s] = d3[0];
+        const float loss = block_sum(lead ? e * e / (float)B : 0.0f, red);
         if (threadIdx.x == 0) A.losses[ag * 3 + c] = loss;
         __syncthreads();
         float* g = c == 0 ? S.gq1 : S.gq2;
@@ -469,54 +529,60 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     }
     W = stage(actor, wsm);
     __syncthreads();
-    float ap[4] = {0.f, 0.f, 0.f, 0.f};
-    if (act) {
-        layer1_smem(W, xs + s * LI, h1);
-        store_row(S.ah1 + s * kH, h1);
-        layer2(W, h1, h2);
-        store_row(S.ah2 + s * kH, h2);
-        layer3<4>(W, h2, ap, true);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) x[28 + k] = ap[k];
-    }
+    float ap[4];
+    l1_smem_half(W, xs + sc * LI, hf, h1m);
+    if (act) store_half(S.ah1 + s * kH, hf, h1m);
+    gather(h1m, hf, lo, hi);
+    l2_half(W, lo, hi, hf, h2m);
+    if (act) store_half(S.ah2 + s * kH, hf, h2m);
+    gather(h2m, hf, lo, hi);
+    l3_full<4>(W, lo, hi, ap, true);
+    if (act && hf == 1) *reinterpret_cast<float4*>(xcr + 28) = make_float4(ap[0], ap[1], ap[2], ap[3]);  // (o_c, pi(o_a))
     __syncthreads();
     W = stage(Q[0], wsm);  // the updated Q1
     __syncthreads();
-    float lossa = 0.0f;
     float da[4] = {0.f, 0.f, 0.f, 0.f};
-    if (act) {
-        float q[1], d2[kH];
-        layer1_reg(W, x, h1);
-        layer2(W, h1, h2);
-        layer3<1>(W, h2, q, false);
-        lossa = -q[0] / (float)B;
+    float lossa;
+    {
+        float q[1], d2m[kHH];
+        l1_row_half(W, xcr, hf, h1m);
+        if (act) store_half(S.h1 + s * kH, hf, h1m);
+        gather(h1m, hf, lo, hi);
+        l2_half(W, lo, hi, hf, h2m);
+        gather(h2m, hf, lo, hi);
+        l3_full<1>(W, lo, hi, q, false);
+        lossa = lead ? -q[0] / (float)B : 0.0f;
         const float d3[1] = {-1.0f / (float)B};
-        delta2<1>(W, d3, h2, d2);
-        delta1(W, d2, h1);  // h1 <- d1 of Q1
-        // dL/da = (W1^T d1)[28..31]
+        d2_half<1>(W, d3, h2m, hf, d2m);
+        load_half(S.h1 + sc * kH, hf, h1m);
+        d1_half(W, d2m, hf, h1m);  // h1m <- my half of Q1's d1
+        // dL/da = (W1^T d1)[28..31]: partial over my 32 rows of W1, pair-summed
+        const float* Wm = W.W1 + kHH * hf * kCI;
 #pragma unroll
-        for (int j = 0; j < kH; ++j) {
-            const float4 w = ld4(W.W1 + j * kCI + 28);
-            da[0] = fmaf(w.x, h1[j], da[0]);
-            da[1] = fmaf(w.y, h1[j], da[1]);
-            da[2] = fmaf(w.z, h1[j], da[2]);
-            da[3] = fmaf(w.w, h1[j], da[3]);
+        for (int j = 0; j < kHH; ++j) {
+            const float4 w = ld4(Wm + j * kCI + 28);
+            da[0] = fmaf(w.x, h1m[j], da[0]);
+            da[1] = fmaf(w.y, h1m[j], da[1]);
+            da[2] = fmaf(w.z, h1m[j], da[2]);
+            da[3] = fmaf(w.w, h1m[j], da[3]);
         }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) da[k] += __shfl_xor_sync(0xffffffffu, da[k], 1);
     }
     __syncthreads();
     W = stage(actor, wsm);
     __syncthreads();
-    if (act) {
-        float d3a[4], e2[kH];
+    {
+        float d3a[4], e2m[kHH];
 #pragma unroll
         for (int k = 0; k < 4; ++k) d3a[k] = da[k] * (1.0f - ap[k] * ap[k]);
-        load_row(S.ah2 + s * kH, h2);
-        delta2<4>(W, d3a, h2, e2);
-        store_row(S.ad2 + s * kH, e2);
-        load_row(S.ah1 + s * kH, h1);
-        delta1(W, e2, h1);  // h1 <- actor d1
-        store_row(S.ad1 + s * kH, h1);
-        *reinterpret_cast<float4*>(S.ad3 + s * 4) = make_float4(d3a[0], d3a[1], d3a[2], d3a[3]);
+        load_half(S.ah2 + sc * kH, hf, h2m);
+        d2_half<4>(W, d3a, h2m, hf, e2m);
+        if (act) store_half(S.ad2 + s * kH, hf, e2m);
+        load_half(S.ah1 + sc * kH, hf, h1m);
+        d1_half(W, e2m, hf, h1m);  // h1m <- my half of the actor's d1
+        if (act) store_half(S.ad1 + s * kH, hf, h1m);
+        if (lead) *reinterpret_cast<float4*>(S.ad3 + s * 4) = make_float4(d3a[0], d3a[1], d3a[2], d3a[3]);
     }
     const float loss = block_sum(lossa, red);
     if (threadIdx.x == 0) A.losses[ag * 3 + 2] = loss;
@@ -552,7 +618,7 @@ int64_t td3_scratch_bytes(int in_dim, int B) { return 4 * td3_scratch_floats(in_
 
 cudaError_t launch_td3_update(const TD3Dev& A, cudaStream_t s)
 {
-    if (A.B < 1 || A.B > kT || A.in_dim < 1 || A.in_dim > 256) return cudaErrorNotSupported;
+    if (A.B < 1 || A.B > kB || A.in_dim < 1 || A.in_dim > 256) return cudaErrorNotSupported;
     const size_t smem = td3_smem_bytes(A.in_dim, A.B);
     if (smem > 220 * 1024) return cudaErrorNotSupported;
     static bool attr = false;
