@@ -67,9 +67,13 @@ struct NetS {
     int in, ld1, out;
 };
 
+// Rows 32..63 of the staged W1 and W2 sit 4 floats further ("skew"), so the two threads of a
+// pair -- reading row j and row j + 32 at the same time -- hit different shared-memory banks.
+constexpr int kSkew = 4;
+
 __host__ __device__ constexpr int stage_floats(int in, int out)
 {
-    return kH * pad4(in) + kH + kH * kH + kH + out * kH + 4;
+    return kH * pad4(in) + kSkew + kH + kH * kH + kSkew + kH + out * kH + 4;
 }
 
 // CTA-cooperative copy of a net into shared memory at sm (16-byte aligned); caller syncs.
@@ -80,18 +84,18 @@ __device__ NetS stage(const NetP& n, float* sm)
     S.out = n.out;
     S.ld1 = pad4(n.in);
     S.W1 = sm;
-    S.b1 = S.W1 + kH * S.ld1;
+    S.b1 = S.W1 + kH * S.ld1 + kSkew;
     S.W2 = S.b1 + kH;
-    S.b2 = S.W2 + kH * kH;
+    S.b2 = S.W2 + kH * kH + kSkew;
     S.W3 = S.b2 + kH;
     S.b3 = S.W3 + n.out * kH;
 #pragma unroll 4
     for (int e = threadIdx.x; e < kH * S.ld1; e += blockDim.x) {
         const int j = e / S.ld1, i = e - j * S.ld1;
-        S.W1[e] = i < n.in ? n.W1[j * n.in + i] : 0.0f;
+        S.W1[e + (j >= kHH ? kSkew : 0)] = i < n.in ? n.W1[j * n.in + i] : 0.0f;
     }
 #pragma unroll 4
-    for (int e = threadIdx.x; e < kH * kH; e += blockDim.x) S.W2[e] = n.W2[e];
+    for (int e = threadIdx.x; e < kH * kH; e += blockDim.x) S.W2[e + (e >= kHH * kH ? kSkew : 0)] = n.W2[e];
     for (int e = threadIdx.x; e < n.out * kH; e += blockDim.x) S.W3[e] = n.W3[e];
     for (int e = threadIdx.x; e < kH; e += blockDim.x) {
         S.b1[e] = n.b1[e];
@@ -121,7 +125,7 @@ __device__ __forceinline__ void fma4(float& acc, float4 w, float4 x)
 // 16 outputs per pass over the row.
 __device__ __forceinline__ void l1_smem_half(const NetS& S, const float* x, int hf, float (&out)[kHH])
 {
-    const float* Wm = S.W1 + kHH * hf * S.ld1;
+    const float* Wm = S.W1 + kHH * hf * S.ld1 + kSkew * hf;
     const float* bm = S.b1 + kHH * hf;
 #pragma unroll
     for (int jb = 0; jb < kHH; jb += 16) {
@@ -151,7 +155,7 @@ __device__ __forceinline__ void l1_row_half(const NetS& S, const float* xrow, in
         x[c + 2] = v.z;
         x[c + 3] = v.w;
     }
-    const float* Wm = S.W1 + kHH * hf * kCI;
+    const float* Wm = S.W1 + kHH * hf * kCI + kSkew * hf;
     const float* bm = S.b1 + kHH * hf;
 #pragma unroll
     for (int j = 0; j < kHH; ++j) {
@@ -179,7 +183,7 @@ __device__ __forceinline__ void gather(const float (&mine)[kHH], int hf, float (
 __device__ __forceinline__ void l2_half(const NetS& S, const float (&lo)[kHH], const float (&hi)[kHH], int hf,
                                         float (&out)[kHH])
 {
-    const float* Wm = S.W2 + kHH * hf * kH;
+    const float* Wm = S.W2 + kHH * hf * kH + kSkew * hf;
     const float* bm = S.b2 + kHH * hf;
 #pragma unroll
     for (int j = 0; j < kHH; ++j) {
@@ -232,7 +236,7 @@ __device__ __forceinline__ void d2_half(const NetS& S, const float (&d3)[OUT], c
 // entry (the partner's partial of my half).
 __device__ __forceinline__ void d1_half(const NetS& S, const float (&d2m)[kHH], int hf, float (&h1d1m)[kHH])
 {
-    const float* Wm = S.W2 + kHH * hf * kH;
+    const float* Wm = S.W2 + kHH * hf * kH + kSkew * hf;
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
         float acc[kHH];
@@ -557,7 +561,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         load_half(S.h1 + sc * kH, hf, h1m);
         d1_half(W, d2m, hf, h1m);  // h1m <- my half of Q1's d1
         // dL/da = (W1^T d1)[28..31]: partial over my 32 rows of W1, pair-summed
-        const float* Wm = W.W1 + kHH * hf * kCI;
+        const float* Wm = W.W1 + kHH * hf * kCI + kSkew * hf;
 #pragma unroll
         for (int j = 0; j < kHH; ++j) {
             const float4 w = ld4(Wm + j * kCI + 28);
