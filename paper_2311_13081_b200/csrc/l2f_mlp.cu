@@ -62,28 +62,14 @@ constexpr uint32_t OFF_RTAB = (OFF_TMEM + 8 + 15) & ~15u;     // reset sampling 
 constexpr uint32_t OFF_STAT = (OFF_RTAB + 256 + 127) & ~127u;  // reset scratch (40 uint4 per warp); reused by stats
 constexpr uint32_t kScratchBytes = (kThreads / 32) * kResetScratch * 16;
 static_assert(kScratchBytes >= (kThreads / 32) * kStatsLen * 8, "stats rows fit in the scratch");
-// Warp-specialised observation noise (L2F_MLP_WS, rollout only): a fourth warpgroup draws the
-// next steps' observation-noise normals for all three tiles into a double-buffered TMEM stash
-// (producer warp q writes TMEM lane quarter q, the quarter env warp q of every tile reads),
-// handed over through per-(tile, buffer, quarter) ready/free mbarriers; setmaxnreg moves the
-// register file to the env warps (152) from the producers (56).  Measured 1 % slower than the
-// hooks (the fourth warp per scheduler stretches every other phase as much as it removes from
-// the hooks: the issue slots, not the latency, are what the noise costs), so off by default.
-#ifndef L2F_MLP_WS
-#define L2F_MLP_WS 0
-#endif
-constexpr bool kWS = L2F_MLP_WS != 0 && kE == 1;
-constexpr int kLaunchThreads = kThreads + (kWS ? 128 : 0);
-constexpr int kStashBufs = kWS ? 2 : 1;
-constexpr uint32_t OFF_NBAR = (OFF_STAT + kScratchBytes + 7) & ~7u;  // ready[kG][2][4], free[kG][2][4]
-constexpr uint32_t kSmemBytes = OFF_NBAR + (kWS ? 2 * kG * 2 * 4 * 8 : 0);
+constexpr uint32_t kSmemBytes = OFF_STAT + kScratchBytes;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 constexpr uint32_t kTmemCols = 512;
 // TMEM map: accumulators 64 columns per tile from 0; A2 (h1/h2 as fp16: 32 columns + 8 with the
 // ones column) 40 per tile from 64 kTiles; the per-env noise stash (18 used) 24 per tile after.
 constexpr uint32_t kA2Col = 64 * kTiles;
 constexpr uint32_t kStashCol = kA2Col + 40 * kTiles;
-static_assert(kStashCol + 24 * kTiles * kStashBufs <= kTmemCols, "TMEM budget");
+static_assert(kStashCol + 24 * kTiles <= kTmemCols, "TMEM budget");
 
 constexpr uint32_t kIdescN64 = tc::make_idesc(128, 64, 0, 0);
 constexpr uint32_t kIdescN64BMN = tc::make_idesc(128, 64, 0, 1);
@@ -330,19 +316,6 @@ __device__ __forceinline__ void load_obs_noise(const GroupCtx& c, int k, float z
     z[18] = z[19] = 0.0f;
 }
 
-__device__ __forceinline__ void load_obs_noise_at(uint32_t stash_row, float z[20])
-{
-    uint32_t v[16], w[4];
-    tc::tmem_ld16(stash_row, v);
-    tc::tmem_ld4(stash_row + 16, w);
-    tc::tmem_wait_ld();
-#pragma unroll
-    for (int j = 0; j < 16; ++j) z[j] = __uint_as_float(v[j]);
-    z[16] = __uint_as_float(w[0]);
-    z[17] = __uint_as_float(w[1]);
-    z[18] = z[19] = 0.0f;
-}
-
 __device__ __forceinline__ uint32_t a1_row(const GroupCtx& c, int k) { return c.a1_row + k * kA1Bytes; }
 
 __device__ __forceinline__ void write_obs_row(const GroupCtx& c, int k, const float o[kObsCore])
@@ -368,8 +341,6 @@ __device__ void setup_cta(const PolicyDev& W, uint32_t sbase, int n_hist, const 
     if (P) reset_table_to_smem(*P, reinterpret_cast<float4*>(smem + OFF_RTAB));
     if (threadIdx.x == 0) {
         for (int g = 0; g < kG; ++g) tc::mbar_init(sbase + OFF_BAR + 8 * g, 1);  // MMA done
-        if (kWS)
-            for (int b = 0; b < 2 * kG * 2 * 4; ++b) tc::mbar_init(sbase + OFF_NBAR + 8 * b, 1);  // noise ready / free
         tc::fence_mbar_init();
     }
     if (threadIdx.x < 32) tc::tmem_alloc(sbase + OFF_TMEM, kTmemCols);
@@ -415,62 +386,6 @@ __device__ __forceinline__ GroupCtx make_ctx(uint32_t sbase)
     return c;
 }
 
-__device__ __forceinline__ uint32_t nbar_ready(uint32_t sbase, int g, int b, int q)
-{
-    return sbase + OFF_NBAR + 8 * ((g * 2 + b) * 4 + q);
-}
-__device__ __forceinline__ uint32_t nbar_free(uint32_t sbase, int g, int b, int q)
-{
-    return sbase + OFF_NBAR + 8 * (kG * 2 * 4 + (g * 2 + b) * 4 + q);
-}
-
-// The noise-producer warpgroup (warps kThreads/32 .. +3): lane l of warp q serves env row
-// 32 q + l of every tile; for each group g it walks the same (unit, step) sequence as the
-// group and, one step ahead at most (two buffers), stashes the observation-noise normals of
-// step t (Philox stream OBS at counter t, Q20) for its row.
-__device__ void noise_producer(const DevParams& P, uint32_t sbase, int32_t T, int32_t n_units)
-{
-    extern __shared__ __align__(1024) uint8_t smem[];
-    const int q = (threadIdx.x >> 5) & 3, r = (threadIdx.x & 31) + 32 * q;
-    const uint32_t tbase = __shfl_sync(0xffffffffu, *reinterpret_cast<const uint32_t*>(smem + OFF_TMEM), 0);
-    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
-    uint32_t nstep[kG] = {};
-    for (int round = 0;; ++round) {
-        bool any = false;
-        int u[kG];
-#pragma unroll
-        for (int g = 0; g < kG; ++g) {
-            u[g] = blockIdx.x * kG + g + round * gridDim.x * kG;
-            any |= u[g] < n_units;
-        }
-        if (!any) break;
-        for (int32_t ks = 0; ks < T; ++ks) {
-            const uint32_t t = P.t0 + (uint32_t)ks;
-#pragma unroll 1
-            for (int g = 0; g < kG; ++g) {
-                if (u[g] >= n_units) continue;
-                const uint32_t gid = P.id_offset + (uint32_t)((int64_t)u[g] * kM + r);
-                const int b = nstep[g] & 1;
-                const uint32_t use = nstep[g] >> 1;
-                if (use > 0) {
-                    tc::mbar_wait(nbar_free(sbase, g, b, q), (use - 1) & 1);
-                    tc::fence_after();
-                }
-                float z[20];
-                obs_noise_blocks(P, gid, t, 0, 5, z);
-                const uint32_t row = tbase + lane_off + kStashCol + 24 * (kTiles * b + g);
-                tc::tmem_st8(row + 0, z, 0);
-                tc::tmem_st8(row + 8, z, 8);
-                tc::tmem_st2(row + 16, z[16], z[17]);
-                tc::tmem_wait_st();
-                tc::fence_before();
-                if ((threadIdx.x & 31) == 0) tc::mbar_arrive(nbar_ready(sbase, g, b, q));
-                ++nstep[g];
-            }
-        }
-    }
-}
-
 __device__ void teardown_cta()
 {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -486,7 +401,7 @@ __device__ void teardown_cta()
 // independent dependency chains (Philox, Box-Muller, RK4) interleave in the same basic blocks.
 // -------------------------------------------------------------------------------------------
 template <bool kDR>
-__global__ void __launch_bounds__(kLaunchThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     rollout_mlp_kernel(const DevParams P, const DevBufs B, const PolicyDev W, int32_t T, float* __restrict__ trace,
                        const int64_t* __restrict__ trace_ids, int32_t K, int32_t n_units)
 {
@@ -494,26 +409,15 @@ __global__ void __launch_bounds__(kLaunchThreads, 1)
     const uint32_t sbase = tc::smem_u32(smem);
     const int NH = P.n_hist;
     setup_cta(W, sbase, NH, &P);
-    StatAcc st;  // the warp's statistics (zero for the producer warps)
-    stat_zero(st);
-    double steps_done = 0.0;
-    if (kWS && threadIdx.x >= kThreads) {  // the noise-producer warpgroup
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
-        if (P.flags & F_OBS_NOISE) noise_producer(P, sbase, T, n_units);
-    } else {
-    if (kWS) asm volatile("setmaxnreg.inc.sync.aligned.u32 152;" ::: "memory");
     GroupCtx c = make_ctx(sbase);
     const int64_t N = P.n;
     const int r = threadIdx.x % kM;
     uint4* const rscratch = reinterpret_cast<uint4*>(smem + OFF_STAT) + (threadIdx.x >> 5) * kResetScratch;
     const float4* const rtab = reinterpret_cast<const float4*>(smem + OFF_RTAB);
+    StatAcc st;
+    stat_zero(st);
+    double steps_done = 0.0;
     const bool obs_noise = (P.flags & F_OBS_NOISE) != 0;
-    StatAcc sta;  // (env-branch accumulators, kept out of the producer's register budget)
-    stat_zero(sta);
-    double steps_env = 0.0;
-    const int gq = (threadIdx.x >> 5) & 3;  // this warp's TMEM lane quarter
-    const int grp = (int)(threadIdx.x / kM);
-    uint32_t nstep = 0;                      // steps consumed from the producer (WS)
 
     // unit u = tiles u kE .. u kE + kE - 1 (one per tile slot)
     for (int u = blockIdx.x * kG + (int)(threadIdx.x / kM); u < n_units; u += gridDim.x * kG) {
@@ -560,7 +464,7 @@ __global__ void __launch_bounds__(kLaunchThreads, 1)
             if (trace && active[k])
                 for (int q = 0; q < K; ++q)
                     if (trace_ids[q] == i[k]) tslot[k] = q;
-            if (!kWS && obs_noise) stash_obs_noise(P, c, k, gid[k], P.t0, 3);
+            if (obs_noise) stash_obs_noise(P, c, k, gid[k], P.t0, 3);
         }
         // ring rotation (t - 1) mod N_H and write position (-t) mod N_H, advanced incrementally
         uint32_t rot = NH > 0 ? (P.t0 + (uint32_t)NH - 1u) % (uint32_t)NH : 0u;
@@ -571,27 +475,15 @@ __global__ void __launch_bounds__(kLaunchThreads, 1)
         const StageW& W = P.stage[sg];
         for (const uint32_t t_stop = stage_stop(P, sg, t_last); t < t_stop; ++t) {
             const int32_t ks = (int32_t)(t - P.t0);
-            if (!kWS) tc::tmem_wait_st();  // the stashed noise of this step
+            tc::tmem_wait_st();  // the stashed noise of this step
 #pragma unroll
             for (int k = 0; k < kE; ++k) {
                 float ob[kObsCore];
                 float z[20];
-                if (obs_noise) {
-                    if (kWS) {  // the producer's buffer (nstep & 1) of this step
-                        const int bf = nstep & 1;
-                        tc::mbar_wait(nbar_ready(sbase, grp, bf, gq), (nstep >> 1) & 1);
-                        tc::fence_after();
-                        load_obs_noise_at(c.stash_row + 24 * kTiles * bf, z);
-                        tc::fence_before();
-                        if ((threadIdx.x & 31) == 0) tc::mbar_arrive(nbar_free(sbase, grp, bf, gq));
-                    } else {
-                        load_obs_noise(c, k, z);
-                    }
-                }
+                if (obs_noise) load_obs_noise(c, k, z);
                 observe_core_z(P, e[k].s, z, ob);
                 write_obs_row(c, k, ob);
             }
-            ++nstep;
             float a[kE][4], za[kE][4];
             // noise draws inside the MMA latency, unconditionally (no flag branch splits the
             // independent Philox chains into separate basic blocks; unused draws are discarded)
@@ -604,7 +496,7 @@ __global__ void __launch_bounds__(kLaunchThreads, 1)
 #pragma unroll
                         for (int q = 0; q < 4; ++q) za[k][q] = an ? za[k][q] : 0.0f;
                     }
-                    if (!kWS) stash_obs_noise(P, c, k, gid[k], t + 1, l - 1);
+                    stash_obs_noise(P, c, k, gid[k], t + 1, l - 1);
                 }
             });
             if (NH > 0 && ++rot == (uint32_t)NH) rot = 0;
@@ -632,7 +524,7 @@ __global__ void __launch_bounds__(kLaunchThreads, 1)
             for (int k = 0; k < kE; ++k) {
                 uint32_t fl = o[k].flags;
                 const bool ended = (fl & (D_TERM | D_TRUNC)) != 0;
-                if (ended && active[k]) stat_episode(sta, o[k]);
+                if (ended && active[k]) stat_episode(st, o[k]);
                 L2F_PHASE(c, 14);
                 bool did_reset = false;
                 float hf[4];
@@ -696,12 +588,9 @@ __global__ void __launch_bounds__(kLaunchThreads, 1)
                 B.hist[((int64_t)s * 4 + 2) * N + ik] = __low2float(y);
                 B.hist[((int64_t)s * 4 + 3) * N + ik] = __high2float(y);
             }
-            steps_env += (double)T;
+            steps_done += (double)T;
         }
     }
-    st = sta;
-    steps_done = steps_env;
-    }  // env groups
 #ifdef L2F_PHASE_TIMING
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -975,11 +864,9 @@ cudaError_t launch_rollout_mlp(const DevParams& P, const DevBufs& B, const Polic
     }
     const int n_units = (int)units_for(P.n);
     if (P.flags & F_DOMAIN_RAND)
-        rollout_mlp_kernel<true><<<grid_for(P.n), kLaunchThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K,
-                                                                                   n_units);
+        rollout_mlp_kernel<true><<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, n_units);
     else
-        rollout_mlp_kernel<false><<<grid_for(P.n), kLaunchThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K,
-                                                                                    n_units);
+        rollout_mlp_kernel<false><<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, n_units);
     return cudaGetLastError();
 }
 
