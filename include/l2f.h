@@ -315,6 +315,14 @@ L2F_API l2f_status l2f_td3_update(float* d_params, int32_t n_agents, int32_t in_
                                   int64_t t_actor, int32_t update_actor, float* d_losses, void* d_scratch,
                                   void* stream);
 
+/* The actor of agent `agent` of a TD3 parameter block array as the fp16 rollout policy:
+ * writes W1[64][in_dim], b1[64], W2[64][64], b2[64], W3[4][64], b3[4] (fp16 bits, round to
+ * nearest even) contiguously to d_out (caller-owned, 64 in_dim + 4420 halves) and fills *out
+ * with pointers into it, ready for l2f_rollout / l2f_policy_forward / l2f_track -- training
+ * and rollouts stay on the device.  Asynchronous on `stream`. */
+L2F_API l2f_status l2f_td3_export_actor(const float* d_params, int32_t agent, int32_t in_dim, uint16_t* d_out,
+                                        l2f_policy* out, void* stream);
+
 /* ---- state access --------------------------------------------------------------------- */
 
 L2F_API l2f_status l2f_get_state(l2f_env* env, l2f_state_view* out);

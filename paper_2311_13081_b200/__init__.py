@@ -320,6 +320,18 @@ class TD3:
         return {"q1": f[:, g0:g0 + self.nc], "q2": f[:, g0 + self.nc:g0 + 2 * self.nc],
                 "actor": f[:, g0 + 2 * self.nc:g0 + 2 * self.nc + self.na]}
 
+    def actor_policy(self, agent: int = 0, stream=None) -> "Policy":
+        """The agent's actor as a device fp16 Policy (l2f_td3_export_actor; no host round trip)."""
+        from .abi import PolicyS
+        pol = Policy.__new__(Policy)
+        buf = torch.empty(self.na, dtype=torch.int16, device=self.device)
+        pol.t = {"buf": buf}
+        pol.in_dim, pol.hidden = self.in_dim, 64
+        pol.s = PolicyS()
+        _check(lib().l2f_td3_export_actor(_ptr(self.params), int(agent), self.in_dim, _ptr(buf), C.byref(pol.s),
+                                          _stream(stream)), "l2f_td3_export_actor")
+        return pol
+
     def actor_policy_weights(self, agent: int = 0) -> dict:
         """The agent's actor as fp16 bit patterns in the l2f_policy layout (for Policy / rollouts)."""
         import numpy as np

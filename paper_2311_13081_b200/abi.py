@@ -12,7 +12,7 @@ STATE_DIM, OBS_CORE, MAX_HIST, STATS_LEN, TRACE_FIELDS = 17, 18, 32, 8, 32
 DONE_TERMINATED, DONE_TRUNCATED, DONE_DIVERGED, DONE_RESET = 1, 2, 4, 8
 STATS = ["episodes", "terminated", "truncated", "diverged", "sum_len", "sum_ret", "sum_ret_sq", "env_steps"]
 EXPORTS = ["l2f_workspace_size", "l2f_create", "l2f_destroy", "l2f_reset", "l2f_step", "l2f_rollout",
-           "l2f_episode_stats", "l2f_step_host", "l2f_rollout_host", "l2f_get_state", "l2f_set_t", "l2f_set_state", "l2f_track", "l2f_td3_sizes", "l2f_td3_update",
+           "l2f_episode_stats", "l2f_step_host", "l2f_rollout_host", "l2f_get_state", "l2f_set_t", "l2f_set_state", "l2f_track", "l2f_td3_sizes", "l2f_td3_update", "l2f_td3_export_actor",
            "l2f_policy_forward", "l2f_recompute_rewards", "l2f_selftest_philox", "l2f_launch_count", "l2f_last_error", "l2f_abi_version"]
 
 
@@ -157,6 +157,7 @@ def lib():
         L.l2f_set_state.argtypes = [vp, C.POINTER(StateView), vp]
         L.l2f_track.argtypes = [vp, vp, C.POINTER(Tracking), vp]
         L.l2f_td3_sizes.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.l2f_td3_export_actor.argtypes = [vp, C.c_int32, C.c_int32, vp, C.POINTER(PolicyS), vp]
         L.l2f_td3_update.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.POINTER(TD3Batch), C.POINTER(TD3Hyper),
                                      C.c_int64, C.c_int64, C.c_int32, vp, vp, vp]
         L.l2f_policy_forward.argtypes = [C.POINTER(PolicyS), vp, vp, C.c_int64, vp]

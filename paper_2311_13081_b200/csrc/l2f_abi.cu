@@ -544,6 +544,25 @@ l2f_status l2f_td3_update(float* d_params, int32_t n_agents, int32_t in_dim, int
     return launched(e, "l2f_td3_update");
 }
 
+l2f_status l2f_td3_export_actor(const float* d_params, int32_t agent, int32_t in_dim, uint16_t* d_out,
+                                l2f_policy* out, void* stream)
+{
+    if (!d_params || !d_out || !out || agent < 0 || in_dim < 1 || in_dim > 256)
+        return fail(L2F_ERR_INVALID_ARGUMENT, "bad td3_export_actor arguments");
+    const cudaError_t e = launch_td3_export_actor(d_params, td3_block_floats(in_dim), agent, in_dim, d_out,
+                                                  (cudaStream_t)stream);
+    const int64_t H = 64;
+    out->W1 = d_out;
+    out->b1 = out->W1 + H * in_dim;
+    out->W2 = out->b1 + H;
+    out->b2 = out->W2 + H * H;
+    out->W3 = out->b2 + H;
+    out->b3 = out->W3 + 4 * H;
+    out->in_dim = in_dim;
+    out->hidden = (int32_t)H;
+    return launched(e, "l2f_td3_export_actor");
+}
+
 l2f_status l2f_episode_stats(l2f_env* env, double* d_out, int32_t reset_accumulators, void* stream)
 {
     if (!env || !d_out) return fail(L2F_ERR_INVALID_ARGUMENT, "env/out is NULL");

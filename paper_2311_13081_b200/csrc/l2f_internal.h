@@ -71,5 +71,7 @@ struct TD3Dev {
 int64_t td3_block_floats(int in_dim);
 int64_t td3_scratch_bytes(int in_dim, int B);
 cudaError_t launch_td3_update(const TD3Dev& A, cudaStream_t s);
+cudaError_t launch_td3_export_actor(const float* params, int64_t block, int agent, int in_dim, uint16_t* out,
+                                    cudaStream_t s);
 
 }  // namespace l2f

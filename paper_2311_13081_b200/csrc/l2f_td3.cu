@@ -23,6 +23,8 @@
 // (L2-resident).
 #include <cmath>
 
+#include <cuda_fp16.h>
+
 #include "l2f_internal.h"
 
 namespace l2f {
@@ -616,6 +618,20 @@ size_t td3_smem_bytes(int in_dim, int B)
 }
 
 }  // namespace
+
+__global__ void td3_export_actor_kernel(const float* __restrict__ actor, int n, uint16_t* __restrict__ out)
+{
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        out[k] = __half_as_ushort(__float2half_rn(actor[k]));
+}
+
+cudaError_t launch_td3_export_actor(const float* params, int64_t block, int agent, int in_dim, uint16_t* out,
+                                    cudaStream_t s)
+{
+    const int n = net_size(in_dim, 4);
+    td3_export_actor_kernel<<<(n + 255) / 256, 256, 0, s>>>(params + (int64_t)agent * block, n, out);
+    return cudaGetLastError();
+}
 
 int64_t td3_block_floats(int in_dim) { return 4 * (int64_t)net_size(in_dim, 4) + 8 * (int64_t)net_size(kCI, 1); }
 int64_t td3_scratch_bytes(int in_dim, int B) { return 4 * td3_scratch_floats(in_dim, B); }

@@ -151,3 +151,19 @@ def test_td3_invalid_arguments(pkg):
         pkg.TD3(1, 146, 0)
     with pytest.raises(Exception):
         pkg.TD3(1, 146, 257)
+
+
+def test_td3_export_actor_on_device_matches_host_rounding(pkg):
+    """l2f_td3_export_actor == fp16 RNE of the actor block (numpy), and the exported policy
+    drives policy_forward identically to the host-converted one."""
+    td3 = pkg.TD3(3, 146, 32)
+    td3.params.copy_(torch.as_tensor(np.stack([init_block(td3, 20 + a) for a in range(3)])))
+    pol_dev = td3.actor_policy(agent=2)
+    W = td3.actor_policy_weights(2)
+    host = np.concatenate([W[k].ravel() for k in ("W1", "b1", "W2", "b2", "W3", "b3")])
+    dev = pol_dev.t["buf"].cpu().numpy().view(np.uint16)
+    assert np.array_equal(dev, host)
+    obs = torch.randn(1000, 146, device="cuda") * 0.3
+    a1 = pkg.policy_forward(pol_dev, obs)
+    a2 = pkg.policy_forward(pkg.Policy(W), obs)
+    assert torch.equal(a1, a2)
