@@ -10,8 +10,11 @@ reward + curriculum, termination, auto-reset and DR-free C5 physics, then the ep
 reduction and (N > 1) its NCCL all-reduce.  Workload (BASELINE configs[4], per GPU shard):
 2^21 envs per GPU x 1000 steps; at N = 8 this is exactly the 2^24-env C5 config; weak scaling.
 
-Prints ONE JSON line (rank 0).  Secondary measurements of the other configs (C3 single-step
-API against the HBM roofline, C4, the open-loop dynamics mode) ride along under "modes".
+Prints ONE JSON line (rank 0).  Secondary measurements ride along under "modes": the C3
+single-step API against the HBM roofline (and its host-buffer e2e), reward recalculation over
+a replay buffer (f2, HBM roofline), the open-loop dynamics-only mode next to the paper's
+figure, the C5 env step without the MLP, Lissajous tracking (f3) and the batched TD3 update
+(f4, FP32 roofline).
 """
 from __future__ import annotations
 
@@ -205,7 +208,7 @@ def main():
     ap.add_argument("--T", type=int, default=T_ROLLOUT)
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", default="mlp", choices=["mlp", "step", "open"])
+    ap.add_argument("--mode", default="mlp", choices=["mlp", "open"])  # open: Philox random actions, no MLP
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
