@@ -166,14 +166,19 @@ typedef struct {
 
 /* Borrowed device views into the env workspace (valid until l2f_destroy).  The caller may
  * read or overwrite them between calls (checkpoint / resume / set_state).  q is not
- * re-normalised on write (precondition ||q|| = 1). */
+ * re-normalised on write (precondition ||q|| = 1).
+ * Layout: structure of arrays of float4 groups plus a tail: for an array of C components,
+ * components c < 4 floor(C/4) of env i are float (c/4) N 4 + 4 i + c % 4 (a warp moves each
+ * group as 512 contiguous bytes, one 128-bit access per thread), and the C % 4 remaining
+ * components follow as an [N][C % 4] block.  Exactly 4 C N bytes, no padding. */
 typedef struct {
-    float* state;      /* [17][N] */
-    float* dist;       /* [6][N]  */
-    float* dr;         /* [5][N]  factors (1 when DR is off) */
-    float* hist;       /* [N_H][4][N] ring: slot (tau mod N_H) holds the action applied at step tau */
+    float* state;      /* C = 17: [4][N][4] (p, q(w,x,y,z), v, omega, omega_m 0..2) + [N] omega_m3 */
+    float* dist;       /* C = 6:  [1][N][4] (f_r world N, tau_x) + [N][2] (tau_y, tau_z) body N m */
+    float* dr;         /* C = 5:  [1][N][4] (m, J_xx, J_yy, J_zz factors) + [N] thrust factor;
+                          factors are 1 when DR is off */
+    float* hist;       /* [N_H][N][4] ring: slot (tau mod N_H) holds the action applied at step tau */
     int32_t* hist_t0;  /* [N] first step of the current episode */
-    float* hist_fill;  /* [4][N] the episode's initial history value (Q10)                      */
+    float* hist_fill;  /* [N][4] the episode's initial history value (Q10)                      */
                        /* Logical history at step t, H[k] (k-th most recent): tau = t-1-k;
                           H[k] = hist[tau mod N_H] if tau >= hist_t0 else hist_fill.  A reset
                           writes only hist_t0 / hist_fill (O(1) bytes per env, not N_H x 16).  */

@@ -105,14 +105,67 @@ class Env:
             esz = torch.empty(0, dtype=dtype).element_size()
             return self.ws[off: off + count * esz].view(dtype).view(*shape)
 
-        self.state = view(v.state, 17 * n, torch.float32, (17, n))
-        self.dist = view(v.dist, 6 * n, torch.float32, (6, n))
-        self.dr = view(v.dr, 5 * n, torch.float32, (5, n))
-        self.hist = view(v.hist, nh * 4 * n, torch.float32, (nh, 4, n))
+        # raw workspace views in the ABI layout (include/l2f.h): float4 groups + a tail block
+        self._grp = {}
+        for name, ptr, c in (("state", v.state, 17), ("dist", v.dist, 6), ("dr", v.dr, 5)):
+            self._grp[name] = (view(ptr, c * n, torch.float32, (c * n,)), c)
+        self.hist4 = view(v.hist, nh * 4 * n, torch.float32, (nh, n, 4))
         self.hist_t0 = view(v.hist_t0, n, torch.int32, (n,))
-        self.hist_fill = view(v.hist_fill, 4 * n, torch.float32, (4, n))
+        self.hist_fill4 = view(v.hist_fill, 4 * n, torch.float32, (n, 4))
         self.ep_step = view(v.ep_step, n, torch.int32, (n,))
         self.ep_return = view(v.ep_return, n, torch.float32, (n,))
+
+    def _g2l(self, name) -> torch.Tensor:  # raw grouped array -> [C][N] (copy)
+        flat, c = self._grp[name]
+        n, g, r = self.n, c // 4, c % 4
+        parts = [flat[:4 * g * n].view(g, n, 4).permute(0, 2, 1).reshape(4 * g, n)]
+        if r:
+            parts.append(flat[4 * g * n:].view(n, r).t())
+        return torch.cat(parts, 0).contiguous()
+
+    def raw(self, name) -> torch.Tensor:
+        """The flat workspace view of a grouped array (state / dist / dr), ABI layout."""
+        return self._grp[name][0]
+
+    @property
+    def state(self) -> torch.Tensor:
+        """[17][N] copy of the state (component-major)."""
+        return self._g2l("state")
+
+    @property
+    def dist(self) -> torch.Tensor:
+        return self._g2l("dist")
+
+    @property
+    def dr(self) -> torch.Tensor:
+        return self._g2l("dr")
+
+    @property
+    def hist(self) -> torch.Tensor:
+        """[N_H][4][N] copy of the action-history ring."""
+        return self.hist4.permute(0, 2, 1).contiguous()
+
+    @property
+    def hist_fill(self) -> torch.Tensor:
+        """[4][N] copy of the episodes' history fill values."""
+        return self.hist_fill4.t().contiguous()
+
+    def set_logical(self, name: str, value):
+        """Write a component-major array (as returned by the properties above) into the workspace."""
+        x = torch.as_tensor(value).to(device=self.device)
+        if name in self._grp:
+            flat, c = self._grp[name]
+            n, g, r = self.n, c // 4, c % 4
+            x = x.to(torch.float32)
+            flat[:4 * g * n].view(g, n, 4).copy_(x[:4 * g].reshape(g, 4, n).permute(0, 2, 1))
+            if r:
+                flat[4 * g * n:].view(n, r).copy_(x[4 * g:].t())
+        elif name == "hist":
+            self.hist4.copy_(x.to(torch.float32).permute(0, 2, 1))
+        elif name == "hist_fill":
+            self.hist_fill4.copy_(x.to(torch.float32).t())
+        else:
+            getattr(self, name).copy_(x)
 
     # -------------------------------------------------------------------------------
     @property
@@ -126,9 +179,10 @@ class Env:
         _check(lib().l2f_set_t(self.h, int(value)), "l2f_set_t")
 
     def get_state(self) -> dict:
-        """Copy of the full env state (device tensors) for checkpointing; see set_state."""
-        return {"state": self.state.clone(), "dist": self.dist.clone(), "dr": self.dr.clone(),
-                "hist": self.hist.clone(), "hist_t0": self.hist_t0.clone(), "hist_fill": self.hist_fill.clone(),
+        """Copy of the full env state (device tensors, the raw ABI layouts) for checkpointing;
+        see set_state."""
+        return {"state": self.raw("state").clone(), "dist": self.raw("dist").clone(), "dr": self.raw("dr").clone(),
+                "hist": self.hist4.clone(), "hist_t0": self.hist_t0.clone(), "hist_fill": self.hist_fill4.clone(),
                 "ep_step": self.ep_step.clone(), "ep_return": self.ep_return.clone(), "t": self.t}
 
     def set_state(self, snap: dict, stream=None):
@@ -154,8 +208,13 @@ class Env:
         v.ep_return = ptr("ep_return", torch.float32)
         v.t = int(snap.get("t", self.t))
         # sizes as the snapshot has them (the library rejects a mismatch before copying)
-        ns = {int(snap[k].shape[-1]) for k in ("state", "dist", "dr", "hist", "hist_t0", "hist_fill", "ep_step",
-                                                "ep_return") if snap.get(k) is not None}
+        per_env = {"state": 17, "dist": 6, "dr": 5}  # flat raw arrays: C x N floats
+        ns = set()
+        for k in ("state", "dist", "dr", "hist", "hist_fill", "hist_t0", "ep_step", "ep_return"):
+            x = snap.get(k)
+            if x is None:
+                continue
+            ns.add(int(x.numel() // per_env[k]) if k in per_env else int(x.shape[1] if k == "hist" else x.shape[0]))
         if len(ns) > 1:
             raise L2FError(f"set_state: inconsistent env counts {sorted(ns)}")
         v.num_envs = ns.pop() if ns else self.n

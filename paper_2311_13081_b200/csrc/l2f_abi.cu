@@ -64,7 +64,7 @@ Layout layout_for(const l2f_config& c)
         return at;
     };
     L.n_slots = n_slots_for(c.num_envs);
-    L.state = take(4 * N * L2F_STATE_DIM);
+    L.state = take(4 * N * L2F_STATE_DIM);  // float4 groups + tail (DevBufs): exact bytes
     L.dist = take(4 * N * L2F_DIST_DIM);
     L.dr = take(4 * N * L2F_DR_DIM);
     L.hist = take(4 * N * 4 * (size_t)(c.action_history > 0 ? c.action_history : 1));
@@ -341,12 +341,12 @@ l2f_status l2f_create(const l2f_config* cfg, void* d_workspace, size_t bytes, l2
     env->device = attr.device;
     env->L = L;
     env->ws = (uint8_t*)d_workspace;
-    env->B.state = (float*)(env->ws + L.state);
-    env->B.dist = (float*)(env->ws + L.dist);
-    env->B.dr = (float*)(env->ws + L.dr);
-    env->B.hist = (float*)(env->ws + L.hist);
+    env->B.state = (float4*)(env->ws + L.state);
+    env->B.dist = (float4*)(env->ws + L.dist);
+    env->B.dr = (float4*)(env->ws + L.dr);
+    env->B.hist = (float4*)(env->ws + L.hist);
     env->B.hist_t0 = (int32_t*)(env->ws + L.hist_t0);
-    env->B.hist_fill = (float*)(env->ws + L.hist_fill);
+    env->B.hist_fill = (float4*)(env->ws + L.hist_fill);
     env->B.ep_step = (int32_t*)(env->ws + L.ep_step);
     env->B.ep_return = (float*)(env->ws + L.ep_return);
     env->B.slots = (double*)(env->ws + L.slots);
@@ -643,12 +643,12 @@ l2f_status l2f_rollout_host(l2f_env* env, const l2f_policy* h_policy, int32_t T,
 l2f_status l2f_get_state(l2f_env* env, l2f_state_view* out)
 {
     if (!env || !out) return fail(L2F_ERR_INVALID_ARGUMENT, "env/out is NULL");
-    out->state = env->B.state;
-    out->dist = env->B.dist;
-    out->dr = env->B.dr;
-    out->hist = env->B.hist;
+    out->state = (float*)env->B.state;
+    out->dist = (float*)env->B.dist;
+    out->dr = (float*)env->B.dr;
+    out->hist = (float*)env->B.hist;
     out->hist_t0 = env->B.hist_t0;
-    out->hist_fill = env->B.hist_fill;
+    out->hist_fill = (float*)env->B.hist_fill;
     out->ep_step = env->B.ep_step;
     out->ep_return = env->B.ep_return;
     out->t = env->t;

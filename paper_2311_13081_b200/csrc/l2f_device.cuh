@@ -72,17 +72,18 @@ struct DevParams {
     StageW stage[kMaxStages];
 };
 
-// Workspace views (SoA, [C][N]).
+// Workspace views: structure of arrays of float4 groups plus a tail (grp_load): a warp moves each
+// group as 512 contiguous bytes with one 128-bit access per thread, and no byte is padding.
 struct DevBufs {
-    float* state;     // [17][N]
-    float* dist;      // [6][N]
-    float* dr;        // [5][N]
-    float* hist;      // [N_H][4][N] ring: slot (tau mod N_H) = action applied at step tau
-    int32_t* hist_t0; // [N] first step of the current episode: ring entries with tau < hist_t0
-    float* hist_fill; // [4][N]   read as hist_fill (the episode's initial history, Q10)
-    int32_t* ep_step; // [N]
-    float* ep_return; // [N]
-    double* slots;    // [n_slots][8] per-block statistics partials
+    float4* state;     // [4][N] float4 (p, q, v, w, w_m0..2) + [N] float (w_m3)
+    float4* dist;      // [1][N] float4 (f_r, tau_x) + [N] float2 (tau_y, tau_z)
+    float4* dr;        // [1][N] float4 (m, J_xx, J_yy, J_zz) + [N] float (thrust scale)
+    float4* hist;      // [N_H][N] ring: slot (tau mod N_H) = action applied at step tau
+    int32_t* hist_t0;  // [N] first step of the current episode: ring entries with tau < hist_t0
+    float4* hist_fill; // [N]   read as hist_fill (the episode's initial history, Q10)
+    int32_t* ep_step;  // [N]
+    float* ep_return;  // [N]
+    double* slots;     // [n_slots][8] per-block statistics partials
     int32_t n_slots;
 };
 
@@ -314,6 +315,40 @@ __device__ __forceinline__ void deriv(const DevParams& P, const Phys& ph, const 
     dy[4] = (txy.x - cx) * ph.iJx;
     dy[5] = (txy.y - cy) * ph.iJy;
     dy[6] = (tz - cz) * ph.iJz;
+}
+
+// Float4-group SoA (DevBufs): components 0 .. 4 floor(C/4) - 1 of env i as float4 groups
+// (element (c/4) N + i, lane c % 4), the C % 4 tail components as one float / float2 element
+// i of an [N] array right after the groups.  Exact bytes (no padding), one 128-bit access per
+// group and one 32/64-bit access for the tail.
+template <int C>
+__device__ __forceinline__ void grp_load(const float4* base, int64_t i, int64_t N, float* out)
+{
+    constexpr int G = C / 4, R = C % 4;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const float4 v = base[g * N + i];
+        out[4 * g] = v.x, out[4 * g + 1] = v.y, out[4 * g + 2] = v.z, out[4 * g + 3] = v.w;
+    }
+    if constexpr (R == 1) {
+        out[4 * G] = reinterpret_cast<const float*>(base + G * N)[i];
+    } else if constexpr (R == 2) {
+        const float2 v = reinterpret_cast<const float2*>(base + G * N)[i];
+        out[4 * G] = v.x, out[4 * G + 1] = v.y;
+    }
+    static_assert(R < 3, "tail of 0, 1 or 2 components");
+}
+template <int C>
+__device__ __forceinline__ void grp_store(float4* base, int64_t i, int64_t N, const float* v)
+{
+    constexpr int G = C / 4, R = C % 4;
+#pragma unroll
+    for (int g = 0; g < G; ++g) base[g * N + i] = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+    if constexpr (R == 1) {
+        reinterpret_cast<float*>(base + G * N)[i] = v[4 * G];
+    } else if constexpr (R == 2) {
+        reinterpret_cast<float2*>(base + G * N)[i] = make_float2(v[4 * G], v[4 * G + 1]);
+    }
 }
 
 // SoA walkers: rows c = 0..C-1 of column i of a [C][N] array, visited in order with one
@@ -781,11 +816,11 @@ __device__ __forceinline__ void hist_entry(const DevBufs& B, int64_t N, int n_hi
     const int64_t tau = t - 1 - k;
     if (tau >= (int64_t)t0) {
         const int slot = (int)(((tau % n_hist) + n_hist) % n_hist);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) h[c] = B.hist[((int64_t)slot * 4 + c) * N + i];
+        const float4 v = B.hist[(int64_t)slot * N + i];
+        h[0] = v.x, h[1] = v.y, h[2] = v.z, h[3] = v.w;
     } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) h[c] = B.hist_fill[(int64_t)c * N + i];
+        const float4 v = B.hist_fill[i];
+        h[0] = v.x, h[1] = v.y, h[2] = v.z, h[3] = v.w;
     }
 }
 

@@ -19,11 +19,10 @@ namespace l2f {
 template <bool kDR>
 __device__ __forceinline__ void load_env(const DevParams& P, const DevBufs& B, int64_t i, EnvReg& e)
 {
-    const uint32_t n = (uint32_t)P.n;
-    soa_load<kStateDim>(B.state, i, n, e.s);
-    soa_load<6>(B.dist, i, n, e.dist);
+    grp_load<kStateDim>(B.state, i, P.n, e.s);
+    grp_load<6>(B.dist, i, P.n, e.dist);
     if (kDR) {
-        soa_load<5>(B.dr, i, n, e.dr);
+        grp_load<5>(B.dr, i, P.n, e.dr);
     } else {
 #pragma unroll
         for (int c = 0; c < 5; ++c) e.dr[c] = 1.0f;
@@ -48,7 +47,7 @@ __device__ __forceinline__ void dummy_env(EnvReg& e)
 
 __device__ __forceinline__ void store_state(const DevParams& P, const DevBufs& B, int64_t i, const EnvReg& e)
 {
-    soa_store<kStateDim>(B.state, i, (uint32_t)P.n, e.s);
+    grp_store<kStateDim>(B.state, i, P.n, e.s);
     B.ep_step[i] = e.ep_step;
     B.ep_return[i] = e.ep_return;
 }
@@ -57,9 +56,8 @@ __device__ __forceinline__ void store_state(const DevParams& P, const DevBufs& B
 __device__ __forceinline__ void store_episode_consts(const DevParams& P, const DevBufs& B, int64_t i,
                                                      const EnvReg& e)
 {
-    const uint32_t n = (uint32_t)P.n;
-    soa_store<6>(B.dist, i, n, e.dist);
-    if (P.flags & F_DOMAIN_RAND) soa_store<5>(B.dr, i, n, e.dr);
+    grp_store<6>(B.dist, i, P.n, e.dist);
+    if (P.flags & F_DOMAIN_RAND) grp_store<5>(B.dr, i, P.n, e.dr);
 }
 
 // A new episode starting at step t0: O(1) bytes (marker + fill value), the ring itself is
@@ -68,7 +66,7 @@ __device__ __forceinline__ void hist_restart(const DevParams& P, const DevBufs& 
                                              const float h[4])
 {
     B.hist_t0[i] = (int32_t)t0;
-    soa_store<4>(B.hist_fill, i, (uint32_t)P.n, h);
+    B.hist_fill[i] = make_float4(h[0], h[1], h[2], h[3]);
 }
 
 // Dense actor observation row [18 + 4 N_H]: obs_core then H most-recent-first at
@@ -155,7 +153,7 @@ __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const D
     if (active) {
         if (P.n_hist > 0) {
             const int slot = P.hist_slot0;  // t0 mod N_H (written for every env: deterministic ring)
-            soa_store<4>(B.hist + (int64_t)slot * 4 * N, i, (uint32_t)N, o.a);
+            B.hist[(int64_t)slot * N + i] = make_float4(o.a[0], o.a[1], o.a[2], o.a[3]);
             if (did_reset) hist_restart(P, B, i, t + 1, hf);
         }
         store_state(P, B, i, e);
@@ -195,10 +193,8 @@ __global__ void __launch_bounds__(kStepBlock) reset_kernel(const DevParams P, co
     reset_env(P, e, gid, P.t0, hf);
     store_state(P, B, i, e);
     const int64_t NN = N;
-#pragma unroll
-    for (int c = 0; c < 6; ++c) B.dist[c * NN + i] = e.dist[c];
-#pragma unroll
-    for (int c = 0; c < 5; ++c) B.dr[c * NN + i] = e.dr[c];
+    grp_store<6>(B.dist, i, NN, e.dist);
+    grp_store<5>(B.dr, i, NN, e.dr);
     if (P.n_hist > 0) hist_restart(P, B, i, P.t0, hf);
     if (O.obs_core || O.obs_dense) {
         float ob[kObsCore];
@@ -285,8 +281,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
             e.ep_return = 0.0f;
         }
         if (active && P.n_hist > 0) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) B.hist[((int64_t)slot * 4 + c) * N + i] = o.a[c];
+            B.hist[(int64_t)slot * N + i] = make_float4(o.a[0], o.a[1], o.a[2], o.a[3]);
             if (did_reset) hist_restart(P, B, i, t + 1, hf);
         }
         if (++slot == P.n_hist) slot = 0;

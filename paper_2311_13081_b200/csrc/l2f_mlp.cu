@@ -432,12 +432,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             active[k] = i[k] < N;
             gid[k] = P.id_offset + (uint32_t)i[k];
             if (active[k]) {
+                grp_load<kStateDim>(B.state, i[k], N, e[k].s);
+                grp_load<6>(B.dist, i[k], N, e[k].dist);
+                if (kDR)
+                    grp_load<5>(B.dr, i[k], N, e[k].dr);
+                else
 #pragma unroll
-                for (int q = 0; q < kStateDim; ++q) e[k].s[q] = B.state[q * N + i[k]];
-#pragma unroll
-                for (int q = 0; q < 6; ++q) e[k].dist[q] = B.dist[q * N + i[k]];
-#pragma unroll
-                for (int q = 0; q < 5; ++q) e[k].dr[q] = kDR ? B.dr[q * N + i[k]] : 1.0f;
+                    for (int q = 0; q < 5; ++q) e[k].dr[q] = 1.0f;
                 e[k].ep_step = B.ep_step[i[k]];
                 e[k].ep_return = B.ep_return[i[k]];
             } else {
@@ -568,13 +569,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < kE; ++k) {
             if (!active[k]) continue;
             const int64_t ik = i[k];
-#pragma unroll
-            for (int q = 0; q < kStateDim; ++q) B.state[q * N + ik] = e[k].s[q];
-#pragma unroll
-            for (int q = 0; q < 6; ++q) B.dist[q * N + ik] = e[k].dist[q];
-            if (kDR)
-#pragma unroll
-                for (int q = 0; q < 5; ++q) B.dr[q * N + ik] = e[k].dr[q];
+            grp_store<kStateDim>(B.state, ik, N, e[k].s);
+            grp_store<6>(B.dist, ik, N, e[k].dist);
+            if (kDR) grp_store<5>(B.dr, ik, N, e[k].dr);
             B.ep_step[ik] = e[k].ep_step;
             B.ep_return[ik] = e[k].ep_return;
             // the ring now holds the full logical history: every entry valid
@@ -583,10 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t h01, h23;
                 tc::lds64(hist_addr(c, k, (NH - s) % NH), h01, h23);
                 const __half2 x = *reinterpret_cast<__half2*>(&h01), y = *reinterpret_cast<__half2*>(&h23);
-                B.hist[((int64_t)s * 4 + 0) * N + ik] = __low2float(x);
-                B.hist[((int64_t)s * 4 + 1) * N + ik] = __high2float(x);
-                B.hist[((int64_t)s * 4 + 2) * N + ik] = __low2float(y);
-                B.hist[((int64_t)s * 4 + 3) * N + ik] = __high2float(y);
+                B.hist[(int64_t)s * N + ik] = make_float4(__low2float(x), __high2float(x), __low2float(y), __high2float(y));
             }
             steps_done += (double)T;
         }
@@ -791,28 +785,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             S.rmse_xy[ik] = ok[k] > 0 ? (float)sqrt(sexy[k] / ok[k]) : 0.0f;
             S.steps_ok[ik] = ok[k];
             // the env is left in the final tracking state (history ring complete, as after a rollout)
-#pragma unroll
-            for (int q = 0; q < kStateDim; ++q) B.state[q * N + ik] = e[k].s[q];
-#pragma unroll
-            for (int q = 0; q < 6; ++q) B.dist[q * N + ik] = 0.0f;
-#pragma unroll
-            for (int q = 0; q < 5; ++q) B.dr[q * N + ik] = 1.0f;
+            grp_store<kStateDim>(B.state, ik, N, e[k].s);
+            grp_store<6>(B.dist, ik, N, e[k].dist);
+            grp_store<5>(B.dr, ik, N, e[k].dr);
             B.ep_step[ik] = ok[k];
             B.ep_return[ik] = 0.0f;
             if (NH > 0) {
                 const int32_t t_end = (int32_t)(P.t0 + (uint32_t)S.n_steps);
                 B.hist_t0[ik] = t_end - NH;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) B.hist_fill[(int64_t)q * N + ik] = S.hover_a;
+                B.hist_fill[ik] = make_float4(S.hover_a, S.hover_a, S.hover_a, S.hover_a);
             }
             for (int sl = 0; sl < NH; ++sl) {
                 uint32_t h01, h23;
                 tc::lds64(hist_addr(c, k, (NH - sl) % NH), h01, h23);
                 const __half2 x = *reinterpret_cast<__half2*>(&h01), y = *reinterpret_cast<__half2*>(&h23);
-                B.hist[((int64_t)sl * 4 + 0) * N + ik] = __low2float(x);
-                B.hist[((int64_t)sl * 4 + 1) * N + ik] = __high2float(x);
-                B.hist[((int64_t)sl * 4 + 2) * N + ik] = __low2float(y);
-                B.hist[((int64_t)sl * 4 + 3) * N + ik] = __high2float(y);
+                B.hist[(int64_t)sl * N + ik] = make_float4(__low2float(x), __high2float(x), __low2float(y), __high2float(y));
             }
         }
     }

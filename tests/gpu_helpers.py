@@ -47,7 +47,7 @@ def snapshot(env) -> dict:
 
 def load_snapshot(env, snap: dict):
     for k, v in snap.items():
-        getattr(env, k).copy_(torch.as_tensor(v))
+        env.set_logical(k, v)
     torch.cuda.synchronize()
 
 

@@ -67,8 +67,9 @@ def test_workspace_size_and_validation(L):
     n = 1 << 20
     st, b, _ = _size(L, cfg, n)
     assert st == 0
-    # state 68 + dist 24 + dr 20 + hist 512 + counters 8 + staging (16 + 72 + 4 + 1) B per env
-    assert 725 * n <= b <= 760 * n
+    # state 68 + dist 24 + dr 20 + hist 512 + fill 16 + counters 12 + staging
+    # (16 + 72 + 4 + 1) B per env
+    assert 740 * n <= b <= 770 * n
     assert _size(L, cfg, 0)[0] == 1
     assert _size(L, cfg, 10, off=(1 << 32) - 5)[0] == 1
     assert _size(L, inputs.config_c3(n_hist=33), 10)[0] == 1
