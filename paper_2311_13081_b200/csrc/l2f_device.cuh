@@ -338,6 +338,19 @@ __device__ __forceinline__ void grp_load(const float4* base, int64_t i, int64_t 
     }
     static_assert(R < 3, "tail of 0, 1 or 2 components");
 }
+// Scalar-access variant of grp_load (same layout): for kernels that read a state once, where
+// 128-bit register quads only constrain the allocator of the hot loop that follows.
+template <int C>
+__device__ __forceinline__ void grp_load_scalar(const float4* base4, int64_t i, int64_t N, float* out)
+{
+    constexpr int G = C / 4, R = C % 4;
+    const float* base = reinterpret_cast<const float*>(base4);
+#pragma unroll
+    for (int c = 0; c < 4 * G; ++c) out[c] = base[((c / 4) * N + i) * 4 + (c % 4)];
+#pragma unroll
+    for (int c = 0; c < R; ++c) out[4 * G + c] = base[4 * G * N + i * R + c];
+}
+
 template <int C>
 __device__ __forceinline__ void grp_store(float4* base, int64_t i, int64_t N, const float* v)
 {

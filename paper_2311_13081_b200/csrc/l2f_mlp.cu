@@ -432,10 +432,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             active[k] = i[k] < N;
             gid[k] = P.id_offset + (uint32_t)i[k];
             if (active[k]) {
-                grp_load<kStateDim>(B.state, i[k], N, e[k].s);
-                grp_load<6>(B.dist, i[k], N, e[k].dist);
+                grp_load_scalar<kStateDim>(B.state, i[k], N, e[k].s);
+                grp_load_scalar<6>(B.dist, i[k], N, e[k].dist);
                 if (kDR)
-                    grp_load<5>(B.dr, i[k], N, e[k].dr);
+                    grp_load_scalar<5>(B.dr, i[k], N, e[k].dr);
                 else
 #pragma unroll
                     for (int q = 0; q < 5; ++q) e[k].dr[q] = 1.0f;
