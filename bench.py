@@ -47,6 +47,9 @@ MLP_FLOPS = 2 * (146 * 64 + 64 * 64 + 64 * 4)
 ALU_OPS_PER_ENV_STEP = 1071
 #  open-loop rollout with Philox random actions (no observation, no MLP)
 ALU_OPS_PER_ENV_STEP_OPEN = 657
+#  the same with every feature off (C1 flags 0: no noise, termination, reset): random action 56,
+#  clip + RPM map 12, RK4 428, reward/termination/counters 32, history + statistics 4
+ALU_OPS_PER_ENV_STEP_DYN = 532
 SMS = 148
 
 
@@ -437,9 +440,14 @@ def secondary(pkg, inputs, torch, dev, pk, f_clk):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     rate = n * 1000 / (ms / 1e3)
+    alu = SMS * 128 * f_clk / 1e12
     out["open_loop_dynamics"] = {"value": rate, "unit": "env-steps/s", "ms": ms,
                                  "workload": "2^20 envs x 1000 steps, Philox random actions, no noise/termination",
-                                 "vs_paper_T2000": rate / 1.284e9}
+                                 "vs_paper_T2000": rate / 1.284e9,
+                                 "roofline": {"bound": "alu", "achieved": ALU_OPS_PER_ENV_STEP_DYN * rate / 1e12,
+                                              "peak": alu, "unit": "Tops/s",
+                                              "frac": ALU_OPS_PER_ENV_STEP_DYN * rate / 1e12 / alu,
+                                              "ops_per_env_step": ALU_OPS_PER_ENV_STEP_DYN}}
     del env
     # the full C5 env step without the actor MLP (Philox random actions), for the MLP's share
     n = 1 << 21
