@@ -39,10 +39,16 @@ def close_obs(gpu_obs, ref_obs, s_prev):
     return close_step(gpu_obs, ref_obs, prev)
 
 
-def snapshot(env) -> dict:
+def snapshot(env, cols=None) -> dict:
+    """Component-major copies of the env arrays; cols: only these env columns (full-size runs)."""
     torch.cuda.synchronize()
-    return {k: getattr(env, k).detach().cpu().numpy().copy()
-            for k in ("state", "dist", "dr", "hist", "hist_t0", "hist_fill", "ep_step", "ep_return")}
+    out = {}
+    for k in ("state", "dist", "dr", "hist", "hist_t0", "hist_fill", "ep_step", "ep_return"):
+        x = getattr(env, k).detach()
+        if cols is not None:
+            x = x[..., torch.as_tensor(np.asarray(cols), device=x.device)]
+        out[k] = x.cpu().numpy().copy()
+    return out
 
 
 def load_snapshot(env, snap: dict):

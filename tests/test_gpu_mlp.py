@@ -73,19 +73,21 @@ def _teacher_forced(pkg, cfg, n, T, K, t0=0, seed=7, check_every=1):
     env = pkg.Env(cfg, n)
     env.reset()
     env.t = t0
-    snap0 = snapshot(env)
     ids = inputs.trace_ids(n, K, seed=3)
+    full = n <= 1 << 14  # large runs: snapshots of the sampled columns only
+    snap0 = snapshot(env) if full else snapshot(env, ids)
     tr = env.rollout(T, policy=pol, trace_ids=torch.as_tensor(ids)).cpu().numpy()
-    after = snapshot(env)
+    after = snapshot(env) if full else snapshot(env, ids)
     n_checked = n_excl = 0
     worst = 0.0
     for j, i in enumerate(ids):
+        c = i if full else j  # column of env i in the snapshots
         e = oracle.new_envs(1)
-        e[0]["dist"] = snap0["dist"][:, i]
-        e[0]["dr"] = snap0["dr"][:, i]
-        H = list(logical_hist(snap0, i, t0, nh)) if nh else []
-        ep = int(snap0["ep_step"][i])
-        ret = float(snap0["ep_return"][i])
+        e[0]["dist"] = snap0["dist"][:, c]
+        e[0]["dr"] = snap0["dr"][:, c]
+        H = list(logical_hist(snap0, c, t0, nh)) if nh else []
+        ep = int(snap0["ep_step"][c])
+        ret = float(snap0["ep_return"][c])
         for k in range(T):
             t = t0 + k
             rec = tr[k, j]
@@ -112,7 +114,7 @@ def _teacher_forced(pkg, cfg, n, T, K, t0=0, seed=7, check_every=1):
             assert int(rec[26]) == so.flags or abs(min(so.margin, key=abs)) < 1e-4, (j, k, rec[26], so.flags)
             if int(rec[26]) != so.flags:
                 break  # near-threshold flip (Q22): stop following this env
-            nxt = tr[k + 1, j, :17] if k + 1 < T else after["state"][:, i]
+            nxt = tr[k + 1, j, :17] if k + 1 < T else after["state"][:, c]
             ref_next = e[0]["s"]
             prev = rec[:17] if not (so.flags & oracle.FLAG_RESET) else ref_next
             assert np.all(close_step(nxt, ref_next, prev)), (j, k, nxt - ref_next)
@@ -129,6 +131,17 @@ def test_mlp_rollout_teacher_forced_c4(pkg):
     cfg = inputs.config_c4()
     n_checked, n_excl, worst, _, _, _ = _teacher_forced(pkg, cfg, n=2000, T=60, K=48)
     assert n_checked > 1000
+    assert worst <= 1e-4, worst
+
+
+def test_mlp_rollout_full_size_c5_shard_sampled(pkg):
+    """The bench's launch configuration: the C5 per-GPU shard (2^21 envs) in one rollout
+    launch with a curriculum boundary inside, checked teacher-forced on 40 sampled envs spread
+    over the whole batch (full sizes on sampled outputs)."""
+    cfg = inputs.config_c5()
+    cfg["curriculum"]["interval"] = 12
+    n_checked, _, worst, _, _, _ = _teacher_forced(pkg, cfg, n=1 << 21, T=25, K=40, t0=5)
+    assert n_checked > 800
     assert worst <= 1e-4, worst
 
 

@@ -167,3 +167,23 @@ def test_td3_export_actor_on_device_matches_host_rounding(pkg):
     a1 = pkg.policy_forward(pol_dev, obs)
     a2 = pkg.policy_forward(pkg.Policy(W), obs)
     assert torch.equal(a1, a2)
+
+
+def test_td3_bench_configuration_sampled(pkg):
+    """The bench's configuration (148 agents x batch 256 x in_dim 146, one CTA per SM): three
+    sampled agents' losses and critic/actor gradients vs the oracle."""
+    A, B, I = 148, 256, 146
+    td3 = pkg.TD3(A, I, B)
+    blocks = np.stack([init_block(td3, 50 + (a % 7)) for a in range(A)])
+    td3.params.copy_(torch.as_tensor(blocks))
+    bt = make_batch(A, B, I, 77)
+    losses = td3.update({k: torch.as_tensor(v) for k, v in bt.items()}, update_actor=True).cpu().numpy()
+    gg = {k: v.cpu().numpy() for k, v in td3.grads().items()}
+    for a in (0, 73, 147):
+        P = blocks[a].astype(np.float64)
+        lo, go = oracle.td3_update(P, I, {k: v[a].astype(np.float64) for k, v in bt.items()}, td3.hyper,
+                                   update_actor=True, want_grads=True)
+        assert np.allclose(losses[a], lo, rtol=2e-4, atol=1e-6)
+        nc = td3.nc
+        for name, ref in (("q1", go[:nc]), ("q2", go[nc:2 * nc]), ("actor", go[2 * nc:])):
+            assert np.abs(gg[name][a] - ref).max() <= 1e-4 * np.abs(ref).max() + 1e-7, (a, name)

@@ -130,3 +130,19 @@ def test_track_tiny_runs_match_oracle(pkg, n, steps):
     for i in (0, n - 1):
         orr, _, ook, _ = oracle.track(cfg, ph, i, 0, 5.5, steps)
         assert ok[i] == ook and abs(r[i] - orr) <= 1e-4 + 1e-3 * orr
+
+
+def test_track_full_size_sampled(pkg):
+    """The bench's tracking configuration (2^20 envs, Table III cycle times), sampled envs vs
+    the oracle with the deterministic zero actor (no chaos: tight agreement)."""
+    cfg = inputs.config_c4()
+    n, steps = 1 << 20, 120
+    W = zero_policy()
+    env = pkg.Env(cfg, n)
+    T = cycle_times(n)
+    out = env.track(pkg.Policy(W), torch.as_tensor(T, device="cuda"), steps)
+    r, ok = out["rmse"].cpu().numpy(), out["steps_ok"].cpu().numpy()
+    ph = oracle.PolicyHandle(W)
+    for i in inputs.trace_ids(n, 12, seed=9):
+        orr, _, ook, _ = oracle.track(cfg, ph, int(i), 0, float(T[i]), steps)
+        assert ok[i] == ook and abs(r[i] - orr) <= 1e-5 + 1e-4 * orr, (i, r[i], orr, ok[i], ook)
