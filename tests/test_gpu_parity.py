@@ -466,3 +466,30 @@ def test_recompute_rewards_bitwise_and_vs_oracle(pkg):
     for j in range(0, s_np.shape[1], 97):
         ref = oracle.recompute_reward(cfg, later, s_np[:, j], a_np[:, j])
         assert close(r2[j], ref, abs_=1e-5), (j, r2[j], ref)
+
+
+@pytest.mark.gpu
+def test_rollout_split_across_many_curriculum_stages(pkg):
+    """More curriculum stages in one rollout than a launch carries (kMaxStages = 8): the
+    rollout is split into several launches and stays bitwise equal to T single steps, with
+    per-step rewards following the stage schedule."""
+    cfg = inputs.config_c2()
+    cfg["curriculum"]["interval"] = 2  # a new stage every second step
+    n, T = 1000, 30
+    acts = inputs.actions_near_hover(T, n, seed=21)
+    A = dev_actions(acts)
+    e1 = pkg.Env(cfg, n)
+    e1.reset()
+    rew = []
+    for k in range(T):
+        o = e1.make_out(obs_core=False, reward=True, flags=False)
+        e1.step(A[k].contiguous(), o)
+        rew.append(o["reward"].cpu().numpy())
+    e2 = pkg.Env(cfg, n)
+    e2.reset()
+    tr = e2.rollout(T, actions=A, trace_ids=torch.arange(0, n, 97)).cpu().numpy()
+    s1, s2 = snapshot(e1), snapshot(e2)
+    for k in s1:
+        assert np.array_equal(s1[k], s2[k]), k
+    for j, i in enumerate(range(0, n, 97)):
+        assert np.array_equal(tr[:, j, 25], np.array([r[i] for r in rew], dtype=np.float32)), i
