@@ -22,6 +22,7 @@
 // per sample.  Per-sample rows the weight gradients need go to a per-agent global scratch
 // (L2-resident).
 #include <cmath>
+#include <cstdio>
 
 #include <cuda_fp16.h>
 
@@ -73,6 +74,19 @@ struct NetS {
 // pair -- reading row j and row j + 32 at the same time -- hit different shared-memory banks.
 constexpr int kSkew = 4;
 
+// Debug build only (-DL2F_TD3_TIMING): CTA-0 thread-0 clock() at phase boundaries, printed.
+#ifdef L2F_TD3_TIMING
+#define TD3_MARK(k)                                              \
+    do {                                                         \
+        __syncthreads();                                         \
+        if (blockIdx.x == 0 && threadIdx.x == 0) mark[k] = clock64(); \
+    } while (0)
+#else
+#define TD3_MARK(k) \
+    do {            \
+    } while (0)
+#endif
+
 __host__ __device__ constexpr int stage_floats(int in, int out)
 {
     return kH * pad4(in) + kSkew + kH + kH * kH + kSkew + kH + out * kH + 4;
@@ -91,10 +105,10 @@ __device__ NetS stage(const NetP& n, float* sm)
     S.b2 = S.W2 + kH * kH + kSkew;
     S.W3 = S.b2 + kH;
     S.b3 = S.W3 + n.out * kH;
-#pragma unroll 4
-    for (int e = threadIdx.x; e < kH * S.ld1; e += blockDim.x) {
-        const int j = e / S.ld1, i = e - j * S.ld1;
-        S.W1[e + (j >= kHH ? kSkew : 0)] = i < n.in ? n.W1[j * n.in + i] : 0.0f;
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int j = threadIdx.x >> 5; j < kH; j += nw) {  // a warp per row: no division, coalesced
+        float* dst = S.W1 + j * S.ld1 + (j >= kHH ? kSkew : 0);
+        for (int i = lane; i < S.ld1; i += 32) dst[i] = i < n.in ? n.W1[j * n.in + i] : 0.0f;
     }
 #pragma unroll 4
     for (int e = threadIdx.x; e < kH * kH; e += blockDim.x) S.W2[e + (e >= kHH * kH ? kSkew : 0)] = n.W2[e];
@@ -108,6 +122,19 @@ __device__ NetS stage(const NetP& n, float* sm)
 }
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+// Input rows [B][I] (global) -> shared [B][LI] zero-padded, a warp per row (coalesced, no
+// per-element division).
+__device__ __forceinline__ void stage_rows(const float* src, int B, int I, int LI, float* dst)
+{
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int r = threadIdx.x >> 5; r < B; r += nw) {
+        const float* s = src + (int64_t)r * I;
+        float* d = dst + r * LI;
+#pragma unroll 2
+        for (int i = lane; i < LI; i += 32) d[i] = i < I ? s[i] : 0.0f;
+    }
+}
 
 // Compiler scheduling fence: keeps the fully unrolled 64-wide loops from hoisting hundreds of
 // shared-memory loads ahead (which spills), without emitting an instruction.
@@ -434,12 +461,12 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     float* const xt = S.d1 + sc * kH;  // target-critic input row (o_c', a'): S.d1 is free until phase 2
     float* const xcr = S.xc + sc * kCI;  // critic input row (o_c, a)
 
+#ifdef L2F_TD3_TIMING
+    long long mark[16] = {};
+#endif
+    TD3_MARK(0);
     // ---- 1. target: a' = clip(pi'(o_a') + clip(sigma eps, -c, c), -1, 1); y = r + g (1-d) min Q'
-#pragma unroll 4
-    for (int e = threadIdx.x; e < B * LI; e += blockDim.x) {
-        const int r = e / LI, i = e - r * LI;
-        xs[e] = i < I ? A.o_a2[((int64_t)ag * B + r) * I + i] : 0.0f;
-    }
+    stage_rows(A.o_a2 + (int64_t)ag * B * I, B, I, LI, xs);
     NetS W = stage(actor_t, wsm);
     __syncthreads();
     {
@@ -488,6 +515,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     }
     __syncwarp();
 
+    TD3_MARK(1);
     // ---- 2. critics: MSE to y, Adam
     const AdamC Ac{A.lr_critic, A.beta1, A.beta2, A.c1_critic, A.c2_critic, A.adam_eps};
     for (int c = 0; c < 2; ++c) {
@@ -515,11 +543,14 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         __syncthreads();
         float* g = c == 0 ? S.gq1 : S.gq2;
         NetP gn = net_at(g, kCI, 1);
+        TD3_MARK(2 + 3 * c);
         grad_layer(S.d1, kH, S.xc, kCI, B, kH, kCI, gn.W1, gn.b1);
         grad_layer(S.d2, kH, S.h1, kH, B, kH, kH, gn.W2, gn.b2);
         grad_layer(S.d3, 1, S.h2, kH, B, 1, kH, gn.W3, gn.b3);
         __syncthreads();
+        TD3_MARK(3 + 3 * c);
         adam(Q[c].W1, m_c[c], v_c[c], g, nc, Ac);
+        TD3_MARK(4 + 3 * c);
     }
     if (!A.update_actor) {
         if (threadIdx.x == 0) A.losses[ag * 3 + 2] = 0.0f;
@@ -528,11 +559,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
 
     // ---- 3. actor: ascend Q1(o_c, pi(o_a)) through the updated Q1's action input, Adam
     __syncthreads();
-#pragma unroll 4
-    for (int e = threadIdx.x; e < B * LI; e += blockDim.x) {
-        const int r = e / LI, i = e - r * LI;
-        xs[e] = i < I ? A.o_a[((int64_t)ag * B + r) * I + i] : 0.0f;
-    }
+    stage_rows(A.o_a + (int64_t)ag * B * I, B, I, LI, xs);
     W = stage(actor, wsm);
     __syncthreads();
     float ap[4];
@@ -594,12 +621,15 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     if (threadIdx.x == 0) A.losses[ag * 3 + 2] = loss;
     __syncthreads();
     NetP ga = net_at(S.ga, I, 4);
+    TD3_MARK(8);
     grad_layer(S.ad1, kH, xs, LI, B, kH, I, ga.W1, ga.b1);
     grad_layer(S.ad2, kH, S.ah1, kH, B, kH, kH, ga.W2, ga.b2);
     grad_layer(S.ad3, 4, S.ah2, kH, B, 4, kH, ga.W3, ga.b3);
     __syncthreads();
     const AdamC Aa{A.lr_actor, A.beta1, A.beta2, A.c1_actor, A.c2_actor, A.adam_eps};
+    TD3_MARK(9);
     adam(actor.W1, m_a, v_a, S.ga, na, Aa);
+    TD3_MARK(10);
     __syncthreads();
     // ---- 4. Polyak averaging of the three targets
     const float tau = A.tau;
@@ -609,6 +639,16 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     for (int c = 0; c < 2; ++c)
 #pragma unroll 4
         for (int k = threadIdx.x; k < nc; k += blockDim.x) Qt[c].W1[k] = fmaf(tau, Q[c].W1[k], (1.0f - tau) * Qt[c].W1[k]);
+    TD3_MARK(11);
+#ifdef L2F_TD3_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        printf("L2F_TD3 target %lld critic0 fwdbwd %lld grads %lld adam %lld critic1 fwdbwd %lld grads %lld adam %lld "
+               "actor fwdbwd %lld grads %lld adam %lld polyak %lld total %lld\n",
+               mark[1] - mark[0], mark[2] - mark[1], mark[3] - mark[2], mark[4] - mark[3], mark[5] - mark[4],
+               mark[6] - mark[5], mark[7] - mark[6], mark[8] - mark[7], mark[9] - mark[8], mark[10] - mark[9],
+               mark[11] - mark[10], mark[11] - mark[0]);
+    }
+#endif
 }
 
 size_t td3_smem_bytes(int in_dim, int B)
