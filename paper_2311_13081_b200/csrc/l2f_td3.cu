@@ -105,13 +105,41 @@ __device__ NetS stage(const NetP& n, float* sm)
     S.b2 = S.W2 + kH * kH + kSkew;
     S.W3 = S.b2 + kH;
     S.b3 = S.W3 + n.out * kH;
+    // All loads of a batch are issued before its stores (the global source may not alias the
+    // shared destination, but the compiler cannot prove it): 8 loads in flight per thread.
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int j = threadIdx.x >> 5; j < kH; j += nw) {  // a warp per row: no division, coalesced
-        float* dst = S.W1 + j * S.ld1 + (j >= kHH ? kSkew : 0);
-        for (int i = lane; i < S.ld1; i += 32) dst[i] = i < n.in ? n.W1[j * n.in + i] : 0.0f;
+    for (int j0 = threadIdx.x >> 5; j0 < kH; j0 += 2 * nw) {  // a warp per row, two rows at a time
+        for (int i0 = lane; i0 < S.ld1; i0 += 128) {
+            float t[2][4];
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + r * nw, i = i0 + 32 * u;
+                    t[r][u] = (j < kH && i < n.in) ? __ldg(n.W1 + j * n.in + i) : 0.0f;
+                }
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + r * nw, i = i0 + 32 * u;
+                    if (j < kH && i < S.ld1) S.W1[j * S.ld1 + (j >= kHH ? kSkew : 0) + i] = t[r][u];
+                }
+        }
     }
-#pragma unroll 4
-    for (int e = threadIdx.x; e < kH * kH; e += blockDim.x) S.W2[e + (e >= kHH * kH ? kSkew : 0)] = n.W2[e];
+    for (int e0 = threadIdx.x; e0 < kH * kH; e0 += 8 * blockDim.x) {
+        float t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * blockDim.x;
+            t[u] = e < kH * kH ? __ldg(n.W2 + e) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < kH * kH) S.W2[e + (e >= kHH * kH ? kSkew : 0)] = t[u];
+        }
+    }
     for (int e = threadIdx.x; e < n.out * kH; e += blockDim.x) S.W3[e] = n.W3[e];
     for (int e = threadIdx.x; e < kH; e += blockDim.x) {
         S.b1[e] = n.b1[e];
@@ -128,11 +156,24 @@ __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast
 __device__ __forceinline__ void stage_rows(const float* src, int B, int I, int LI, float* dst)
 {
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int r = threadIdx.x >> 5; r < B; r += nw) {
-        const float* s = src + (int64_t)r * I;
-        float* d = dst + r * LI;
-#pragma unroll 2
-        for (int i = lane; i < LI; i += 32) d[i] = i < I ? s[i] : 0.0f;
+    for (int r0 = threadIdx.x >> 5; r0 < B; r0 += 2 * nw) {  // two rows x 4 chunks per batch
+        for (int i0 = lane; i0 < LI; i0 += 128) {
+            float t[2][4];
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int r = r0 + q * nw, i = i0 + 32 * u;
+                    t[q][u] = (r < B && i < I) ? __ldg(src + (int64_t)r * I + i) : 0.0f;
+                }
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int r = r0 + q * nw, i = i0 + 32 * u;
+                    if (r < B && i < LI) dst[r * LI + i] = t[q][u];
+                }
+        }
     }
 }
 
@@ -309,49 +350,82 @@ __device__ __forceinline__ void load_half(const float* row, int hf, float (&v)[k
     }
 }
 
-// Weight gradient of one layer, reduced over the batch: gW[j][i] = sum_s D[s][j] X[s][i] (gW
-// row stride K, unpadded: the parameter layout), gb[j] = sum_s D[s][j].  CTA-cooperative,
-// 4 x 4 register tiles; D rows (ldd) and X rows (ldx) 16-byte aligned, ldx >= pad4(K) with
-// zero padding.
-__device__ void grad_layer(const float* D, int ldd, const float* X, int ldx, int B, int N, int K, float* gW,
-                           float* gb)
+// Weight gradients of a net's three layers, reduced over the batch: gW[j][i] = sum_s D[s][j]
+// X[s][i] (gW row stride K, unpadded: the parameter layout), gb[j] = sum_s D[s][j].
+// CTA-cooperative over one tile space holding every layer's 4 x 4 output tiles and ceil(N/4)
+// bias tiles (so the three layers and the biases run concurrently, one thread per tile).
+// Adjacent threads take adjacent tiles of a row block: their X loads of a sample are
+// contiguous, their D loads one broadcast.  D rows (ldd) and X rows (ldx) 16-byte aligned, ldx
+// >= pad4(K) with zero padding; N % 4 == 0 or N == 1.
+struct GradL {
+    const float* D;
+    const float* X;
+    float *gW, *gb;
+    int ldd, ldx, N, K;
+};
+
+__device__ void grad_layers(const GradL (&L)[3], int B)
 {
-    const int tj = (N + 3) / 4, ti = (K + 3) / 4;
-    for (int tile = threadIdx.x; tile < tj * ti; tile += blockDim.x) {
-        const int j0 = (tile / ti) * 4, i0 = (tile % ti) * 4;
-        float acc[4][4] = {};
-        if (N % 4 == 0) {
-#pragma unroll 8
-            for (int s = 0; s < B; ++s) {
-                const float4 d = ld4(D + s * ldd + j0), x = ld4(X + s * ldx + i0);
-                const float dv[4] = {d.x, d.y, d.z, d.w}, xv[4] = {x.x, x.y, x.z, x.w};
+    int cnt[3], tot = 0;
 #pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(dv[a], xv[b], acc[a][b]);
-            }
-        } else {  // N = 1 (the critic's output layer)
-#pragma unroll 8
-            for (int s = 0; s < B; ++s) {
-                const float d = D[s * ldd + j0];
-                const float4 x = ld4(X + s * ldx + i0);
-                acc[0][0] = fmaf(d, x.x, acc[0][0]);
-                acc[0][1] = fmaf(d, x.y, acc[0][1]);
-                acc[0][2] = fmaf(d, x.z, acc[0][2]);
-                acc[0][3] = fmaf(d, x.w, acc[0][3]);
-            }
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if (j0 + a < N && i0 + b < K) gW[(j0 + a) * K + i0 + b] = acc[a][b];
+    for (int l = 0; l < 3; ++l) {
+        const int tj = (L[l].N + 3) / 4, ti = (L[l].K + 3) / 4;
+        cnt[l] = tj * ti + tj;
+        tot += cnt[l];
     }
-    for (int j = threadIdx.x; j < N; j += blockDim.x) {
-        float acc = 0.0f;
+    for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+        const int l = t < cnt[0] ? 0 : (t < cnt[0] + cnt[1] ? 1 : 2);
+        const int tile = t - (l > 0 ? cnt[0] : 0) - (l > 1 ? cnt[1] : 0);
+        const GradL G = L[l];
+        const int ti = (G.K + 3) / 4, nw = ((G.N + 3) / 4) * ti;
+        float acc[4][4] = {};
+        if (tile < nw) {
+            const int j0 = (tile / ti) * 4, i0 = (tile % ti) * 4;
+            if (G.N % 4 == 0) {
 #pragma unroll 8
-        for (int s = 0; s < B; ++s) acc += D[s * ldd + j];
-        gb[j] = acc;
+                for (int s = 0; s < B; ++s) {
+                    const float4 d = ld4(G.D + s * G.ldd + j0), x = ld4(G.X + s * G.ldx + i0);
+                    const float dv[4] = {d.x, d.y, d.z, d.w}, xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(dv[a], xv[b], acc[a][b]);
+                }
+            } else {  // N = 1 (the critic's output layer)
+#pragma unroll 8
+                for (int s = 0; s < B; ++s) {
+                    const float d = G.D[s * G.ldd];
+                    const float4 x = ld4(G.X + s * G.ldx + i0);
+                    acc[0][0] = fmaf(d, x.x, acc[0][0]);
+                    acc[0][1] = fmaf(d, x.y, acc[0][1]);
+                    acc[0][2] = fmaf(d, x.z, acc[0][2]);
+                    acc[0][3] = fmaf(d, x.w, acc[0][3]);
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    if (j0 + a < G.N && i0 + b < G.K) G.gW[(j0 + a) * G.K + i0 + b] = acc[a][b];
+        } else {  // bias tile: row sums of D
+            const int j0 = (tile - nw) * 4;
+            if (G.N % 4 == 0) {
+#pragma unroll 8
+                for (int s = 0; s < B; ++s) {
+                    const float4 d = ld4(G.D + s * G.ldd + j0);
+                    acc[0][0] += d.x;
+                    acc[1][0] += d.y;
+                    acc[2][0] += d.z;
+                    acc[3][0] += d.w;
+                }
+            } else {
+#pragma unroll 8
+                for (int s = 0; s < B; ++s) acc[0][0] += G.D[s * G.ldd];
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+                if (j0 + a < G.N) G.gb[j0 + a] = acc[a][0];
+        }
     }
 }
 
@@ -359,16 +433,37 @@ struct AdamC {
     float lr, b1, b2, c1, c2, eps;  // c1 = 1 - beta1^t, c2 = 1 - beta2^t
 };
 
-__device__ void adam(float* th, float* m, float* v, const float* g, int n, const AdamC& A)
+// Adam on n parameters; with tgt != nullptr also the Polyak step of the matching target net,
+// tgt <- tau theta_new + (1 - tau) tgt (the same arithmetic as a separate pass after Adam).
+// Four elements per thread per batch, all loads issued before the stores.
+__device__ void adam(float* th, float* m, float* v, const float* g, int n, const AdamC& A, float* tgt, float tau)
 {
-#pragma unroll 4
-    for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        const float gk = g[k];
-        const float mk = fmaf(A.b1, m[k], (1.0f - A.b1) * gk);
-        const float vk = fmaf(A.b2, v[k], (1.0f - A.b2) * gk * gk);
-        m[k] = mk;
-        v[k] = vk;
-        th[k] -= A.lr * (mk / A.c1) / (sqrtf(vk / A.c2) + A.eps);
+    const int T = blockDim.x;
+    for (int k0 = threadIdx.x; k0 < n; k0 += 4 * T) {
+        float gk[4], mk[4], vk[4], tk[4], pk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = k0 + u * T;
+            const bool in = k < n;
+            gk[u] = in ? g[k] : 0.0f;
+            mk[u] = in ? m[k] : 0.0f;
+            vk[u] = in ? v[k] : 0.0f;
+            tk[u] = in ? th[k] : 0.0f;
+            pk[u] = (in && tgt) ? tgt[k] : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = k0 + u * T;
+            if (k < n) {
+                const float mn = fmaf(A.b1, mk[u], (1.0f - A.b1) * gk[u]);
+                const float vn = fmaf(A.b2, vk[u], (1.0f - A.b2) * gk[u] * gk[u]);
+                const float tn = tk[u] - A.lr * (mn / A.c1) / (sqrtf(vn / A.c2) + A.eps);
+                m[k] = mn;
+                v[k] = vn;
+                th[k] = tn;
+                if (tgt) tgt[k] = fmaf(tau, tn, (1.0f - tau) * pk[u]);
+            }
+        }
     }
 }
 
@@ -544,12 +639,13 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         float* g = c == 0 ? S.gq1 : S.gq2;
         NetP gn = net_at(g, kCI, 1);
         TD3_MARK(2 + 3 * c);
-        grad_layer(S.d1, kH, S.xc, kCI, B, kH, kCI, gn.W1, gn.b1);
-        grad_layer(S.d2, kH, S.h1, kH, B, kH, kH, gn.W2, gn.b2);
-        grad_layer(S.d3, 1, S.h2, kH, B, 1, kH, gn.W3, gn.b3);
+        const GradL gl[3] = {{S.d1, S.xc, gn.W1, gn.b1, kH, kCI, kH, kCI},
+                             {S.d2, S.h1, gn.W2, gn.b2, kH, kH, kH, kH},
+                             {S.d3, S.h2, gn.W3, gn.b3, 1, kH, 1, kH}};
+        grad_layers(gl, B);
         __syncthreads();
         TD3_MARK(3 + 3 * c);
-        adam(Q[c].W1, m_c[c], v_c[c], g, nc, Ac);
+        adam(Q[c].W1, m_c[c], v_c[c], g, nc, Ac, A.update_actor ? Qt[c].W1 : nullptr, A.tau);  // (+ Polyak)
         TD3_MARK(4 + 3 * c);
     }
     if (!A.update_actor) {
@@ -622,23 +718,15 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     __syncthreads();
     NetP ga = net_at(S.ga, I, 4);
     TD3_MARK(8);
-    grad_layer(S.ad1, kH, xs, LI, B, kH, I, ga.W1, ga.b1);
-    grad_layer(S.ad2, kH, S.ah1, kH, B, kH, kH, ga.W2, ga.b2);
-    grad_layer(S.ad3, 4, S.ah2, kH, B, 4, kH, ga.W3, ga.b3);
+    const GradL gl[3] = {{S.ad1, xs, ga.W1, ga.b1, kH, LI, kH, I},
+                         {S.ad2, S.ah1, ga.W2, ga.b2, kH, kH, kH, kH},
+                         {S.ad3, S.ah2, ga.W3, ga.b3, 4, kH, 4, kH}};
+    grad_layers(gl, B);
     __syncthreads();
     const AdamC Aa{A.lr_actor, A.beta1, A.beta2, A.c1_actor, A.c2_actor, A.adam_eps};
     TD3_MARK(9);
-    adam(actor.W1, m_a, v_a, S.ga, na, Aa);
+    adam(actor.W1, m_a, v_a, S.ga, na, Aa, actor_t.W1, A.tau);  // ---- 4. with the actor target's Polyak step
     TD3_MARK(10);
-    __syncthreads();
-    // ---- 4. Polyak averaging of the three targets
-    const float tau = A.tau;
-#pragma unroll 4
-    for (int k = threadIdx.x; k < na; k += blockDim.x)
-        actor_t.W1[k] = fmaf(tau, actor.W1[k], (1.0f - tau) * actor_t.W1[k]);
-    for (int c = 0; c < 2; ++c)
-#pragma unroll 4
-        for (int k = threadIdx.x; k < nc; k += blockDim.x) Qt[c].W1[k] = fmaf(tau, Q[c].W1[k], (1.0f - tau) * Qt[c].W1[k]);
     TD3_MARK(11);
 #ifdef L2F_TD3_TIMING
     if (blockIdx.x == 0 && threadIdx.x == 0) {
