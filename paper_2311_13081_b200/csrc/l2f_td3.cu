@@ -564,6 +564,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     stage_rows(A.o_a2 + (int64_t)ag * B * I, B, I, LI, xs);
     NetS W = stage(actor_t, wsm);
     __syncthreads();
+    TD3_MARK(12);
     {
         float at[4];
         l1_smem_half(W, xs + sc * LI, hf, h1m);
@@ -586,6 +587,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         }
     }
     __syncwarp();
+    TD3_MARK(13);
     float qmin = 0.0f;
     for (int c = 0; c < 2; ++c) {
         __syncthreads();
@@ -658,6 +660,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     stage_rows(A.o_a + (int64_t)ag * B * I, B, I, LI, xs);
     W = stage(actor, wsm);
     __syncthreads();
+    TD3_MARK(14);
     float ap[4];
     l1_smem_half(W, xs + sc * LI, hf, h1m);
     if (act) store_half(S.ah1 + s * kH, hf, h1m);
@@ -667,6 +670,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     gather(h2m, hf, lo, hi);
     l3_full<4>(W, lo, hi, ap, true);
     if (act && hf == 1) *reinterpret_cast<float4*>(xcr + 28) = make_float4(ap[0], ap[1], ap[2], ap[3]);  // (o_c, pi(o_a))
+    TD3_MARK(15);
     __syncthreads();
     W = stage(Q[0], wsm);  // the updated Q1
     __syncthreads();
@@ -735,6 +739,9 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
                mark[1] - mark[0], mark[2] - mark[1], mark[3] - mark[2], mark[4] - mark[3], mark[5] - mark[4],
                mark[6] - mark[5], mark[7] - mark[6], mark[8] - mark[7], mark[9] - mark[8], mark[10] - mark[9],
                mark[11] - mark[10], mark[11] - mark[0]);
+        printf("L2F_TD3 target: stage %lld actor fwd %lld critics %lld; actor: stage %lld fwd %lld rest %lld\n",
+               mark[12] - mark[0], mark[13] - mark[12], mark[1] - mark[13], mark[14] - mark[7], mark[15] - mark[14],
+               mark[8] - mark[15]);
     }
 #endif
 }
