@@ -303,7 +303,8 @@ typedef struct {
  * (FP32): [actor, actor', Q1, Q2, Q1', Q2', m_actor, v_actor, m_Q1, v_Q1, m_Q2, v_Q2]; each
  * net is W1[64][in], b1[64], W2[64][64], b2[64], W3[out][64], b3[out] with the actor
  * in_dim -> 4 (ReLU, ReLU, tanh) and the critics 32 -> 1 (ReLU, ReLU, linear) on
- * concat(o_c, a).  INVALID_ARGUMENT unless 1 <= batch <= 256 and 1 <= in_dim <= 256. */
+ * concat(o_c, a).  INVALID_ARGUMENT unless 1 <= batch <= 256 and 1 <= in_dim <= 156 (the
+ * paper's largest observation, N_H = 32, is 146; the bound is the kernel's shared-memory plan). */
 L2F_API l2f_status l2f_td3_sizes(int32_t in_dim, int32_t batch, int64_t* block_floats,
                                  int64_t* scratch_bytes_per_agent);
 

@@ -486,8 +486,8 @@ l2f_status l2f_track(l2f_env* env, const l2f_policy* policy, const l2f_tracking*
 
 l2f_status l2f_td3_sizes(int32_t in_dim, int32_t batch, int64_t* block_floats, int64_t* scratch_bytes_per_agent)
 {
-    if (in_dim < 1 || in_dim > 256 || batch < 1 || batch > 256)
-        return fail(L2F_ERR_INVALID_ARGUMENT, "TD3 needs 1 <= in_dim <= 256 and 1 <= batch <= 256");
+    if (in_dim < 1 || in_dim > td3_max_in_dim() || batch < 1 || batch > 256)
+        return fail(L2F_ERR_INVALID_ARGUMENT, "TD3 needs 1 <= in_dim <= 156 and 1 <= batch <= 256");
     if (block_floats) *block_floats = td3_block_floats(in_dim);
     if (scratch_bytes_per_agent) *scratch_bytes_per_agent = td3_scratch_bytes(in_dim, batch);
     return L2F_OK;

@@ -60,7 +60,7 @@ struct TrackDev {
 cudaError_t launch_track_mlp(const DevParams& P, const DevBufs& B, const PolicyDev& W, const TrackDev& S,
                              cudaStream_t s);
 
-// Batched TD3 update (l2f_td3.cu): one CTA per agent, one thread per sample.
+// Batched TD3 update (l2f_td3.cu): one CTA per agent, CTA-wide batch GEMMs.
 struct TD3Dev {
     float* params;          // [A][block] flat FP32 blocks (td3_block_floats)
     float* scratch;         // [A][scratch_floats]
@@ -71,6 +71,7 @@ struct TD3Dev {
     float gamma, tau, sigma_t, clip_t, lr_actor, lr_critic, beta1, beta2, adam_eps;
     float c1_critic, c2_critic, c1_actor, c2_actor;  // Adam bias corrections 1 - beta^t
 };
+int td3_max_in_dim();
 int64_t td3_block_floats(int in_dim);
 int64_t td3_scratch_bytes(int in_dim, int B);
 cudaError_t launch_td3_update(const TD3Dev& A, cudaStream_t s);
