@@ -23,7 +23,8 @@
 // shared-memory bound).  Backward deltas are the same GEMM against W2 (in place, masked by
 // ReLU'), weight gradients 8 x 4 tiles reduced over a warp's sample range with the partial
 // sums of the ranges combined by the Adam pass (deterministic order).  The actor input rows
-// (in_dim floats) are read straight from global memory by the GEMMs (each row by one warp).
+// (in_dim floats, the one operand that does not fit) are staged in column parts with cp.async
+// into the activation buffers that are free at that point.
 #include <cmath>
 #include <cstdio>
 
@@ -116,34 +117,49 @@ struct XSm {  // a swizzled shared-memory activation buffer
     int ld;
     __device__ __forceinline__ float4 operator()(int s, int c4) const { return ld4(p + sw(s, c4, ld)); }
 };
-struct XGl {  // batch input rows [B][I] in global memory (read-only): zero beyond I, rows clamped
+struct XSp {  // a plain shared-memory row buffer (row stride ld floats, 16-byte aligned rows)
     const float* p;
-    int I, B;
-    __device__ __forceinline__ float4 operator()(int s, int c4) const
-    {
-        const float* r = p + (int64_t)min(s, B - 1) * I;
-        const int k = 4 * c4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (!(I & 1)) {  // rows 8-byte aligned
-            if (k + 2 <= I) {
-                const float2 a = __ldg(reinterpret_cast<const float2*>(r + k));
-                v.x = a.x;
-                v.y = a.y;
-            }
-            if (k + 4 <= I) {
-                const float2 b = __ldg(reinterpret_cast<const float2*>(r + k + 2));
-                v.z = b.x;
-                v.w = b.y;
-            }
-        } else {
-            if (k < I) v.x = __ldg(r + k);
-            if (k + 1 < I) v.y = __ldg(r + k + 1);
-            if (k + 2 < I) v.z = __ldg(r + k + 2);
-            if (k + 3 < I) v.w = __ldg(r + k + 3);
-        }
-        return v;
-    }
+    int ld;
+    __device__ __forceinline__ float4 operator()(int s, int c4) const { return ld4(p + s * ld + 4 * c4); }
 };
+
+// The actor input is consumed in column parts of up to kPW floats (kPW / 16 = 5 gradient
+// column blocks), staged in shared memory rows of kPLd floats (21 float4s: four consecutive
+// rows hit four different bank groups).
+constexpr int kPW = 80;
+constexpr int kPLd = 84;
+
+__device__ __forceinline__ void cp_async(float* dst, const float* src, int bytes_total, int bytes_src)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    if (bytes_total == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(bytes_src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(bytes_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Columns [k0, k0 + w) of the batch rows X [B][I] (global) -> dst [B][kPLd] with cp.async
+// (all copies in flight at once), zero beyond I; a warp per row.  Caller waits + syncs.
+__device__ void stage_cols(const float* X, int B, int I, int k0, int w, float* dst)
+{
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (!(I & 1)) {  // 8-byte pieces (I even: rows 8-byte aligned)
+        const int np = (w + 1) >> 1;
+        for (int r = threadIdx.x >> 5; r < B; r += nw)
+            for (int q = lane; q < np; q += 32) {
+                const int k = k0 + 2 * q;
+                const int b = k + 2 <= I ? 8 : (k < I ? 4 : 0);
+                cp_async(dst + r * kPLd + 2 * q, X + (int64_t)r * I + (b ? k : 0), 8, b);
+            }
+    } else {
+        for (int r = threadIdx.x >> 5; r < B; r += nw)
+            for (int q = lane; q < w; q += 32) {
+                const int k = k0 + q;
+                cp_async(dst + r * kPLd + q, X + (int64_t)r * I + (k < I ? k : 0), 4, k < I ? 4 : 0);
+            }
+    }
+}
 
 // rows x cols (global, row stride gs) -> shared (row stride ds), columns cols..ds-1 zeroed.  A
 // warp per row, two rows x four 32-column chunks per batch, all loads before the stores (the
@@ -210,22 +226,13 @@ __device__ NetS stage(const NetP& n, float* sm)
 // samples 16 w + g + 4 i (i < 4) -- four consecutive rows per load instruction -- and the
 // outputs o + 8 m (m < 8) -- eight consecutive weight rows per load instruction.
 template <class XA>
-__device__ __forceinline__ void fwd_gemm(const XA& X, int K4, const float* W, int ldw, const float* b, float* Y,
-                                         bool relu, int B)
+__device__ __forceinline__ void fwd_acc(const XA& X, int c0, int nc, const float* W, int ldw, float (&acc)[4][8])
 {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane & 3, o = lane >> 2;
-    if (16 * w >= B) return;
     const int s0 = 16 * w + g;
-    float acc[4][8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {
-        const float bj = b[o + 8 * m];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[i][m] = bj;
-    }
-    const float* Wo = W + o * ldw;
+    const float* Wo = W + o * ldw + 4 * c0;
 #pragma unroll 2
-    for (int c = 0; c < K4; ++c) {
+    for (int c = 0; c < nc; ++c) {
         float4 x[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) x[i] = X(s0 + 4 * i, c);
@@ -236,10 +243,57 @@ __device__ __forceinline__ void fwd_gemm(const XA& X, int K4, const float* W, in
             for (int i = 0; i < 4; ++i) fma4(acc[i][m], wv, x[i]);
         }
     }
+}
+
+__device__ __forceinline__ void fwd_init(const float* b, float (&acc)[4][8])
+{
+    const int o = (threadIdx.x & 31) >> 2;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const float bj = b[o + 8 * m];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i][m] = bj;
+    }
+}
+
+__device__ __forceinline__ void fwd_store(const float (&acc)[4][8], float* Y, bool relu)
+{
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane & 3, o = lane >> 2;
+    const int s0 = 16 * w + g;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int m = 0; m < 8; ++m) at(Y, s0 + 4 * i, o + 8 * m, kH) = relu ? fmaxf(acc[i][m], 0.0f) : acc[i][m];
+}
+
+template <class XA>
+__device__ __forceinline__ void fwd_gemm(const XA& X, int K4, const float* W, int ldw, const float* b, float* Y,
+                                         bool relu, int B)
+{
+    if (16 * (int)(threadIdx.x >> 5) >= B) return;
+    float acc[4][8];
+    fwd_init(b, acc);
+    fwd_acc(X, 0, K4, W, ldw, acc);
+    fwd_store(acc, Y, relu);
+}
+
+// The actor's input layer: Y = relu(X W1^T + b1) with X [B][I] global, consumed in staged
+// column parts (stage: kB x kPLd floats of free shared memory).  Contains barriers: all
+// threads call it.
+__device__ void fwd_input_layer(const float* X, int I, int B, const NetS& W, float* Y, float* stagebuf)
+{
+    const bool busy = 16 * (int)(threadIdx.x >> 5) < B;
+    float acc[4][8];
+    for (int k0 = 0; k0 < I; k0 += kPW) {
+        const int w = min(kPW, pad4(I) - k0);
+        __syncthreads();
+        stage_cols(X, B, I, k0, w, stagebuf);
+        cp_async_wait_all();
+        __syncthreads();  // (also publishes the caller's staged net)
+        if (k0 == 0) fwd_init(W.b1, acc);
+        if (busy) fwd_acc(XSp{stagebuf, kPLd}, k0 / 4, w / 4, W.W1, W.ld1, acc);
+    }
+    if (busy) fwd_store(acc, Y, true);
 }
 
 // In place: H[s][k] <- (sum_j D[s][j] W2[j][k]) if H[s][k] > 0 else 0 (the delta through a
@@ -296,15 +350,17 @@ __device__ __forceinline__ void bwd_gemm(const float* D, const float* W2, float*
 // = lane >> 2, kq = lane & 3) the 8 x 4 tile j = 8 jg + a, k = 16 wc + 4 kq + b.  The
 // partial ranges are summed by the Adam pass (fixed order).
 template <class XA>
-__device__ __forceinline__ void wgrad(const float* D, const XA& X, int K, int B, int S, float* P, float* Pb)
+__device__ __forceinline__ void wgrad(const float* D, const XA& X, int K, int B, int S, float* P, float* Pb,
+                                      int ldP = -1, bool with_bias = true)
 {
+    if (ldP < 0) ldP = K;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, jg = lane >> 2, kq = lane & 3;
     const int NC = (K + 15) / 16;
     if (w >= NC * S) return;
     const int wc = w % NC, p = w / NC;
     const int ch = (B + S - 1) / S, sb = min(B, p * ch), se = min(B, sb + ch);
     const int c4 = 4 * wc + kq;
-    const bool bias = wc == 0 && kq == 0;
+    const bool bias = with_bias && wc == 0 && kq == 0;
     float acc[8][4], bacc[8];
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
@@ -326,12 +382,12 @@ __device__ __forceinline__ void wgrad(const float* D, const XA& X, int K, int B,
 #pragma unroll
             for (int a = 0; a < 8; ++a) bacc[a] += dv[a];
     }
-    float* Pp = P + (int64_t)p * kH * K;
+    float* Pp = P + (int64_t)p * kH * ldP;
 #pragma unroll
     for (int a = 0; a < 8; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b)
-            if (4 * c4 + b < K) Pp[(8 * jg + a) * K + 4 * c4 + b] = acc[a][b];
+            if (4 * c4 + b < K) Pp[(8 * jg + a) * ldP + 4 * c4 + b] = acc[a][b];
     if (bias)
 #pragma unroll
         for (int a = 0; a < 8; ++a) Pb[p * kH + 8 * jg + a] = bacc[a];
@@ -439,8 +495,8 @@ struct PartL {
 };
 __host__ __device__ inline int wg_splits(int in)
 {
-    const int nc = (in + 15) / 16;
-    return nc >= 16 ? 1 : 16 / nc;
+    const int nc = (in + 15) / 16;  // column blocks of one staged part (<= kPW / 16)
+    return 16 / (nc < kPW / 16 ? nc : kPW / 16);
 }
 __host__ __device__ inline PartL part_layout(int in, int out)
 {
@@ -463,11 +519,11 @@ __host__ __device__ inline PartL part_layout(int in, int out)
     return L;
 }
 
-// Backward of a net from its two activation buffers: Hb = H2 (-> D2 in place), Ha = H1 (->
-// D1 in place), input X; d3 rows (4 floats) in smem.  Writes the partial gradients.
-template <class XA>
-__device__ void net_backward(const NetS& W, int out, const float* d3s, float* Ha, float* Hb, const XA& X, int in,
-                             int B, int s, int hf, const float (&d3)[4], float* part, const PartL& L)
+// Backward of a net from its two activation buffers, up to the input layer's delta: Hb =
+// H2 (-> D2 in place), Ha = H1 (-> D1 in place); d3 rows (4 floats) in smem.  Writes the
+// partial gradients of W3/b3 and W2/b2; the caller does W1/b1 (from its input rows).
+__device__ void net_backward(const NetS& W, int out, const float* d3s, float* Ha, float* Hb, int B, int s, int hf,
+                             const float (&d3)[4], float* part, const PartL& L)
 {
     wgrad_out(d3s, out, Hb, B, part + L.w3, part + L.b3);
     __syncthreads();
@@ -482,7 +538,6 @@ __device__ void net_backward(const NetS& W, int out, const float* d3s, float* Ha
     __syncthreads();
     bwd_gemm(Hb, W.W2, Ha, B);
     __syncthreads();
-    wgrad(Ha, X, in, B, L.S1, part + L.w1, part + L.b1);
 }
 
 struct AdamC {
@@ -498,13 +553,13 @@ __device__ void adam_seg(float* th, float* m, float* v, const float* part, int S
 {
     const int T = blockDim.x;
     for (int k0 = threadIdx.x; k0 < n; k0 += 4 * T) {
-        float gk[4], mk[4], vk[4], tk[4], pk[4];
+        float gk[4], mk[4], vk[4], tk[4], pk[4], pp[4][8];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int k = k0 + u * T;
             const bool in = k < n;
-            gk[u] = 0.0f;
-            for (int p = 0; p < S; ++p) gk[u] += in ? part[p * n + k] : 0.0f;
+#pragma unroll
+            for (int p = 0; p < 8; ++p) pp[u][p] = (in && p < S) ? part[p * n + k] : 0.0f;
             mk[u] = in ? m[k] : 0.0f;
             vk[u] = in ? v[k] : 0.0f;
             tk[u] = in ? th[k] : 0.0f;
@@ -513,6 +568,9 @@ __device__ void adam_seg(float* th, float* m, float* v, const float* part, int S
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int k = k0 + u * T;
+            gk[u] = pp[u][0];
+#pragma unroll
+            for (int p = 1; p < 8; ++p) gk[u] += pp[u][p];  // (in order; the unused ranges add 0)
             if (k < n) {
                 const float mn = fmaf(A.b1, mk[u], (1.0f - A.b1) * gk[u]);
                 const float vn = fmaf(A.b2, vk[u], (1.0f - A.b2) * gk[u] * gk[u]);
@@ -594,8 +652,6 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     float* X32 = Bb + kB * kH;            // [kB][32] swizzled critic inputs
     float* D3 = X32 + kB * kCI;           // [kB][4] output-layer deltas
     float* red = D3 + kB * 4;             // [32]
-    const XGl Xa2{A.o_a2 + (int64_t)ag * B * I, I, B}, Xa{A.o_a + (int64_t)ag * B * I, I, B};
-    const int K4a = (I + 3) / 4;
 
 #ifdef L2F_TD3_TIMING
     long long mark[16] = {};
@@ -603,8 +659,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     TD3_MARK(0);
     // ---- 1. target: a' = clip(pi'(o_a') + clip(sigma eps, -c, c), -1, 1); y = r + g (1-d) min Q'
     NetS W = stage(actor_t, Wsm);
-    __syncthreads();
-    fwd_gemm(Xa2, K4a, W.W1, W.ld1, W.b1, Ab, true, B);
+    fwd_input_layer(A.o_a2 + (int64_t)ag * B * I, I, B, W, Ab, Bb);  // (stages into Bb + X32)
     __syncthreads();
     fwd_gemm(XSm{Ab, kH}, kH / 4, W.W2, kLd2, W.b2, Bb, true, B);
     __syncthreads();
@@ -662,7 +717,8 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         const float loss = block_sum(lead ? e * e / (float)B : 0.0f, red);  // (its barriers publish D3)
         if (threadIdx.x == 0) A.losses[ag * 3 + c] = loss;
         TD3_MARK(3 + 3 * c);
-        net_backward(W, 1, D3, Ab, Bb, XSm{X32, kCI}, kCI, B, s, hf, d3, part, Lc);
+        net_backward(W, 1, D3, Ab, Bb, B, s, hf, d3, part, Lc);
+        wgrad(Ab, XSm{X32, kCI}, kCI, B, Lc.S1, part + Lc.w1, part + Lc.b1);
         __syncthreads();
         TD3_MARK(4 + 3 * c);
         float* mc = m_a + 2 * na + 2 * c * nc;
@@ -678,8 +734,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     // ---- 3. actor: ascend Q1(o_c, pi(o_a)) through the updated Q1's action input, Adam + Polyak
     __syncthreads();
     W = stage(actor, Wsm);
-    __syncthreads();
-    fwd_gemm(Xa, K4a, W.W1, W.ld1, W.b1, Ab, true, B);
+    fwd_input_layer(A.o_a + (int64_t)ag * B * I, I, B, W, Ab, Bb);
     __syncthreads();
     fwd_gemm(XSm{Ab, kH}, kH / 4, W.W2, kLd2, W.b2, Bb, true, B);
     __syncthreads();
@@ -743,7 +798,16 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         st4(Bb + 4 * e, ld4(AH2 + 4 * e));
     }
     __syncthreads();
-    net_backward(W, 4, D3, Ab, Bb, Xa, I, B, s, hf, d3a, part, La);
+    net_backward(W, 4, D3, Ab, Bb, B, s, hf, d3a, part, La);
+    for (int k0 = 0; k0 < I; k0 += kPW) {  // W1/b1 from staged column parts of o_a (into Bb + X32)
+        const int w = min(kPW, pad4(I) - k0);
+        if (k0 > 0) __syncthreads();
+        stage_cols(A.o_a + (int64_t)ag * B * I, B, I, k0, w, Bb);
+        cp_async_wait_all();
+        __syncthreads();
+        wgrad(Ab, XSp{Bb, kPLd}, min(w, I - k0), B, La.S1, part + La.w1 + k0, part + La.b1, I, k0 == 0);
+    }
+    __syncthreads();
     const float loss = block_sum(lossa, red);
     if (threadIdx.x == 0) A.losses[ag * 3 + 2] = loss;
     TD3_MARK(11);
