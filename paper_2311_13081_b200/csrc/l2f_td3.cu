@@ -107,16 +107,12 @@ __device__ __forceinline__ void fma4(float& acc, float4 w, float4 x)
 __device__ __forceinline__ float comp(float4 v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w)); }
 
 // Activation buffers: row s of ld floats (ld = 32 or 64), float4 slot c4 stored at slot
-// c4 ^ (s & 7).
-__device__ __forceinline__ int sw(int s, int c4, int ld) { return s * ld + ((c4 ^ (s & 7)) << 2); }
+// c4 ^ (s & 3): four consecutive rows put the same column in four different bank groups, and
+// the rows s0 + 4 i a GEMM thread owns share one key (s0 & 3), so their addresses differ by
+// compile-time offsets.
+__device__ __forceinline__ int sw(int s, int c4, int ld) { return s * ld + ((c4 ^ (s & 3)) << 2); }
 __device__ __forceinline__ float& at(float* buf, int s, int k, int ld) { return buf[sw(s, k >> 2, ld) + (k & 3)]; }
 
-// Operand accessors of the batch GEMMs: float4 of inputs 4 c4 .. 4 c4 + 3 of sample s.
-struct XSm {  // a swizzled shared-memory activation buffer
-    const float* p;
-    int ld;
-    __device__ __forceinline__ float4 operator()(int s, int c4) const { return ld4(p + sw(s, c4, ld)); }
-};
 struct XSp {  // a plain shared-memory row buffer (row stride ld floats, 16-byte aligned rows)
     const float* p;
     int ld;
@@ -266,15 +262,32 @@ __device__ __forceinline__ void fwd_store(const float (&acc)[4][8], float* Y, bo
         for (int m = 0; m < 8; ++m) at(Y, s0 + 4 * i, o + 8 * m, kH) = relu ? fmaxf(acc[i][m], 0.0f) : acc[i][m];
 }
 
-template <class XA>
-__device__ __forceinline__ void fwd_gemm(const XA& X, int K4, const float* W, int ldw, const float* b, float* Y,
-                                         bool relu, int B)
+// Y = relu(X W^T + b) with X a swizzled activation buffer (row ld = 32 or 64 floats): the
+// thread's four rows s0 + 4 i share the swizzle key g = s0 & 3, so one XOR per chunk
+// addresses all four.
+__device__ __forceinline__ void fwd_gemm(const float* X, int ld, const float* W, int ldw, const float* b, float* Y,
+                                         int B)
 {
-    if (16 * (int)(threadIdx.x >> 5) >= B) return;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane & 3, o = lane >> 2;
+    if (16 * w >= B) return;
     float acc[4][8];
     fwd_init(b, acc);
-    fwd_acc(X, 0, K4, W, ldw, acc);
-    fwd_store(acc, Y, relu);
+    const float* xr = X + (16 * w + g) * ld;
+    const float* Wo = W + o * ldw;
+#pragma unroll 2
+    for (int c = 0; c < ld / 4; ++c) {
+        const float* xc = xr + 4 * (c ^ g);
+        float4 x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = ld4(xc + 4 * i * ld);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const float4 wv = ld4(Wo + 8 * m * ldw + 4 * c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) fma4(acc[i][m], wv, x[i]);
+        }
+    }
+    fwd_store(acc, Y, true);
 }
 
 // The actor's input layer: Y = relu(X W1^T + b1) with X [B][I] global, consumed in staged
@@ -311,8 +324,9 @@ __device__ __forceinline__ void bwd_gemm(const float* D, const float* W2, float*
 #pragma unroll 2
     for (int c = 0; c < kH / 4; ++c) {
         float4 d[4];
+        const float* dc = D + s0 * kH + 4 * (c ^ g);  // (rows s0 + 4 i share the key g)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) d[i] = ld4(D + sw(s0 + 4 * i, c, kH));
+        for (int i = 0; i < 4; ++i) d[i] = ld4(dc + 4 * i * kH);
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
             const float* wr = W2 + (4 * c + jj) * kLd2 + 8 * o;
@@ -349,18 +363,26 @@ __device__ __forceinline__ void bwd_gemm(const float* D, const float* W2, float*
 // stride K), Pb[p][j] = sum D[s][j].  Warp (wc, p) covers k = 16 wc .. 16 wc + 15; lane (jg
 // = lane >> 2, kq = lane & 3) the 8 x 4 tile j = 8 jg + a, k = 16 wc + 4 kq + b.  The
 // partial ranges are summed by the Adam pass (fixed order).
-template <class XA>
-__device__ __forceinline__ void wgrad(const float* D, const XA& X, int K, int B, int S, float* P, float* Pb,
-                                      int ldP = -1, bool with_bias = true)
+template <bool SWX>
+__device__ __forceinline__ void wgrad(const float* D, const float* X, int ldx, int K, int B, int S, float* P,
+                                      float* Pb, int ldP = -1, bool with_bias = true)
 {
     if (ldP < 0) ldP = K;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, jg = lane >> 2, kq = lane & 3;
     const int NC = (K + 15) / 16;
     if (w >= NC * S) return;
     const int wc = w % NC, p = w / NC;
-    const int ch = (B + S - 1) / S, sb = min(B, p * ch), se = min(B, sb + ch);
+    const int ch = (((B + S - 1) / S) + 3) & ~3;  // ranges start at multiples of 4: s & 3 = unrolled j
+    const int sb = min(B, p * ch), se = min(B, sb + ch);
     const int c4 = 4 * wc + kq;
     const bool bias = with_bias && wc == 0 && kq == 0;
+    // D rows (swizzled, 64): logical slots 2 jg, 2 jg + 1 of row s sit at (2 jg ^ (s & 2)) + {0, 1},
+    // swapped when s is odd; X slot c4 at c4 ^ (s & 3) (swizzled) or c4 (plain)
+    int doff[2], xoff[4];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) doff[e] = ((2 * jg) ^ (2 * e)) << 2;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xoff[j] = SWX ? ((c4 ^ j) << 2) : (c4 << 2);
     float acc[8][4], bacc[8];
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
@@ -368,10 +390,10 @@ __device__ __forceinline__ void wgrad(const float* D, const XA& X, int K, int B,
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
     }
-#pragma unroll 4
-    for (int s = sb; s < se; ++s) {
-        const float4 da = ld4(D + sw(s, 2 * jg, kH)), db = ld4(D + sw(s, 2 * jg + 1, kH));
-        const float4 x = X(s, c4);
+    auto body = [&](int s, int j) {  // j = s & 3 (compile-time in the main loop)
+        const float* dr = D + s * kH + doff[(j >> 1) & 1];
+        const float4 da = ld4(dr + 4 * (j & 1)), db = ld4(dr + 4 * ((j & 1) ^ 1));
+        const float4 x = ld4(X + s * ldx + xoff[j & 3]);
         const float dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
         const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -381,7 +403,14 @@ __device__ __forceinline__ void wgrad(const float* D, const XA& X, int K, int B,
         if (bias)
 #pragma unroll
             for (int a = 0; a < 8; ++a) bacc[a] += dv[a];
+    };
+    const int se4 = sb + ((se - sb) & ~3);
+#pragma unroll 2
+    for (int s4 = sb; s4 < se4; s4 += 4) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) body(s4 + j, j);
     }
+    for (int s = se4; s < se; ++s) body(s, s & 3);
     float* Pp = P + (int64_t)p * kH * ldP;
 #pragma unroll
     for (int a = 0; a < 8; ++a)
@@ -534,14 +563,14 @@ __device__ void net_backward(const NetS& W, int out, const float* d3s, float* Ha
         out_back<4>(W, Hb, s, hf, d3);
     }
     __syncthreads();
-    wgrad(Hb, XSm{Ha, kH}, kH, B, 4, part + L.w2, part + L.b2);
+    wgrad<true>(Hb, Ha, kH, kH, B, 4, part + L.w2, part + L.b2);
     __syncthreads();
     bwd_gemm(Hb, W.W2, Ha, B);
     __syncthreads();
 }
 
 struct AdamC {
-    float lr, b1, b2, c1, c2, eps;  // c1 = 1 - beta1^t, c2 = 1 - beta2^t
+    float lr, b1, b2, r1, r2, eps;  // r1 = 1 / (1 - beta1^t), r2 = 1 / (1 - beta2^t)
 };
 
 // Adam on one parameter segment of n whose gradient is the sum of S partials (stride n) at
@@ -574,7 +603,7 @@ __device__ void adam_seg(float* th, float* m, float* v, const float* part, int S
             if (k < n) {
                 const float mn = fmaf(A.b1, mk[u], (1.0f - A.b1) * gk[u]);
                 const float vn = fmaf(A.b2, vk[u], (1.0f - A.b2) * gk[u] * gk[u]);
-                const float tn = tk[u] - A.lr * (mn / A.c1) / (sqrtf(vn / A.c2) + A.eps);
+                const float tn = tk[u] - A.lr * (mn * A.r1) / (sqrtf(vn * A.r2) + A.eps);
                 gout[k] = gk[u];
                 m[k] = mn;
                 v[k] = vn;
@@ -661,7 +690,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     NetS W = stage(actor_t, Wsm);
     fwd_input_layer(A.o_a2 + (int64_t)ag * B * I, I, B, W, Ab, Bb);  // (stages into Bb + X32)
     __syncthreads();
-    fwd_gemm(XSm{Ab, kH}, kH / 4, W.W2, kLd2, W.b2, Bb, true, B);
+    fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
     __syncthreads();
     {
         float at4[4];
@@ -680,9 +709,9 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     float qmin = 0.0f;
     for (int c = 0; c < 2; ++c) {
         const NetS& Wc = c == 0 ? Wt0 : Wt1;
-        fwd_gemm(XSm{X32, kCI}, kCI / 4, Wc.W1, Wc.ld1, Wc.b1, Ab, true, B);
+        fwd_gemm(X32, kCI, Wc.W1, Wc.ld1, Wc.b1, Ab, B);
         __syncthreads();
-        fwd_gemm(XSm{Ab, kH}, kH / 4, Wc.W2, kLd2, Wc.b2, Bb, true, B);
+        fwd_gemm(Ab, kH, Wc.W2, kLd2, Wc.b2, Bb, B);
         __syncthreads();
         float q[1];
         out_layer<1>(Wc, Bb, s, hf, q);
@@ -699,15 +728,15 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     TD3_MARK(2);
 
     // ---- 2. critics: MSE to y, Adam (+ Polyak of the critic targets on delayed steps)
-    const AdamC Ac{A.lr_critic, A.beta1, A.beta2, A.c1_critic, A.c2_critic, A.adam_eps};
+    const AdamC Ac{A.lr_critic, A.beta1, A.beta2, 1.0f / A.c1_critic, 1.0f / A.c2_critic, A.adam_eps};
     for (int c = 0; c < 2; ++c) {
         const NetP& Qc = c == 0 ? Q0 : Q1;
         __syncthreads();
         W = stage(Qc, Wsm);
         __syncthreads();
-        fwd_gemm(XSm{X32, kCI}, kCI / 4, W.W1, W.ld1, W.b1, Ab, true, B);
+        fwd_gemm(X32, kCI, W.W1, W.ld1, W.b1, Ab, B);
         __syncthreads();
-        fwd_gemm(XSm{Ab, kH}, kH / 4, W.W2, kLd2, W.b2, Bb, true, B);
+        fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
         __syncthreads();
         float q[1];
         out_layer<1>(W, Bb, s, hf, q);
@@ -718,7 +747,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         if (threadIdx.x == 0) A.losses[ag * 3 + c] = loss;
         TD3_MARK(3 + 3 * c);
         net_backward(W, 1, D3, Ab, Bb, B, s, hf, d3, part, Lc);
-        wgrad(Ab, XSm{X32, kCI}, kCI, B, Lc.S1, part + Lc.w1, part + Lc.b1);
+        wgrad<true>(Ab, X32, kCI, kCI, B, Lc.S1, part + Lc.w1, part + Lc.b1);
         __syncthreads();
         TD3_MARK(4 + 3 * c);
         float* mc = m_a + 2 * na + 2 * c * nc;
@@ -736,7 +765,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     W = stage(actor, Wsm);
     fwd_input_layer(A.o_a + (int64_t)ag * B * I, I, B, W, Ab, Bb);
     __syncthreads();
-    fwd_gemm(XSm{Ab, kH}, kH / 4, W.W2, kLd2, W.b2, Bb, true, B);
+    fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
     __syncthreads();
     float ap[4];
     out_layer<4>(W, Bb, s, hf, ap);
@@ -751,9 +780,9 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     W = stage(Q0, Wsm);  // the updated Q1
     __syncthreads();
     TD3_MARK(9);
-    fwd_gemm(XSm{X32, kCI}, kCI / 4, W.W1, W.ld1, W.b1, Ab, true, B);
+    fwd_gemm(X32, kCI, W.W1, W.ld1, W.b1, Ab, B);
     __syncthreads();
-    fwd_gemm(XSm{Ab, kH}, kH / 4, W.W2, kLd2, W.b2, Bb, true, B);
+    fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
     __syncthreads();
     float lossa;
     {
@@ -805,13 +834,13 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         stage_cols(A.o_a + (int64_t)ag * B * I, B, I, k0, w, Bb);
         cp_async_wait_all();
         __syncthreads();
-        wgrad(Ab, XSp{Bb, kPLd}, min(w, I - k0), B, La.S1, part + La.w1 + k0, part + La.b1, I, k0 == 0);
+        wgrad<false>(Ab, Bb, kPLd, min(w, I - k0), B, La.S1, part + La.w1 + k0, part + La.b1, I, k0 == 0);
     }
     __syncthreads();
     const float loss = block_sum(lossa, red);
     if (threadIdx.x == 0) A.losses[ag * 3 + 2] = loss;
     TD3_MARK(11);
-    const AdamC Aa{A.lr_actor, A.beta1, A.beta2, A.c1_actor, A.c2_actor, A.adam_eps};
+    const AdamC Aa{A.lr_actor, A.beta1, A.beta2, 1.0f / A.c1_actor, 1.0f / A.c2_actor, A.adam_eps};
     adam_net(actor.W1, m_a, v_a, ga, part, La, I, 4, Aa, actor_t.W1, A.tau);  // ---- 4. with the actor target's Polyak step
     TD3_MARK(12);
 #ifdef L2F_TD3_TIMING
