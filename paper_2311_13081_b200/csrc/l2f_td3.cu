@@ -104,6 +104,13 @@ __device__ __forceinline__ void fma4(float& acc, float4 w, float4 x)
     acc = fmaf(w.w, x.w, acc);
 }
 
+// Packed FP32 pairs (FFMA2): acc.x accumulates the even, acc.y the odd input of each pair.
+__device__ __forceinline__ void fma4x2(float2& acc, float4 w, float4 x)
+{
+    acc = __ffma2_rn(make_float2(w.x, w.y), make_float2(x.x, x.y), acc);
+    acc = __ffma2_rn(make_float2(w.z, w.w), make_float2(x.z, x.w), acc);
+}
+
 __device__ __forceinline__ float comp(float4 v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w)); }
 
 // Activation buffers: row s of ld floats (ld = 32 or 64), float4 slot c4 stored at slot
@@ -222,7 +229,7 @@ __device__ NetS stage(const NetP& n, float* sm)
 // samples 16 w + g + 4 i (i < 4) -- four consecutive rows per load instruction -- and the
 // outputs o + 8 m (m < 8) -- eight consecutive weight rows per load instruction.
 template <class XA>
-__device__ __forceinline__ void fwd_acc(const XA& X, int c0, int nc, const float* W, int ldw, float (&acc)[4][8])
+__device__ __forceinline__ void fwd_acc(const XA& X, int c0, int nc, const float* W, int ldw, float2 (&acc)[4][8])
 {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane & 3, o = lane >> 2;
     const int s0 = 16 * w + g;
@@ -236,30 +243,33 @@ __device__ __forceinline__ void fwd_acc(const XA& X, int c0, int nc, const float
         for (int m = 0; m < 8; ++m) {
             const float4 wv = ld4(Wo + 8 * m * ldw + 4 * c);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) fma4(acc[i][m], wv, x[i]);
+            for (int i = 0; i < 4; ++i) fma4x2(acc[i][m], wv, x[i]);
         }
     }
 }
 
-__device__ __forceinline__ void fwd_init(const float* b, float (&acc)[4][8])
+__device__ __forceinline__ void fwd_init(const float* b, float2 (&acc)[4][8])
 {
     const int o = (threadIdx.x & 31) >> 2;
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
         const float bj = b[o + 8 * m];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[i][m] = bj;
+        for (int i = 0; i < 4; ++i) acc[i][m] = make_float2(bj, 0.0f);
     }
 }
 
-__device__ __forceinline__ void fwd_store(const float (&acc)[4][8], float* Y, bool relu)
+__device__ __forceinline__ void fwd_store(const float2 (&acc)[4][8], float* Y, bool relu)
 {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane & 3, o = lane >> 2;
     const int s0 = 16 * w + g;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int m = 0; m < 8; ++m) at(Y, s0 + 4 * i, o + 8 * m, kH) = relu ? fmaxf(acc[i][m], 0.0f) : acc[i][m];
+        for (int m = 0; m < 8; ++m) {
+            const float v = acc[i][m].x + acc[i][m].y;
+            at(Y, s0 + 4 * i, o + 8 * m, kH) = relu ? fmaxf(v, 0.0f) : v;
+        }
 }
 
 // Y = relu(X W^T + b) with X a swizzled activation buffer (row ld = 32 or 64 floats): the
@@ -270,7 +280,7 @@ __device__ __forceinline__ void fwd_gemm(const float* X, int ld, const float* W,
 {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane & 3, o = lane >> 2;
     if (16 * w >= B) return;
-    float acc[4][8];
+    float2 acc[4][8];
     fwd_init(b, acc);
     const float* xr = X + (16 * w + g) * ld;
     const float* Wo = W + o * ldw;
@@ -284,7 +294,7 @@ __device__ __forceinline__ void fwd_gemm(const float* X, int ld, const float* W,
         for (int m = 0; m < 8; ++m) {
             const float4 wv = ld4(Wo + 8 * m * ldw + 4 * c);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) fma4(acc[i][m], wv, x[i]);
+            for (int i = 0; i < 4; ++i) fma4x2(acc[i][m], wv, x[i]);
         }
     }
     fwd_store(acc, Y, true);
@@ -296,7 +306,7 @@ __device__ __forceinline__ void fwd_gemm(const float* X, int ld, const float* W,
 __device__ void fwd_input_layer(const float* X, int I, int B, const NetS& W, float* Y, float* stagebuf)
 {
     const bool busy = 16 * (int)(threadIdx.x >> 5) < B;
-    float acc[4][8];
+    float2 acc[4][8];
     for (int k0 = 0; k0 < I; k0 += kPW) {
         const int w = min(kPW, pad4(I) - k0);
         __syncthreads();
@@ -316,11 +326,11 @@ __device__ __forceinline__ void bwd_gemm(const float* D, const float* W2, float*
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane & 3, o = lane >> 2;
     if (16 * w >= B) return;
     const int s0 = 16 * w + g;
-    float acc[4][8];
+    float2 acc[4][4];  // (k, k + 1) pairs of outputs 8 o + 2 q, FFMA2
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int m = 0; m < 8; ++m) acc[i][m] = 0.0f;
+        for (int q = 0; q < 4; ++q) acc[i][q] = make_float2(0.0f, 0.0f);
 #pragma unroll 2
     for (int c = 0; c < kH / 4; ++c) {
         float4 d[4];
@@ -331,17 +341,14 @@ __device__ __forceinline__ void bwd_gemm(const float* D, const float* W2, float*
         for (int jj = 0; jj < 4; ++jj) {
             const float* wr = W2 + (4 * c + jj) * kLd2 + 8 * o;
             const float4 wa = ld4(wr), wb = ld4(wr + 4);
+            const float2 wp[4] = {make_float2(wa.x, wa.y), make_float2(wa.z, wa.w), make_float2(wb.x, wb.y),
+                                  make_float2(wb.z, wb.w)};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const float dv = comp(d[i], jj);
-                acc[i][0] = fmaf(dv, wa.x, acc[i][0]);
-                acc[i][1] = fmaf(dv, wa.y, acc[i][1]);
-                acc[i][2] = fmaf(dv, wa.z, acc[i][2]);
-                acc[i][3] = fmaf(dv, wa.w, acc[i][3]);
-                acc[i][4] = fmaf(dv, wb.x, acc[i][4]);
-                acc[i][5] = fmaf(dv, wb.y, acc[i][5]);
-                acc[i][6] = fmaf(dv, wb.z, acc[i][6]);
-                acc[i][7] = fmaf(dv, wb.w, acc[i][7]);
+                const float2 dd = make_float2(dv, dv);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[i][q] = __ffma2_rn(dd, wp[q], acc[i][q]);
             }
         }
     }
@@ -352,8 +359,9 @@ __device__ __forceinline__ void bwd_gemm(const float* D, const float* W2, float*
         for (int hh = 0; hh < 2; ++hh) {
             float* p = H + sw(s, 2 * o + hh, kH);
             const float4 h = ld4(p);
-            st4(p, make_float4(h.x > 0.0f ? acc[i][4 * hh] : 0.0f, h.y > 0.0f ? acc[i][4 * hh + 1] : 0.0f,
-                               h.z > 0.0f ? acc[i][4 * hh + 2] : 0.0f, h.w > 0.0f ? acc[i][4 * hh + 3] : 0.0f));
+            const float2 a = acc[i][2 * hh], b = acc[i][2 * hh + 1];
+            st4(p, make_float4(h.x > 0.0f ? a.x : 0.0f, h.y > 0.0f ? a.y : 0.0f, h.z > 0.0f ? b.x : 0.0f,
+                               h.w > 0.0f ? b.y : 0.0f));
         }
     }
 }
@@ -383,26 +391,29 @@ __device__ __forceinline__ void wgrad(const float* D, const float* X, int ldx, i
     for (int e = 0; e < 2; ++e) doff[e] = ((2 * jg) ^ (2 * e)) << 2;
 #pragma unroll
     for (int j = 0; j < 4; ++j) xoff[j] = SWX ? ((c4 ^ j) << 2) : (c4 << 2);
-    float acc[8][4], bacc[8];
+    float2 acc[4][4], bacc[4];  // rows (8 jg + 2 q, 8 jg + 2 q + 1) as FFMA2 pairs
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-        bacc[a] = 0.0f;
+    for (int q = 0; q < 4; ++q) {
+        bacc[q] = make_float2(0.0f, 0.0f);
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
+        for (int b = 0; b < 4; ++b) acc[q][b] = make_float2(0.0f, 0.0f);
     }
     auto body = [&](int s, int j) {  // j = s & 3 (compile-time in the main loop)
         const float* dr = D + s * kH + doff[(j >> 1) & 1];
         const float4 da = ld4(dr + 4 * (j & 1)), db = ld4(dr + 4 * ((j & 1) ^ 1));
         const float4 x = ld4(X + s * ldx + xoff[j & 3]);
-        const float dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+        const float2 dp[4] = {make_float2(da.x, da.y), make_float2(da.z, da.w), make_float2(db.x, db.y),
+                              make_float2(db.z, db.w)};
         const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-        for (int a = 0; a < 8; ++a)
+        for (int b = 0; b < 4; ++b) {
+            const float2 xx = make_float2(xv[b], xv[b]);
 #pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(dv[a], xv[b], acc[a][b]);
+            for (int q = 0; q < 4; ++q) acc[q][b] = __ffma2_rn(dp[q], xx, acc[q][b]);
+        }
         if (bias)
 #pragma unroll
-            for (int a = 0; a < 8; ++a) bacc[a] += dv[a];
+            for (int q = 0; q < 4; ++q) bacc[q] = __fadd2_rn(bacc[q], dp[q]);
     };
     const int se4 = sb + ((se - sb) & ~3);
 #pragma unroll 2
@@ -413,13 +424,19 @@ __device__ __forceinline__ void wgrad(const float* D, const float* X, int ldx, i
     for (int s = se4; s < se; ++s) body(s, s & 3);
     float* Pp = P + (int64_t)p * kH * ldP;
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+    for (int q = 0; q < 4; ++q)
 #pragma unroll
         for (int b = 0; b < 4; ++b)
-            if (4 * c4 + b < K) Pp[(8 * jg + a) * ldP + 4 * c4 + b] = acc[a][b];
+            if (4 * c4 + b < K) {
+                Pp[(8 * jg + 2 * q) * ldP + 4 * c4 + b] = acc[q][b].x;
+                Pp[(8 * jg + 2 * q + 1) * ldP + 4 * c4 + b] = acc[q][b].y;
+            }
     if (bias)
 #pragma unroll
-        for (int a = 0; a < 8; ++a) Pb[p * kH + 8 * jg + a] = bacc[a];
+        for (int q = 0; q < 4; ++q) {
+            Pb[p * kH + 8 * jg + 2 * q] = bacc[q].x;
+            Pb[p * kH + 8 * jg + 2 * q + 1] = bacc[q].y;
+        }
 }
 
 // Partial output-layer gradients (out <= 4 outputs): P[p][o][k] = sum_{s in range p} d3[s][o]
