@@ -90,3 +90,16 @@ def test_create_rejects_host_memory(L):
     addr = (C.addressof(buf) + 255) & ~255
     st = L.l2f_create(C.byref(c), C.c_void_p(addr), 1 << 19, C.byref(h))
     assert st != 0
+
+
+def test_td3_sizes_and_validation(L):
+    """l2f_td3_sizes is host-only: the parameter block is 4 actor-sized + 8 critic-sized nets
+    (nets, targets, Adam moments; include/l2f.h), bounds on batch and in_dim are enforced."""
+    blk, sb = C.c_int64(), C.c_int64()
+    assert L.l2f_td3_sizes(146, 256, C.byref(blk), C.byref(sb)) == 0
+    net = lambda i, o: 64 * i + 64 + 64 * 64 + 64 + o * 64 + o  # noqa: E731
+    assert blk.value == 4 * net(146, 4) + 8 * net(32, 1)
+    assert sb.value % 256 == 0 and sb.value >= 4 * (256 * 554 + 2 * net(32, 1) + net(146, 4))
+    assert L.l2f_td3_sizes(156, 1, C.byref(blk), C.byref(sb)) == 0
+    for bad in ((157, 256), (0, 256), (146, 0), (146, 257)):
+        assert L.l2f_td3_sizes(bad[0], bad[1], C.byref(blk), C.byref(sb)) == 1, bad

@@ -134,9 +134,10 @@ def test_td3_actor_exports_to_the_rollout(pkg):
     assert torch.isfinite(env.state).all()
 
 
-@pytest.mark.parametrize("A,B,I", [(1, 1, 18), (5, 33, 18), (2, 256, 146)])
+@pytest.mark.parametrize("A,B,I", [(1, 1, 18), (5, 33, 18), (2, 256, 146), (2, 77, 35), (1, 256, 156)])
 def test_td3_edge_shapes_match_oracle(pkg, A, B, I):
-    """Single-sample batch, N_H = 0 actor input (in_dim 18), ragged batch, full batch."""
+    """Single-sample batch, N_H = 0 actor input (in_dim 18), ragged batch, full batch, an odd
+    in_dim (4-byte staging path), the largest supported in_dim (two staged column parts)."""
     td3, P_or, res = run_both(pkg, A, B, I, [True], seed=11)
     losses, gg, ref = res[0]
     for a in range(A):
@@ -151,6 +152,25 @@ def test_td3_invalid_arguments(pkg):
         pkg.TD3(1, 146, 0)
     with pytest.raises(Exception):
         pkg.TD3(1, 146, 257)
+    with pytest.raises(Exception):
+        pkg.TD3(1, 157, 64)  # beyond the kernel's shared-memory plan
+
+
+def test_td3_update_is_deterministic(pkg):
+    """The partial gradients are summed in a fixed order: two learners fed the same state and
+    batch end bitwise equal (losses, gradients, parameters)."""
+    A, B, I = 3, 256, 146
+    bt = {k: torch.as_tensor(v) for k, v in make_batch(A, B, I, 9).items()}
+    res = []
+    for _ in range(2):
+        td3 = pkg.TD3(A, I, B)
+        td3.params.copy_(torch.as_tensor(np.stack([init_block(td3, 40 + a) for a in range(A)])))
+        l1 = td3.update(bt, update_actor=False).clone()
+        l2 = td3.update(bt, update_actor=True).clone()
+        res.append((l1, l2, td3.params.clone(), {k: v.clone() for k, v in td3.grads().items()}))
+    (a1, a2, ap, ag), (b1, b2, bp, bg) = res
+    assert torch.equal(a1, b1) and torch.equal(a2, b2) and torch.equal(ap, bp)
+    assert all(torch.equal(ag[k], bg[k]) for k in ag)
 
 
 def test_td3_export_actor_on_device_matches_host_rounding(pkg):
