@@ -87,9 +87,18 @@ struct NetS {  // a net staged in shared memory
         __syncthreads();                                             \
         if (blockIdx.x == 0 && threadIdx.x == 0) mark[k] = clock64(); \
     } while (0)
+__device__ long long g_td3_sub[32];
+#define TD3_SUB(k)                                                          \
+    do {                                                                    \
+        __syncthreads();                                                    \
+        if (blockIdx.x == 0 && threadIdx.x == 0) g_td3_sub[k] = clock64(); \
+    } while (0)
 #else
 #define TD3_MARK(k) \
     do {            \
+    } while (0)
+#define TD3_SUB(k) \
+    do {           \
     } while (0)
 #endif
 
@@ -164,31 +173,15 @@ __device__ void stage_cols(const float* X, int B, int I, int k0, int w, float* d
     }
 }
 
-// rows x cols (global, row stride gs) -> shared (row stride ds), columns cols..ds-1 zeroed.  A
-// warp per row, two rows x four 32-column chunks per batch, all loads before the stores (the
-// compiler cannot prove the source and destination apart, so a plain copy loop would run one
-// load round trip per element).  Plain loads: the source may have been written by this kernel.
+// rows x cols (global, row stride gs) -> shared (row stride ds), columns cols..ds-1 zeroed:
+// 4-byte cp.async, a warp per row, every copy of the thread in flight at once (the source may
+// have been written by this kernel earlier: cp.async reads through L1 like a plain load).
+// Caller waits (cp_async_wait_all) and syncs.
 __device__ void copy_rows(const float* g, int rows, int cols, int gs, float* d, int ds)
 {
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int r0 = threadIdx.x >> 5; r0 < rows; r0 += 2 * nw)
-        for (int i0 = lane; i0 < ds; i0 += 128) {
-            float t[2][4];
-#pragma unroll
-            for (int q = 0; q < 2; ++q)
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int r = r0 + q * nw, i = i0 + 32 * u;
-                    t[q][u] = (r < rows && i < cols) ? g[(int64_t)r * gs + i] : 0.0f;
-                }
-#pragma unroll
-            for (int q = 0; q < 2; ++q)
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int r = r0 + q * nw, i = i0 + 32 * u;
-                    if (r < rows && i < ds) d[r * ds + i] = t[q][u];
-                }
-        }
+    for (int r = threadIdx.x >> 5; r < rows; r += nw)
+        for (int i = lane; i < ds; i += 32) cp_async(d + r * ds + i, g + (int64_t)r * gs + (i < cols ? i : 0), 4, i < cols ? 4 : 0);
 }
 
 // CTA-cooperative copy of a net into shared memory at sm (16-byte aligned); caller syncs.
@@ -206,13 +199,11 @@ __device__ NetS stage(const NetP& n, float* sm)
     copy_rows(n.W2, kH, kH, kH, W2, kLd2);
     copy_rows(n.W3, n.out, kH, kH, W3, kH);
     for (int e = threadIdx.x; e < 2 * kH + n.out; e += blockDim.x) {
-        if (e < kH)
-            b1[e] = n.b1[e];
-        else if (e < 2 * kH)
-            b2[e - kH] = n.b2[e - kH];
-        else
-            b3[e - 2 * kH] = n.b3[e - 2 * kH];
+        const float* src = e < kH ? n.b1 + e : (e < 2 * kH ? n.b2 + (e - kH) : n.b3 + (e - 2 * kH));
+        float* dst = e < kH ? b1 + e : (e < 2 * kH ? b2 + (e - kH) : b3 + (e - 2 * kH));
+        cp_async(dst, src, 4, 4);
     }
+    cp_async_wait_all();  // (the caller's barrier publishes)
     S.W1 = W1;
     S.b1 = b1;
     S.W2 = W2;
@@ -313,8 +304,10 @@ __device__ void fwd_input_layer(const float* X, int I, int B, const NetS& W, flo
         stage_cols(X, B, I, k0, w, stagebuf);
         cp_async_wait_all();
         __syncthreads();  // (also publishes the caller's staged net)
+        TD3_SUB(2 * (k0 / kPW));
         if (k0 == 0) fwd_init(W.b1, acc);
         if (busy) fwd_acc(XSp{stagebuf, kPLd}, k0 / 4, w / 4, W.W1, W.ld1, acc);
+        TD3_SUB(2 * (k0 / kPW) + 1);
     }
     if (busy) fwd_store(acc, Y, true);
 }
@@ -705,10 +698,13 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     TD3_MARK(0);
     // ---- 1. target: a' = clip(pi'(o_a') + clip(sigma eps, -c, c), -1, 1); y = r + g (1-d) min Q'
     NetS W = stage(actor_t, Wsm);
+    TD3_SUB(8);
     fwd_input_layer(A.o_a2 + (int64_t)ag * B * I, I, B, W, Ab, Bb);  // (stages into Bb + X32)
     __syncthreads();
+    TD3_SUB(9);
     fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
     __syncthreads();
+    TD3_SUB(10);
     {
         float at4[4];
         out_layer<4>(W, Bb, s, hf, at4);
@@ -720,6 +716,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         put_critic_row(X32, s, hf, A.o_c2 + rb * 28, at4);
     }
     __syncthreads();
+    TD3_SUB(11);
     const NetS Wt0 = stage(Qt0, Wsm), Wt1 = stage(Qt1, Wsm + stage_floats(kCI, 1));
     __syncthreads();
     TD3_MARK(1);
@@ -867,6 +864,11 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
                mark[1] - mark[0], mark[2] - mark[1], mark[3] - mark[2], mark[4] - mark[3], mark[5] - mark[4],
                mark[6] - mark[5], mark[7] - mark[6], mark[8] - mark[7], mark[10] - mark[8], mark[11] - mark[10],
                mark[12] - mark[11], mark[12] - mark[0]);
+        printf("L2F_TD3 sub: stage actor_t %lld | input part0: staged %lld compute %lld, part1: staged %lld compute %lld"
+               " (actor phase) | L2 %lld | out+noise %lld | stage 2 critics %lld\n",
+               g_td3_sub[8] - mark[0], g_td3_sub[0] - g_td3_sub[8], g_td3_sub[1] - g_td3_sub[0],
+               g_td3_sub[2] - g_td3_sub[1], g_td3_sub[3] - g_td3_sub[2], g_td3_sub[10] - g_td3_sub[9],
+               g_td3_sub[11] - g_td3_sub[10], mark[1] - g_td3_sub[11]);
     }
 #endif
 }
