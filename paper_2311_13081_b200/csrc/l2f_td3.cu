@@ -151,24 +151,29 @@ __device__ __forceinline__ void cp_async(float* dst, const float* src, int bytes
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// Columns [k0, k0 + w) of the batch rows X [B][I] (global) -> dst [B][kPLd] with cp.async
-// (all copies in flight at once), zero beyond I; a warp per row.  Caller waits + syncs.
-__device__ void stage_cols(const float* X, int B, int I, int k0, int w, float* dst)
+// Columns [k0, k0 + w) of the batch rows X [B][I] (global) -> dst rows of ld floats (plain),
+// or, with ld == 0, the swizzled 64-float activation layout (w <= 64), by cp.async (every copy
+// in flight at once), zero beyond I; a warp per row.  Caller waits + syncs.
+__device__ __forceinline__ int stage_off(int r, int q, int ld)  // float offset of column q of row r
+{
+    return ld ? r * ld + q : r * kH + ((((q >> 2) ^ (r & 3)) << 2) | (q & 3));
+}
+__device__ void stage_cols(const float* X, int B, int I, int k0, int w, float* dst, int ld = kPLd)
 {
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    if (!(I & 1)) {  // 8-byte pieces (I even: rows 8-byte aligned)
+    if (!(I & 1)) {  // 8-byte pieces (I even: rows 8-byte aligned; a piece never straddles a slot)
         const int np = (w + 1) >> 1;
         for (int r = threadIdx.x >> 5; r < B; r += nw)
             for (int q = lane; q < np; q += 32) {
                 const int k = k0 + 2 * q;
                 const int b = k + 2 <= I ? 8 : (k < I ? 4 : 0);
-                cp_async(dst + r * kPLd + 2 * q, X + (int64_t)r * I + (b ? k : 0), 8, b);
+                cp_async(dst + stage_off(r, 2 * q, ld), X + (int64_t)r * I + (b ? k : 0), 8, b);
             }
     } else {
         for (int r = threadIdx.x >> 5; r < B; r += nw)
             for (int q = lane; q < w; q += 32) {
                 const int k = k0 + q;
-                cp_async(dst + r * kPLd + q, X + (int64_t)r * I + (k < I ? k : 0), 4, k < I ? 4 : 0);
+                cp_async(dst + stage_off(r, q, ld), X + (int64_t)r * I + (k < I ? k : 0), 4, k < I ? 4 : 0);
             }
     }
 }
@@ -184,8 +189,9 @@ __device__ void copy_rows(const float* g, int rows, int cols, int gs, float* d, 
         for (int i = lane; i < ds; i += 32) cp_async(d + r * ds + i, g + (int64_t)r * gs + (i < cols ? i : 0), 4, i < cols ? 4 : 0);
 }
 
-// CTA-cooperative copy of a net into shared memory at sm (16-byte aligned); caller syncs.
-__device__ NetS stage(const NetP& n, float* sm)
+// CTA-cooperative copy of a net into shared memory at sm (16-byte aligned): issues the
+// copies (stage_issue) or issues and waits for this thread's (stage); caller syncs.
+__device__ NetS stage_issue(const NetP& n, float* sm)
 {
     NetS S;
     S.ld1 = ldw_of(n.in);
@@ -203,13 +209,19 @@ __device__ NetS stage(const NetP& n, float* sm)
         float* dst = e < kH ? b1 + e : (e < 2 * kH ? b2 + (e - kH) : b3 + (e - 2 * kH));
         cp_async(dst, src, 4, 4);
     }
-    cp_async_wait_all();  // (the caller's barrier publishes)
     S.W1 = W1;
     S.b1 = b1;
     S.W2 = W2;
     S.b2 = b2;
     S.W3 = W3;
     S.b3 = b3;
+    return S;
+}
+
+__device__ NetS stage(const NetP& n, float* sm)
+{
+    const NetS S = stage_issue(n, sm);
+    cp_async_wait_all();  // (the caller's barrier publishes)
     return S;
 }
 
@@ -291,25 +303,55 @@ __device__ __forceinline__ void fwd_gemm(const float* X, int ld, const float* W,
     fwd_store(acc, Y, true);
 }
 
-// The actor's input layer: Y = relu(X W1^T + b1) with X [B][I] global, consumed in staged
-// column parts (stage: kB x kPLd floats of free shared memory).  Contains barriers: all
-// threads call it.
-__device__ void fwd_input_layer(const float* X, int I, int B, const NetS& W, float* Y, float* stagebuf)
+// Chunks [c0, c0 + nc) of the input layer from a swizzled 64-float row buffer (local chunk
+// c at slot c ^ g for the thread's four rows).
+__device__ __forceinline__ void fwd_acc_sw(const float* X, int c0, int nc, const float* W, int ldw,
+                                           float2 (&acc)[4][8])
 {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane & 3, o = lane >> 2;
+    const float* xr = X + (16 * w + g) * kH;
+    const float* Wo = W + o * ldw + 4 * c0;
+#pragma unroll 2
+    for (int c = 0; c < nc; ++c) {
+        const float* xc = xr + 4 * (c ^ g);
+        float4 x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = ld4(xc + 4 * i * kH);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const float4 wv = ld4(Wo + 8 * m * ldw + 4 * c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) fma4x2(acc[i][m], wv, x[i]);
+        }
+    }
+}
+
+// The actor's input layer, Y = relu(X W1^T + b1), X [B][I] global rows (I <= kMaxIn): the
+// net (n -> Wsm) and both column parts of X are staged by one wave of cp.async -- columns
+// [0, kP0) into rows of kP0 floats at P0buf (B + X32: free here), the rest (<= 64) swizzled
+// into Y itself (free until the layer's output is stored, after a barrier).  Contains
+// barriers: all threads call it.
+constexpr int kP0 = 92;  // 23 float4s (odd: four consecutive rows hit four bank groups)
+__device__ NetS fwd_input_layer(const NetP& n, float* Wsm, const float* X, int I, int B, float* Y, float* P0buf)
+{
+    const NetS W = stage_issue(n, Wsm);
+    const int K4 = pad4(I) / 4, c1 = min(K4, kP0 / 4);
+    stage_cols(X, B, I, 0, 4 * c1, P0buf, kP0);
+    if (K4 > c1) stage_cols(X, B, I, kP0, 4 * (K4 - c1), Y, 0);
+    cp_async_wait_all();
+    __syncthreads();
+    TD3_SUB(0);
     const bool busy = 16 * (int)(threadIdx.x >> 5) < B;
     float2 acc[4][8];
-    for (int k0 = 0; k0 < I; k0 += kPW) {
-        const int w = min(kPW, pad4(I) - k0);
-        __syncthreads();
-        stage_cols(X, B, I, k0, w, stagebuf);
-        cp_async_wait_all();
-        __syncthreads();  // (also publishes the caller's staged net)
-        TD3_SUB(2 * (k0 / kPW));
-        if (k0 == 0) fwd_init(W.b1, acc);
-        if (busy) fwd_acc(XSp{stagebuf, kPLd}, k0 / 4, w / 4, W.W1, W.ld1, acc);
-        TD3_SUB(2 * (k0 / kPW) + 1);
+    fwd_init(W.b1, acc);
+    if (busy) {
+        fwd_acc(XSp{P0buf, kP0}, 0, c1, W.W1, W.ld1, acc);
+        if (K4 > c1) fwd_acc_sw(Y, c1, K4 - c1, W.W1, W.ld1, acc);
     }
+    __syncthreads();  // (Y held the second part)
+    TD3_SUB(1);
     if (busy) fwd_store(acc, Y, true);
+    return W;
 }
 
 // In place: H[s][k] <- (sum_j D[s][j] W2[j][k]) if H[s][k] > 0 else 0 (the delta through a
@@ -697,9 +739,8 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
 #endif
     TD3_MARK(0);
     // ---- 1. target: a' = clip(pi'(o_a') + clip(sigma eps, -c, c), -1, 1); y = r + g (1-d) min Q'
-    NetS W = stage(actor_t, Wsm);
     TD3_SUB(8);
-    fwd_input_layer(A.o_a2 + (int64_t)ag * B * I, I, B, W, Ab, Bb);  // (stages into Bb + X32)
+    NetS W = fwd_input_layer(actor_t, Wsm, A.o_a2 + (int64_t)ag * B * I, I, B, Ab, Bb);
     __syncthreads();
     TD3_SUB(9);
     fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
@@ -776,8 +817,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
 
     // ---- 3. actor: ascend Q1(o_c, pi(o_a)) through the updated Q1's action input, Adam + Polyak
     __syncthreads();
-    W = stage(actor, Wsm);
-    fwd_input_layer(A.o_a + (int64_t)ag * B * I, I, B, W, Ab, Bb);
+    W = fwd_input_layer(actor, Wsm, A.o_a + (int64_t)ag * B * I, I, B, Ab, Bb);
     __syncthreads();
     fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
     __syncthreads();
@@ -864,10 +904,9 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
                mark[1] - mark[0], mark[2] - mark[1], mark[3] - mark[2], mark[4] - mark[3], mark[5] - mark[4],
                mark[6] - mark[5], mark[7] - mark[6], mark[8] - mark[7], mark[10] - mark[8], mark[11] - mark[10],
                mark[12] - mark[11], mark[12] - mark[0]);
-        printf("L2F_TD3 sub: stage actor_t %lld | input part0: staged %lld compute %lld, part1: staged %lld compute %lld"
-               " (actor phase) | L2 %lld | out+noise %lld | stage 2 critics %lld\n",
-               g_td3_sub[8] - mark[0], g_td3_sub[0] - g_td3_sub[8], g_td3_sub[1] - g_td3_sub[0],
-               g_td3_sub[2] - g_td3_sub[1], g_td3_sub[3] - g_td3_sub[2], g_td3_sub[10] - g_td3_sub[9],
+        printf("L2F_TD3 sub (actor phase): net + input staged %lld, input layer %lld | (target) L2 %lld | out+noise %lld"
+               " | stage 2 critics %lld\n",
+               g_td3_sub[0] - mark[9] + mark[9] - mark[8], g_td3_sub[1] - g_td3_sub[0], g_td3_sub[10] - g_td3_sub[9],
                g_td3_sub[11] - g_td3_sub[10], mark[1] - g_td3_sub[11]);
     }
 #endif
