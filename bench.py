@@ -172,6 +172,16 @@ def cpu_baseline(cfg, policy_w, target_s=15.0, nthreads=None):
                       f"C5 workload, FP64 C oracle on {nthreads} threads, {el:.1f} s wall"}
 
 
+def main_config(n, T, mode, world):
+    """The workload both arms report (the reference arm times a bounded sample of it)."""
+    return {"workload": "C5 per-GPU shard: 2^21 envs/GPU x 1000 steps fused actor-MLP rollout "
+                        "(146-64-64-4 tcgen05, N_H=32), obs/action noise, reward + 4-stage "
+                        "curriculum, termination, auto-reset, disturbance; NCCL stat all-reduce",
+            "envs_per_gpu": n, "steps_per_rollout": T, "mode": mode,
+            "l2": "inputs larger than L2: env state+history 1.4 GB per GPU",
+            "parallelism": f"env-shard x{world}"}
+
+
 def reference_arm(args):
     """--impl reference: the oracle (the base contract's reference arm for this tier)."""
     world, rank, local = dist_setup(args)
@@ -182,18 +192,22 @@ def reference_arm(args):
     cfg = inputs.config_c5()
     W = inputs.policy_weights(18 + 4 * cfg["n_hist"], 64, seed=7, out_bias=inputs.hover_policy_bias())
     target = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    target = float(os.environ.get("L2F_REF_TARGET_S", target))  # (tests: a short sample)
     vals = []
     cb = None
+    walls = []
     for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         cb = cpu_baseline(cfg, W, target_s=target)
         if k >= args.warmup:
             vals.append(cb["value"])
+            walls.append(time.perf_counter() - t0)
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "env-steps/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(walls) / len(walls),
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C5 per-GPU shard (bounded oracle sample)", "envs_per_gpu": ENVS_PER_GPU,
-                       "steps_per_rollout": T_ROLLOUT},
+            "config": main_config(ENVS_PER_GPU, T_ROLLOUT, "mlp", args.gpus),
             "cpu_baseline": dict(cb, value=v),
             "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "sim_seconds_per_wall_second": v * DT}
@@ -317,12 +331,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32+f16mma", "data": "synthetic",
-                "config": {"workload": "C5 per-GPU shard: 2^21 envs/GPU x 1000 steps fused actor-MLP rollout "
-                                       "(146-64-64-4 tcgen05, N_H=32), obs/action noise, reward + 4-stage "
-                                       "curriculum, termination, auto-reset, disturbance; NCCL stat all-reduce",
-                           "envs_per_gpu": n, "steps_per_rollout": T, "mode": args.mode,
-                           "l2": "inputs larger than L2: env state+history 1.4 GB per GPU",
-                           "parallelism": f"env-shard x{world}"},
+                "config": main_config(n, T, args.mode, world),
                 "sim_seconds_per_wall_second": value * DT,
                 "roofline": roof,
                 "e2e": {"value": e2e_val, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,

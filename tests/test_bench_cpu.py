@@ -1,0 +1,35 @@
+"""bench.py's reference arm (-m "not gpu"): the oracle timed on host cores prints the contract's
+JSON line with the same metric and config as the GPU arm; under torchrun only rank 0 prints."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run(args, env_extra):
+    env = dict(os.environ, L2F_REF_TARGET_S="0.5", **env_extra)
+    return subprocess.run([sys.executable, "bench.py", "--impl", "reference"] + args, cwd=ROOT, env=env,
+                          capture_output=True, text=True, timeout=600)
+
+
+def test_reference_arm_line():
+    sys.path.insert(0, ROOT)
+    import bench
+    r = run(["--steps", "1", "--warmup", "0"], {})
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["metric"] == bench.METRIC and line["unit"] == "env-steps/s"
+    assert line["value"] > 0 and line["higher_is_better"] is True and line["n_gpus"] == 1
+    assert line["config"] == bench.main_config(bench.ENVS_PER_GPU, bench.T_ROLLOUT, "mlp", 1)
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
+    assert line["e2e"] == {"value": line["value"], "unit": "env-steps/s", "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
+
+
+def test_reference_arm_nonzero_rank_is_silent():
+    r = run(["--gpus", "2", "--steps", "1", "--warmup", "0"], {"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip() == ""
