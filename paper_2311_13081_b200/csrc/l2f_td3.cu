@@ -332,15 +332,20 @@ __device__ __forceinline__ void fwd_acc_sw(const float* X, int c0, int nc, const
 // into Y itself (free until the layer's output is stored, after a barrier).  Contains
 // barriers: all threads call it.
 constexpr int kP0 = 92;  // 23 float4s (odd: four consecutive rows hit four bank groups)
-__device__ NetS fwd_input_layer(const NetP& n, float* Wsm, const float* X, int I, int B, float* Y, float* P0buf)
+__device__ NetS input_issue(const NetP& n, float* Wsm, const float* X, int I, int B, float* Y, float* P0buf)
 {
     const NetS W = stage_issue(n, Wsm);
     const int K4 = pad4(I) / 4, c1 = min(K4, kP0 / 4);
     stage_cols(X, B, I, 0, 4 * c1, P0buf, kP0);
     if (K4 > c1) stage_cols(X, B, I, kP0, 4 * (K4 - c1), Y, 0);
+    return W;
+}
+__device__ void input_compute(const NetS& W, int I, int B, float* Y, float* P0buf)
+{
     cp_async_wait_all();
     __syncthreads();
     TD3_SUB(0);
+    const int K4 = pad4(I) / 4, c1 = min(K4, kP0 / 4);
     const bool busy = 16 * (int)(threadIdx.x >> 5) < B;
     float2 acc[4][8];
     fwd_init(W.b1, acc);
@@ -351,6 +356,11 @@ __device__ NetS fwd_input_layer(const NetP& n, float* Wsm, const float* X, int I
     __syncthreads();  // (Y held the second part)
     TD3_SUB(1);
     if (busy) fwd_store(acc, Y, true);
+}
+__device__ NetS fwd_input_layer(const NetP& n, float* Wsm, const float* X, int I, int B, float* Y, float* P0buf)
+{
+    const NetS W = input_issue(n, Wsm, X, I, B, Y, P0buf);
+    input_compute(W, I, B, Y, P0buf);
     return W;
 }
 
@@ -784,10 +794,10 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
 
     // ---- 2. critics: MSE to y, Adam (+ Polyak of the critic targets on delayed steps)
     const AdamC Ac{A.lr_critic, A.beta1, A.beta2, 1.0f / A.c1_critic, 1.0f / A.c2_critic, A.adam_eps};
-    for (int c = 0; c < 2; ++c) {
+    __syncthreads();
+    W = stage(Q0, Wsm);
+    for (int c = 0; c < 2; ++c) {  // (critic 1's net is prefetched during critic 0's Adam)
         const NetP& Qc = c == 0 ? Q0 : Q1;
-        __syncthreads();
-        W = stage(Qc, Wsm);
         __syncthreads();
         fwd_gemm(X32, kCI, W.W1, W.ld1, W.b1, Ab, B);
         __syncthreads();
@@ -805,9 +815,16 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         wgrad<true>(Ab, X32, kCI, kCI, B, Lc.S1, part + Lc.w1, part + Lc.b1);
         __syncthreads();
         TD3_MARK(4 + 3 * c);
+        // prefetch the next phase's shared-memory operands under Adam's HBM traffic: critic 1's
+        // net, or the actor net + input rows (free regions; none of them is updated by this Adam)
+        if (c == 0)
+            W = stage_issue(Q1, Wsm);
+        else if (A.update_actor)
+            W = input_issue(actor, Wsm, A.o_a + (int64_t)ag * B * I, I, B, Ab, Bb);
         float* mc = m_a + 2 * na + 2 * c * nc;
         adam_net(Qc.W1, mc, mc + nc, gq0 + c * nc, part, Lc, kCI, 1, Ac, A.update_actor ? (c == 0 ? Qt0 : Qt1).W1 : nullptr,
                  A.tau);
+        cp_async_wait_all();
         TD3_MARK(5 + 3 * c);
     }
     if (!A.update_actor) {
@@ -816,8 +833,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     }
 
     // ---- 3. actor: ascend Q1(o_c, pi(o_a)) through the updated Q1's action input, Adam + Polyak
-    __syncthreads();
-    W = fwd_input_layer(actor, Wsm, A.o_a + (int64_t)ag * B * I, I, B, Ab, Bb);
+    input_compute(W, I, B, Ab, Bb);  // (net and input rows staged during critic 1's Adam)
     __syncthreads();
     fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
     __syncthreads();
