@@ -332,12 +332,16 @@ __device__ __forceinline__ void fwd_acc_sw(const float* X, int c0, int nc, const
 // into Y itself (free until the layer's output is stored, after a barrier).  Contains
 // barriers: all threads call it.
 constexpr int kP0 = 92;  // 23 float4s (odd: four consecutive rows hit four bank groups)
-__device__ NetS input_issue(const NetP& n, float* Wsm, const float* X, int I, int B, float* Y, float* P0buf)
+__device__ void input_rows_issue(const float* X, int I, int B, float* Y, float* P0buf)
 {
-    const NetS W = stage_issue(n, Wsm);
     const int K4 = pad4(I) / 4, c1 = min(K4, kP0 / 4);
     stage_cols(X, B, I, 0, 4 * c1, P0buf, kP0);
     if (K4 > c1) stage_cols(X, B, I, kP0, 4 * (K4 - c1), Y, 0);
+}
+__device__ NetS input_issue(const NetP& n, float* Wsm, const float* X, int I, int B, float* Y, float* P0buf)
+{
+    const NetS W = stage_issue(n, Wsm);
+    input_rows_issue(X, I, B, Y, P0buf);
     return W;
 }
 __device__ void input_compute(const NetS& W, int I, int B, float* Y, float* P0buf)
@@ -423,10 +427,10 @@ __device__ __forceinline__ void wgrad(const float* D, const float* X, int ldx, i
     if (ldP < 0) ldP = K;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, jg = lane >> 2, kq = lane & 3;
     const int NC = (K + 15) / 16;
-    if (w >= NC * S) return;
-    const int wc = w % NC, p = w / NC;
+    const bool active = w < NC * S;
+    const int wc = w % NC, p = active ? w / NC : S;
     const int ch = (((B + S - 1) / S) + 3) & ~3;  // ranges start at multiples of 4: s & 3 = unrolled j
-    const int sb = min(B, p * ch), se = min(B, sb + ch);
+    const int sb = min(B, (active ? p : 0) * ch), se = min(B, sb + ch);
     const int c4 = 4 * wc + kq;
     const bool bias = with_bias && wc == 0 && kq == 0;
     // D rows (swizzled, 64): logical slots 2 jg, 2 jg + 1 of row s sit at (2 jg ^ (s & 2)) + {0, 1},
@@ -460,34 +464,46 @@ __device__ __forceinline__ void wgrad(const float* D, const float* X, int ldx, i
 #pragma unroll
             for (int q = 0; q < 4; ++q) bacc[q] = __fadd2_rn(bacc[q], dp[q]);
     };
-    const int se4 = sb + ((se - sb) & ~3);
+    if (active) {
+        const int se4 = sb + ((se - sb) & ~3);
 #pragma unroll 2
-    for (int s4 = sb; s4 < se4; s4 += 4) {
+        for (int s4 = sb; s4 < se4; s4 += 4) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) body(s4 + j, j);
-    }
-    for (int s = se4; s < se; ++s) body(s, s & 3);
-    float* Pp = P + (int64_t)p * kH * ldP;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-            if (4 * c4 + b < K) {
-                Pp[(8 * jg + 2 * q) * ldP + 4 * c4 + b] = acc[q][b].x;
-                Pp[(8 * jg + 2 * q + 1) * ldP + 4 * c4 + b] = acc[q][b].y;
-            }
-    if (bias)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            Pb[p * kH + 8 * jg + 2 * q] = bacc[q].x;
-            Pb[p * kH + 8 * jg + 2 * q + 1] = bacc[q].y;
+            for (int j = 0; j < 4; ++j) body(s4 + j, j);
         }
+        for (int s = se4; s < se; ++s) body(s, s & 3);
+    }
+    // the S ranges' partial tiles are summed into the shared-memory gradient P (row stride ldP)
+    // and Pb in range order (deterministic): range 0 stores, ranges 1 .. S-1 add, a barrier
+    // between.  All threads take part in the barriers.
+    for (int r = 0; r < S; ++r) {
+        if (p == r) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    if (4 * c4 + b < K) {
+                        float* g0 = P + (8 * jg + 2 * q) * ldP + 4 * c4 + b;
+                        float* g1 = g0 + ldP;
+                        *g0 = r ? *g0 + acc[q][b].x : acc[q][b].x;
+                        *g1 = r ? *g1 + acc[q][b].y : acc[q][b].y;
+                    }
+            if (bias)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    float* b0 = Pb + 8 * jg + 2 * q;
+                    b0[0] = r ? b0[0] + bacc[q].x : bacc[q].x;
+                    b0[1] = r ? b0[1] + bacc[q].y : bacc[q].y;
+                }
+        }
+        __syncthreads();
+    }
 }
 
-// Partial output-layer gradients (out <= 4 outputs): P[p][o][k] = sum_{s in range p} d3[s][o]
-// H[s][k], Pb[p][o] = sum d3[s][o], 8 ranges (thread t: k = t & 63, p = t >> 6).  d3 rows of
-// 4 floats.
-__device__ __forceinline__ void wgrad_out(const float* d3, int out, const float* H, int B, float* P, float* Pb)
+// Output-layer gradients (out <= 4 outputs) into shared memory: G[o][k] = sum_s d3[s][o]
+// H[s][k] (row stride 64), Gb[o] = sum_s d3[s][o]; 8 sample ranges (thread t: k = t & 63, range
+// t >> 6) summed in range order with a barrier between (deterministic).  d3 rows of 4 floats.
+__device__ __forceinline__ void wgrad_out(const float* d3, int out, const float* H, int B, float* G, float* Gb)
 {
     const int k = threadIdx.x & 63, p = threadIdx.x >> 6;
     const int ch = (B + 7) / 8, sb = min(B, p * ch), se = min(B, sb + ch);
@@ -503,9 +519,13 @@ __device__ __forceinline__ void wgrad_out(const float* d3, int out, const float*
             bacc[o] += dv[o];
         }
     }
-    for (int o = 0; o < out; ++o) {
-        P[(p * out + o) * kH + k] = acc[o];
-        if (k == 0) Pb[p * out + o] = bacc[o];
+    for (int r = 0; r < 8; ++r) {
+        if (p == r)
+            for (int o = 0; o < out; ++o) {
+                G[o * kH + k] = r ? G[o * kH + k] + acc[o] : acc[o];
+                if (k == 0) Gb[o] = r ? Gb[o] + bacc[o] : bacc[o];
+            }
+        __syncthreads();
     }
 }
 
@@ -579,45 +599,38 @@ __device__ __forceinline__ float block_sum(float x, float* red)
     return t;
 }
 
-// Layout of one net's partial gradients (floats): W1 and b1 with S1 sample ranges, W2/b2
-// with 4, W3/b3 with 8.
-struct PartL {
-    int w1, b1, w2, b2, w3, b3, S1, total;
-};
+// Sample ranges of the input layer's weight gradient: the warps not needed for the column
+// blocks of one staged part (<= kPW / 16 blocks) split the batch.
 __host__ __device__ inline int wg_splits(int in)
 {
-    const int nc = (in + 15) / 16;  // column blocks of one staged part (<= kPW / 16)
+    const int nc = (in + 15) / 16;
     return 16 / (nc < kPW / 16 ? nc : kPW / 16);
 }
-__host__ __device__ inline PartL part_layout(int in, int out)
+
+// Shared-memory gradient of a net in the parameter layout (W1 [64][in], b1, W2, b2, W3, b3).
+struct GradS {
+    float *W1, *b1, *W2, *b2, *W3, *b3;
+};
+__device__ __forceinline__ GradS grad_at(float* p, int in, int out)
 {
-    PartL L;
-    L.S1 = wg_splits(in);
-    int p = 0;
-    L.w1 = p;
-    p += L.S1 * kH * in;
-    L.b1 = p;
-    p += L.S1 * kH;
-    L.w2 = p;
-    p += 4 * kH * kH;
-    L.b2 = p;
-    p += 4 * kH;
-    L.w3 = p;
-    p += 8 * out * kH;
-    L.b3 = p;
-    p += 8 * out;
-    L.total = (p + 3) & ~3;
-    return L;
+    GradS G;
+    G.W1 = p;
+    G.b1 = G.W1 + kH * in;
+    G.W2 = G.b1 + kH;
+    G.b2 = G.W2 + kH * kH;
+    G.W3 = G.b2 + kH;
+    G.b3 = G.W3 + out * kH;
+    return G;
 }
 
 // Backward of a net from its two activation buffers, up to the input layer's delta: Hb =
 // H2 (-> D2 in place), Ha = H1 (-> D1 in place); d3 rows (4 floats) in smem.  Writes the
-// partial gradients of W3/b3 and W2/b2; the caller does W1/b1 (from its input rows).
+// W3/b3 gradient to G3 and the W2/b2 gradient to G2 (shared memory, parameter layout); the
+// caller does W1/b1 (from its input rows).  Ends with a barrier.
 __device__ void net_backward(const NetS& W, int out, const float* d3s, float* Ha, float* Hb, int B, int s, int hf,
-                             const float (&d3)[4], float* part, const PartL& L)
+                             const float (&d3)[4], const GradS& G3, const GradS& G2)
 {
-    wgrad_out(d3s, out, Hb, B, part + L.w3, part + L.b3);
-    __syncthreads();
+    wgrad_out(d3s, out, Hb, B, G3.W3, G3.b3);  // (ends with a barrier)
     if (out == 1) {
         const float d1[1] = {d3[0]};
         out_back<1>(W, Hb, s, hf, d1);
@@ -625,8 +638,7 @@ __device__ void net_backward(const NetS& W, int out, const float* d3s, float* Ha
         out_back<4>(W, Hb, s, hf, d3);
     }
     __syncthreads();
-    wgrad<true>(Hb, Ha, kH, kH, B, 4, part + L.w2, part + L.b2);
-    __syncthreads();
+    wgrad<true>(Hb, Ha, kH, kH, B, 4, G2.W2, G2.b2);  // (ends with a barrier)
     bwd_gemm(Hb, W.W2, Ha, B);
     __syncthreads();
 }
@@ -635,22 +647,21 @@ struct AdamC {
     float lr, b1, b2, r1, r2, eps;  // r1 = 1 / (1 - beta1^t), r2 = 1 / (1 - beta2^t)
 };
 
-// Adam on one parameter segment of n whose gradient is the sum of S partials (stride n) at
-// part (summed in order p = 0 .. S-1); the gradient is also stored to gout (the raw-gradient
-// view).  With tgt != nullptr also the Polyak step of the matching target parameters, tgt <-
-// tau theta_new + (1 - tau) tgt.  Four elements per thread per batch, loads before stores.
-__device__ void adam_seg(float* th, float* m, float* v, const float* part, int S, int n, float* gout, const AdamC& A,
-                         float* tgt, float tau)
+// Adam over n parameters th (flat), gradient g in shared memory (same layout); the gradient is
+// also stored to gout (the raw-gradient view).  With tgt != nullptr also the Polyak step of
+// the matching target parameters, tgt <- tau theta_new + (1 - tau) tgt.  Four elements per
+// thread per batch, loads before stores.
+__device__ void adam_net(float* th, float* m, float* v, const float* g, int n, float* gout, const AdamC& A, float* tgt,
+                         float tau)
 {
     const int T = blockDim.x;
     for (int k0 = threadIdx.x; k0 < n; k0 += 4 * T) {
-        float gk[4], mk[4], vk[4], tk[4], pk[4], pp[4][8];
+        float gk[4], mk[4], vk[4], tk[4], pk[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int k = k0 + u * T;
             const bool in = k < n;
-#pragma unroll
-            for (int p = 0; p < 8; ++p) pp[u][p] = (in && p < S) ? part[p * n + k] : 0.0f;
+            gk[u] = in ? g[k] : 0.0f;
             mk[u] = in ? m[k] : 0.0f;
             vk[u] = in ? v[k] : 0.0f;
             tk[u] = in ? th[k] : 0.0f;
@@ -659,9 +670,6 @@ __device__ void adam_seg(float* th, float* m, float* v, const float* part, int S
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int k = k0 + u * T;
-            gk[u] = pp[u][0];
-#pragma unroll
-            for (int p = 1; p < 8; ++p) gk[u] += pp[u][p];  // (in order; the unused ranges add 0)
             if (k < n) {
                 const float mn = fmaf(A.b1, mk[u], (1.0f - A.b1) * gk[u]);
                 const float vn = fmaf(A.b2, vk[u], (1.0f - A.b2) * gk[u] * gk[u]);
@@ -676,29 +684,12 @@ __device__ void adam_seg(float* th, float* m, float* v, const float* part, int S
     }
 }
 
-// Adam (+ Polyak into tgt when non-null) over a whole net's parameters th (flat layout), moments m, v.
-__device__ void adam_net(float* th, float* m, float* v, float* gout, const float* part, const PartL& L, int in, int out,
-                         const AdamC& A, float* tgt, float tau)
-{
-    const int cnt[6] = {kH * in, kH, kH * kH, kH, out * kH, out};
-    const int po[6] = {L.w1, L.b1, L.w2, L.b2, L.w3, L.b3};
-    const int S[6] = {L.S1, L.S1, 4, 4, 8, 8};
-    int off = 0;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) {
-        adam_seg(th + off, m + off, v + off, part + po[q], S[q], cnt[q], gout + off, A, tgt ? tgt + off : nullptr, tau);
-        off += cnt[q];
-    }
-}
-
 // Scratch per agent (floats): [0, B x 554): the actor's activation rows saved across the Q1
 // pass (H1 at 0, H2 at 64 B: swizzled rows); then the raw gradients [Q1, Q2, actor] of the
-// last update (read by the tests through TD3.grads(): they start at B x 554 floats); then
-// the partial-gradient area of the net being updated.
+// last update (read by the tests through TD3.grads(): they start at B x 554 floats).
 __host__ __device__ inline int64_t td3_scratch_floats(int in_dim, int B)
 {
-    const int pa = part_layout(in_dim, 4).total, pc = part_layout(kCI, 1).total;
-    const int64_t f = (int64_t)B * 554 + 2 * net_size(kCI, 1) + net_size(in_dim, 4) + 4 + (pa > pc ? pa : pc);
+    const int64_t f = (int64_t)B * 554 + 2 * net_size(kCI, 1) + net_size(in_dim, 4);
     return (f + 63) & ~(int64_t)63;  // every agent's scratch 256-byte aligned
 }
 
@@ -734,8 +725,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     float* AH2 = scr + (int64_t)B * kH;
     float* gq0 = scr + (int64_t)B * 554;
     float* ga = gq0 + 2 * nc;
-    float* part = ga + na + ((4 - (na & 3)) & 3);
-    const PartL Lc = part_layout(kCI, 1), La = part_layout(I, 4);
+    const int S1c = wg_splits(kCI), S1a = wg_splits(I);
 
     float* Wsm = sm;
     float* Ab = Wsm + td3_wsm_floats(I);  // [kB][64] swizzled
@@ -743,6 +733,16 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     float* X32 = Bb + kB * kH;            // [kB][32] swizzled critic inputs
     float* D3 = X32 + kB * kCI;           // [kB][4] output-layer deltas
     float* red = D3 + kB * 4;             // [32]
+    // gradients in shared memory (parameter layout): a critic's next to its staged net; the
+    // actor's over its net once that is dead (W2/W3 parts first in X32, free at that point)
+    const GradS Gc = grad_at(Wsm + stage_floats(kCI, 1), kCI, 1);
+    const GradS Ga = grad_at(Wsm, I, 4);
+    GradS Gt;  // (actor W2/b2/W3/b3 staging in X32: contiguous like the parameter layout)
+    Gt.W2 = X32;
+    Gt.b2 = Gt.W2 + kH * kH;
+    Gt.W3 = Gt.b2 + kH;
+    Gt.b3 = Gt.W3 + 4 * kH;
+    Gt.W1 = Gt.b1 = nullptr;
 
 #ifdef L2F_TD3_TIMING
     long long mark[16] = {};
@@ -811,19 +811,23 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         const float loss = block_sum(lead ? e * e / (float)B : 0.0f, red);  // (its barriers publish D3)
         if (threadIdx.x == 0) A.losses[ag * 3 + c] = loss;
         TD3_MARK(3 + 3 * c);
-        net_backward(W, 1, D3, Ab, Bb, B, s, hf, d3, part, Lc);
-        wgrad<true>(Ab, X32, kCI, kCI, B, Lc.S1, part + Lc.w1, part + Lc.b1);
-        __syncthreads();
+        net_backward(W, 1, D3, Ab, Bb, B, s, hf, d3, Gc, Gc);
+        wgrad<true>(Ab, X32, kCI, kCI, B, S1c, Gc.W1, Gc.b1);  // (ends with a barrier)
         TD3_MARK(4 + 3 * c);
         // prefetch the next phase's shared-memory operands under Adam's HBM traffic: critic 1's
-        // net, or the actor net + input rows (free regions; none of them is updated by this Adam)
+        // net (beside the gradient this Adam reads), or the actor's input rows (free buffers;
+        // nothing prefetched is updated by this Adam)
         if (c == 0)
             W = stage_issue(Q1, Wsm);
         else if (A.update_actor)
-            W = input_issue(actor, Wsm, A.o_a + (int64_t)ag * B * I, I, B, Ab, Bb);
+            input_rows_issue(A.o_a + (int64_t)ag * B * I, I, B, Ab, Bb);
         float* mc = m_a + 2 * na + 2 * c * nc;
-        adam_net(Qc.W1, mc, mc + nc, gq0 + c * nc, part, Lc, kCI, 1, Ac, A.update_actor ? (c == 0 ? Qt0 : Qt1).W1 : nullptr,
+        adam_net(Qc.W1, mc, mc + nc, Gc.W1, nc, gq0 + c * nc, Ac, A.update_actor ? (c == 0 ? Qt0 : Qt1).W1 : nullptr,
                  A.tau);
+        if (c == 1 && A.update_actor) {
+            __syncthreads();  // (every thread's Adam has read the gradient next to the net region)
+            W = stage_issue(actor, Wsm);
+        }
         cp_async_wait_all();
         TD3_MARK(5 + 3 * c);
     }
@@ -833,7 +837,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     }
 
     // ---- 3. actor: ascend Q1(o_c, pi(o_a)) through the updated Q1's action input, Adam + Polyak
-    input_compute(W, I, B, Ab, Bb);  // (net and input rows staged during critic 1's Adam)
+    input_compute(W, I, B, Ab, Bb);  // (input rows staged during critic 1's Adam)
     __syncthreads();
     fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
     __syncthreads();
@@ -897,21 +901,22 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         st4(Bb + 4 * e, ld4(AH2 + 4 * e));
     }
     __syncthreads();
-    net_backward(W, 4, D3, Ab, Bb, B, s, hf, d3a, part, La);
+    net_backward(W, 4, D3, Ab, Bb, B, s, hf, d3a, Gt, Gt);  // (W2/W3 gradients into X32)
+    // the actor net is dead now: its W2/b2/W3/b3 gradient moves next to where W1's goes
+    for (int e = threadIdx.x; e < (kH * kH + kH + 4 * kH + 4) / 4; e += blockDim.x) st4(Ga.W2 + 4 * e, ld4(Gt.W2 + 4 * e));
     for (int k0 = 0; k0 < I; k0 += kPW) {  // W1/b1 from staged column parts of o_a (into Bb + X32)
         const int w = min(kPW, pad4(I) - k0);
-        if (k0 > 0) __syncthreads();
+        __syncthreads();
         stage_cols(A.o_a + (int64_t)ag * B * I, B, I, k0, w, Bb);
         cp_async_wait_all();
         __syncthreads();
-        wgrad<false>(Ab, Bb, kPLd, min(w, I - k0), B, La.S1, part + La.w1 + k0, part + La.b1, I, k0 == 0);
+        wgrad<false>(Ab, Bb, kPLd, min(w, I - k0), B, S1a, Ga.W1 + k0, Ga.b1, I, k0 == 0);  // (ends with a barrier)
     }
-    __syncthreads();
     const float loss = block_sum(lossa, red);
     if (threadIdx.x == 0) A.losses[ag * 3 + 2] = loss;
     TD3_MARK(11);
     const AdamC Aa{A.lr_actor, A.beta1, A.beta2, 1.0f / A.c1_actor, 1.0f / A.c2_actor, A.adam_eps};
-    adam_net(actor.W1, m_a, v_a, ga, part, La, I, 4, Aa, actor_t.W1, A.tau);  // ---- 4. with the actor target's Polyak step
+    adam_net(actor.W1, m_a, v_a, Ga.W1, na, ga, Aa, actor_t.W1, A.tau);  // ---- 4. with the actor target's Polyak step
     TD3_MARK(12);
 #ifdef L2F_TD3_TIMING
     if (blockIdx.x == 0 && threadIdx.x == 0) {
