@@ -225,6 +225,12 @@ __device__ NetS stage(const NetP& n, float* sm)
     return S;
 }
 
+// Warp w reads and writes only the rows [16 w, 16 w + 16) of the activation buffers in every
+// per-sample step (forward and delta GEMMs, output layer, critic-input rows): between two such
+// steps a warp barrier suffices; the CTA barrier is needed only around the weight-gradient
+// reductions (all rows), staging and restaging of the shared net, and the row save/restore.
+__device__ __forceinline__ void own_rows_sync() { __syncwarp(); }
+
 // ---- CTA-wide batch GEMMs over the activation rows (no barriers inside) ----
 
 // Y = act(X W^T + b) for a 64-output layer, W rows of stride ldw (K4 float4 chunks, zero
@@ -357,7 +363,7 @@ __device__ void input_compute(const NetS& W, int I, int B, float* Y, float* P0bu
         fwd_acc(XSp{P0buf, kP0}, 0, c1, W.W1, W.ld1, acc);
         if (K4 > c1) fwd_acc_sw(Y, c1, K4 - c1, W.W1, W.ld1, acc);
     }
-    __syncthreads();  // (Y held the second part)
+    own_rows_sync();  // (Y held the second part: the warp's own rows)
     TD3_SUB(1);
     if (busy) fwd_store(acc, Y, true);
 }
@@ -751,10 +757,10 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     // ---- 1. target: a' = clip(pi'(o_a') + clip(sigma eps, -c, c), -1, 1); y = r + g (1-d) min Q'
     TD3_SUB(8);
     NetS W = fwd_input_layer(actor_t, Wsm, A.o_a2 + (int64_t)ag * B * I, I, B, Ab, Bb);
-    __syncthreads();
+    own_rows_sync();
     TD3_SUB(9);
     fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
-    __syncthreads();
+    own_rows_sync();
     TD3_SUB(10);
     {
         float at4[4];
@@ -775,15 +781,15 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     for (int c = 0; c < 2; ++c) {
         const NetS& Wc = c == 0 ? Wt0 : Wt1;
         fwd_gemm(X32, kCI, Wc.W1, Wc.ld1, Wc.b1, Ab, B);
-        __syncthreads();
+        own_rows_sync();
         fwd_gemm(Ab, kH, Wc.W2, kLd2, Wc.b2, Bb, B);
-        __syncthreads();
+        own_rows_sync();
         float q[1];
         out_layer<1>(Wc, Bb, s, hf, q);
         qmin = c == 0 ? q[0] : fminf(qmin, q[0]);
     }
     const float y = __ldg(A.r + rb) + A.gamma * (1.0f - __ldg(A.done + rb)) * qmin;
-    __syncthreads();
+    own_rows_sync();
     {  // the critic input rows (o_c, a), shared by both critics
         float a4[4];
 #pragma unroll
@@ -800,9 +806,9 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         const NetP& Qc = c == 0 ? Q0 : Q1;
         __syncthreads();
         fwd_gemm(X32, kCI, W.W1, W.ld1, W.b1, Ab, B);
-        __syncthreads();
+        own_rows_sync();
         fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
-        __syncthreads();
+        own_rows_sync();
         float q[1];
         out_layer<1>(W, Bb, s, hf, q);
         const float e = q[0] - y;
@@ -838,26 +844,30 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
 
     // ---- 3. actor: ascend Q1(o_c, pi(o_a)) through the updated Q1's action input, Adam + Polyak
     input_compute(W, I, B, Ab, Bb);  // (input rows staged during critic 1's Adam)
-    __syncthreads();
+    own_rows_sync();
     fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
-    __syncthreads();
+    own_rows_sync();
     float ap[4];
     out_layer<4>(W, Bb, s, hf, ap);
 #pragma unroll
     for (int k = 0; k < 4; ++k) ap[k] = tanhf(ap[k]);
     put_critic_row(X32, s, hf, A.o_c + rb * 28, ap);  // (o_c, pi(o_a))
-    for (int e = threadIdx.x; e < B * kH / 4; e += blockDim.x) {  // save the actor's H1, H2 rows
-        st4(AH1 + 4 * e, ld4(Ab + 4 * e));
-        st4(AH2 + 4 * e, ld4(Bb + 4 * e));
+    const int wr0 = 16 * (threadIdx.x >> 5), lane = threadIdx.x & 31;  // the warp's own rows
+    for (int e = lane; e < 16 * kH / 4; e += 32) {  // save the actor's H1, H2 rows
+        const int off = wr0 * kH + 4 * e;
+        if (wr0 + (4 * e) / kH < B) {
+            st4(AH1 + off, ld4(Ab + off));
+            st4(AH2 + off, ld4(Bb + off));
+        }
     }
     __syncthreads();
     W = stage(Q0, Wsm);  // the updated Q1
     __syncthreads();
     TD3_MARK(9);
     fwd_gemm(X32, kCI, W.W1, W.ld1, W.b1, Ab, B);
-    __syncthreads();
+    own_rows_sync();
     fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
-    __syncthreads();
+    own_rows_sync();
     float lossa;
     {
         float q[1];
@@ -866,9 +876,9 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         const float d3[1] = {-1.0f / (float)B};
         out_back<1>(W, Bb, s, hf, d3);
     }
-    __syncthreads();
+    own_rows_sync();
     bwd_gemm(Bb, W.W2, Ab, B);
-    __syncthreads();
+    own_rows_sync();
     float d3a[4];
     {  // dL/da = (W1^T d1)[28..31], d3a = dL/da (1 - a^2): my 32 rows of W1, pair-summed
         float da[4] = {0.f, 0.f, 0.f, 0.f};
@@ -896,9 +906,12 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
     __syncthreads();
     TD3_MARK(10);
     W = stage(actor, Wsm);
-    for (int e = threadIdx.x; e < B * kH / 4; e += blockDim.x) {  // restore the actor's H1, H2 rows
-        st4(Ab + 4 * e, ld4(AH1 + 4 * e));
-        st4(Bb + 4 * e, ld4(AH2 + 4 * e));
+    for (int e = lane; e < 16 * kH / 4; e += 32) {  // restore the actor's H1, H2 rows
+        const int off = wr0 * kH + 4 * e;
+        if (wr0 + (4 * e) / kH < B) {
+            st4(Ab + off, ld4(AH1 + off));
+            st4(Bb + off, ld4(AH2 + off));
+        }
     }
     __syncthreads();
     net_backward(W, 4, D3, Ab, Bb, B, s, hf, d3a, Gt, Gt);  // (W2/W3 gradients into X32)
