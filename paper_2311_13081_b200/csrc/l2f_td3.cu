@@ -191,30 +191,38 @@ __device__ void copy_rows(const float* g, int rows, int cols, int gs, float* d, 
 
 // CTA-cooperative copy of a net into shared memory at sm (16-byte aligned): issues the
 // copies (stage_issue) or issues and waits for this thread's (stage); caller syncs.
-__device__ NetS stage_issue(const NetP& n, float* sm)
+__device__ __forceinline__ NetS stage_view(int in, int out, float* sm)  // where stage_issue puts a net
 {
     NetS S;
-    S.ld1 = ldw_of(n.in);
+    S.ld1 = ldw_of(in);
     float* W1 = sm;
     float* b1 = W1 + kH * S.ld1;
     float* W2 = b1 + kH;
     float* b2 = W2 + kH * kLd2;
     float* W3 = b2 + kH;
-    float* b3 = W3 + n.out * kH;
-    copy_rows(n.W1, kH, n.in, n.in, W1, S.ld1);
-    copy_rows(n.W2, kH, kH, kH, W2, kLd2);
-    copy_rows(n.W3, n.out, kH, kH, W3, kH);
-    for (int e = threadIdx.x; e < 2 * kH + n.out; e += blockDim.x) {
-        const float* src = e < kH ? n.b1 + e : (e < 2 * kH ? n.b2 + (e - kH) : n.b3 + (e - 2 * kH));
-        float* dst = e < kH ? b1 + e : (e < 2 * kH ? b2 + (e - kH) : b3 + (e - 2 * kH));
-        cp_async(dst, src, 4, 4);
-    }
     S.W1 = W1;
     S.b1 = b1;
     S.W2 = W2;
     S.b2 = b2;
     S.W3 = W3;
-    S.b3 = b3;
+    S.b3 = W3 + out * kH;
+    return S;
+}
+
+__device__ NetS stage_issue(const NetP& n, float* sm)
+{
+    const NetS S = stage_view(n.in, n.out, sm);
+    copy_rows(n.W1, kH, n.in, n.in, const_cast<float*>(S.W1), S.ld1);
+    copy_rows(n.W2, kH, kH, kH, const_cast<float*>(S.W2), kLd2);
+    copy_rows(n.W3, n.out, kH, kH, const_cast<float*>(S.W3), kH);
+    float* b1 = const_cast<float*>(S.b1);
+    float* b2 = const_cast<float*>(S.b2);
+    float* b3 = const_cast<float*>(S.b3);
+    for (int e = threadIdx.x; e < 2 * kH + n.out; e += blockDim.x) {
+        const float* src = e < kH ? n.b1 + e : (e < 2 * kH ? n.b2 + (e - kH) : n.b3 + (e - 2 * kH));
+        float* dst = e < kH ? b1 + e : (e < 2 * kH ? b2 + (e - kH) : b3 + (e - 2 * kH));
+        cp_async(dst, src, 4, 4);
+    }
     return S;
 }
 
@@ -844,6 +852,16 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
 
     // ---- 3. actor: ascend Q1(o_c, pi(o_a)) through the updated Q1's action input, Adam + Polyak
     input_compute(W, I, B, Ab, Bb);  // (input rows staged during critic 1's Adam)
+    const NetS Wa = W;
+    // Q1 (the updated Q0 net) is staged under the actor's second layer where that leaves the
+    // actor's W2/W3 intact for its backward: after the actor net, or over its (now dead) W1
+    const int wsz = td3_wsm_floats(I), asz = stage_floats(I, 4), csz = stage_floats(kCI, 1);
+    const int qoff = asz + csz <= wsz ? asz : (kH * ldw_of(I) + kH >= csz ? 0 : -1);
+    NetS Wq;
+    if (qoff >= 0) {
+        __syncthreads();  // (every warp is done with the actor's W1)
+        Wq = stage_issue(Q0, Wsm + qoff);
+    }
     own_rows_sync();
     fwd_gemm(Ab, kH, W.W2, kLd2, W.b2, Bb, B);
     own_rows_sync();
@@ -860,9 +878,13 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
             st4(AH2 + off, ld4(Bb + off));
         }
     }
+    if (qoff < 0) {
+        __syncthreads();
+        Wq = stage_issue(Q0, Wsm);
+    }
+    cp_async_wait_all();
     __syncthreads();
-    W = stage(Q0, Wsm);  // the updated Q1
-    __syncthreads();
+    W = Wq;  // the updated Q1
     TD3_MARK(9);
     fwd_gemm(X32, kCI, W.W1, W.ld1, W.b1, Ab, B);
     own_rows_sync();
@@ -903,9 +925,14 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         }
         if (lead) st4(D3 + 4 * s, make_float4(d3a[0], d3a[1], d3a[2], d3a[3]));
     }
-    __syncthreads();
+    if (qoff < 0) {  // (the Q1 staging overwrote the actor's W2/W3)
+        __syncthreads();
+        W = stage(actor, Wsm);
+    } else {
+        own_rows_sync();
+        W = Wa;
+    }
     TD3_MARK(10);
-    W = stage(actor, Wsm);
     for (int e = lane; e < 16 * kH / 4; e += 32) {  // restore the actor's H1, H2 rows
         const int off = wr0 * kH + 4 * e;
         if (wr0 + (4 * e) / kH < B) {
