@@ -20,11 +20,13 @@
 // consecutive weight rows start in eight different bank groups).  A thread owns a 4-sample x
 // 8-output register tile: per 4-input chunk it loads 4 activation float4s and 8 weight float4s
 // for 128 FMAs (the thread-per-sample formulation loads a weight float4 per 4 FMAs and is
-// shared-memory bound).  Backward deltas are the same GEMM against W2 (in place, masked by
-// ReLU'), weight gradients 8 x 4 tiles reduced over a warp's sample range with the partial
-// sums of the ranges combined by the Adam pass (deterministic order).  The actor input rows
-// (in_dim floats, the one operand that does not fit) are staged in column parts with cp.async
-// into the activation buffers that are free at that point.
+// shared-memory bound; the pairs feed packed FFMA2).  Backward deltas are the same GEMM
+// against W2 (in place, masked by ReLU'); weight gradients are 8 x 4 tiles over a warp's
+// sample range, the ranges summed into a shared-memory gradient block in fixed order
+// (deterministic), which Adam reads.  A warp owns the rows of its 16 samples in every
+// per-sample step, so those steps need only warp barriers.  Nets and the actor input rows
+// (in_dim floats, the one operand that does not fit) are staged by cp.async, the input rows
+// in column parts into whichever activation buffers are free at that point.
 #include <cmath>
 #include <cstdio>
 
