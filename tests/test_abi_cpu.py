@@ -103,3 +103,29 @@ def test_td3_sizes_and_validation(L):
     assert L.l2f_td3_sizes(156, 1, C.byref(blk), C.byref(sb)) == 0
     for bad in ((157, 256), (0, 256), (146, 0), (146, 257)):
         assert L.l2f_td3_sizes(bad[0], bad[1], C.byref(blk), C.byref(sb)) == 1, bad
+
+
+def test_td3_update_validates_before_touching_the_gpu(L):
+    """NULL buffers, zero agents, Adam step 0 and out-of-range hyper-parameters are rejected on
+    the host (INVALID_ARGUMENT) -- no device call is made, so this runs without a GPU."""
+    from paper_2311_13081_b200.abi import TD3Batch, TD3Hyper
+    h = TD3Hyper(gamma=0.99, tau=0.005, sigma_t=0.2, clip_t=0.5, lr_actor=3e-4, lr_critic=3e-4, beta1=0.9,
+                 beta2=0.999, eps=1e-8)
+    fake = C.c_void_p(0x1000)
+    b = TD3Batch(*([0x1000] * 8))
+
+    def call(params=fake, n=4, in_dim=146, batch=256, batch_s=b, hyper=h, tc=1, ta=1, upd=1):
+        return L.l2f_td3_update(params, n, in_dim, batch, C.byref(batch_s), C.byref(hyper), tc, ta, upd, fake, fake,
+                                None)
+
+    assert call(params=None) == 1
+    assert call(n=0) == 1
+    assert call(in_dim=157) == 1
+    assert call(tc=0) == 1
+    assert call(ta=0, upd=1) == 1
+    bad = TD3Batch(*([0x1000] * 7 + [None]))
+    assert call(batch_s=bad) == 1
+    for k, v in (("gamma", 1.5), ("tau", -0.1), ("beta1", 1.0), ("eps", 0.0)):
+        hh = TD3Hyper(**{f: getattr(h, f) for f, _ in TD3Hyper._fields_})
+        setattr(hh, k, v)
+        assert call(hyper=hh) == 1, k
