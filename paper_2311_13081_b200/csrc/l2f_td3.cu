@@ -47,6 +47,12 @@ constexpr int kLd2 = 68;    // staged W2 row stride (17 float4s)
 #ifndef L2F_TD3_UNROLL
 #define L2F_TD3_UNROLL 1  // unroll of the GEMM chunk loops (1: 6.23e5, 2: 6.09e5, 4: 5.84e5 updates/s; spills grow)
 #endif
+#ifndef L2F_TD3_UNROLL_BWD
+#define L2F_TD3_UNROLL_BWD L2F_TD3_UNROLL
+#endif
+#ifndef L2F_TD3_UNROLL_WG
+#define L2F_TD3_UNROLL_WG 2  // the weight-gradient sample loop (4 samples per trip)
+#endif
 #define L2F_TD3_STR(x) #x
 #define L2F_TD3_PRAGMA(x) _Pragma(L2F_TD3_STR(x))
 #define L2F_TD3_PRAGMA_UNROLL L2F_TD3_PRAGMA(unroll L2F_TD3_UNROLL)
@@ -403,7 +409,7 @@ __device__ __forceinline__ void bwd_gemm(const float* D, const float* W2, float*
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[i][q] = make_float2(0.0f, 0.0f);
-L2F_TD3_PRAGMA_UNROLL
+L2F_TD3_PRAGMA(unroll L2F_TD3_UNROLL_BWD)
     for (int c = 0; c < kH / 4; ++c) {
         float4 d[4];
         const float* dc = D + s0 * kH + 4 * (c ^ g);  // (rows s0 + 4 i share the key g)
@@ -489,7 +495,7 @@ __device__ __forceinline__ void wgrad(const float* D, const float* X, int ldx, i
     };
     if (active) {
         const int se4 = sb + ((se - sb) & ~3);
-L2F_TD3_PRAGMA_UNROLL
+L2F_TD3_PRAGMA(unroll L2F_TD3_UNROLL_WG)
         for (int s4 = sb; s4 < se4; s4 += 4) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) body(s4 + j, j);
