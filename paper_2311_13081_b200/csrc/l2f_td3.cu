@@ -451,7 +451,8 @@ L2F_TD3_PRAGMA(unroll L2F_TD3_UNROLL_BWD)
 // partial ranges are summed by the Adam pass (fixed order).
 template <bool SWX>
 __device__ __forceinline__ void wgrad(const float* D, const float* X, int ldx, int K, int B, int S, float* P,
-                                      float* Pb, int ldP = -1, bool with_bias = true)
+                                      float* Pb, int ldP = -1, bool with_bias = true, float* tmp = nullptr,
+                                      float* tmpb = nullptr)
 {
     if (ldP < 0) ldP = K;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, jg = lane >> 2, kq = lane & 3;
@@ -503,8 +504,43 @@ L2F_TD3_PRAGMA(unroll L2F_TD3_UNROLL_WG)
         for (int s = se4; s < se; ++s) body(s, s & 3);
     }
     // the S ranges' partial tiles are summed into the shared-memory gradient P (row stride ldP)
-    // and Pb in range order (deterministic): range 0 stores, ranges 1 .. S-1 add, a barrier
-    // between.  All threads take part in the barriers.
+    // and Pb in range order (deterministic).  With a free buffer (tmp: S x 64 x K, tmpb: S x 64)
+    // every range writes its partial tile at once and one pass sums them after one barrier;
+    // otherwise range 0 stores and ranges 1 .. S-1 add, a barrier between.  All threads take
+    // part in the barriers.
+    if (tmp) {
+        if (p < S) {
+            float* t0 = tmp + p * kH * K;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    if (4 * c4 + b < K) {
+                        t0[(8 * jg + 2 * q) * K + 4 * c4 + b] = acc[q][b].x;
+                        t0[(8 * jg + 2 * q + 1) * K + 4 * c4 + b] = acc[q][b].y;
+                    }
+            if (bias)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    tmpb[p * kH + 8 * jg + 2 * q] = bacc[q].x;
+                    tmpb[p * kH + 8 * jg + 2 * q + 1] = bacc[q].y;
+                }
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < kH * K + (with_bias ? kH : 0); e += blockDim.x) {
+            const bool wgt = e < kH * K;
+            const float* src = wgt ? tmp + e : tmpb + (e - kH * K);
+            const int st = wgt ? kH * K : kH;
+            float v = src[0];
+            for (int r = 1; r < S; ++r) v += src[r * st];
+            if (wgt)
+                P[(e / K) * ldP + e % K] = v;
+            else
+                Pb[e - kH * K] = v;
+        }
+        __syncthreads();
+        return;
+    }
     for (int r = 0; r < S; ++r) {
         if (p == r) {
 #pragma unroll
@@ -530,9 +566,11 @@ L2F_TD3_PRAGMA(unroll L2F_TD3_UNROLL_WG)
 }
 
 // Output-layer gradients (out <= 4 outputs) into shared memory: G[o][k] = sum_s d3[s][o]
-// H[s][k] (row stride 64), Gb[o] = sum_s d3[s][o]; 8 sample ranges (thread t: k = t & 63, range
-// t >> 6) summed in range order with a barrier between (deterministic).  d3 rows of 4 floats.
-__device__ __forceinline__ void wgrad_out(const float* d3, int out, const float* H, int B, float* G, float* Gb)
+// H[s][k] (row stride 64) and, contiguous after it, Gb[o] = sum_s d3[s][o]; 8 sample ranges
+// (thread t: k = t & 63, range t >> 6) write their partial rows to tmp (8 x (64 out + out)
+// floats), one barrier, then one pass sums them in range order (deterministic).  H is no
+// longer read after the barrier; G is complete only after the caller's next barrier.
+__device__ __forceinline__ void wgrad_out(const float* d3, int out, const float* H, int B, float* G, float* tmp)
 {
     const int k = threadIdx.x & 63, p = threadIdx.x >> 6;
     const int ch = (B + 7) / 8, sb = min(B, p * ch), se = min(B, sb + ch);
@@ -548,13 +586,16 @@ __device__ __forceinline__ void wgrad_out(const float* d3, int out, const float*
             bacc[o] += dv[o];
         }
     }
-    for (int r = 0; r < 8; ++r) {
-        if (p == r)
-            for (int o = 0; o < out; ++o) {
-                G[o * kH + k] = r ? G[o * kH + k] + acc[o] : acc[o];
-                if (k == 0) Gb[o] = r ? Gb[o] + bacc[o] : bacc[o];
-            }
-        __syncthreads();
+    const int rl = out * kH + out;
+    for (int o = 0; o < out; ++o) {
+        tmp[p * rl + o * kH + k] = acc[o];
+        if (k == 0) tmp[p * rl + out * kH + o] = bacc[o];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < rl; e += blockDim.x) {
+        float v = tmp[e];
+        for (int r = 1; r < 8; ++r) v += tmp[r * rl + e];
+        G[e] = v;
     }
 }
 
@@ -657,9 +698,9 @@ __device__ __forceinline__ GradS grad_at(float* p, int in, int out)
 // W3/b3 gradient to G3 and the W2/b2 gradient to G2 (shared memory, parameter layout); the
 // caller does W1/b1 (from its input rows).  Ends with a barrier.
 __device__ void net_backward(const NetS& W, int out, const float* d3s, float* Ha, float* Hb, int B, int s, int hf,
-                             const float (&d3)[4], const GradS& G3, const GradS& G2)
+                             const float (&d3)[4], const GradS& G3, const GradS& G2, float* tmp)
 {
-    wgrad_out(d3s, out, Hb, B, G3.W3, G3.b3);  // (ends with a barrier)
+    wgrad_out(d3s, out, Hb, B, G3.W3, tmp);  // (G3.b3 follows G3.W3; Hb free after its barrier)
     if (out == 1) {
         const float d1[1] = {d3[0]};
         out_back<1>(W, Hb, s, hf, d1);
@@ -724,8 +765,12 @@ __host__ __device__ inline int64_t td3_scratch_floats(int in_dim, int B)
 
 __host__ __device__ inline int td3_wsm_floats(int in_dim)
 {
+    // the larger of: the actor net; both critic nets; a critic net + its gradient + the
+    // output-layer gradient scratch (8 x 65 floats, wgrad_out)
     const int a = stage_floats(in_dim, 4), c = 2 * stage_floats(kCI, 1);
-    return pad4(a > c ? a : c);
+    const int g = stage_floats(kCI, 1) + net_size(kCI, 1) + 4 + 8 * (kH + 1);
+    const int m = a > c ? a : c;
+    return pad4(m > g ? m : g);
 }
 
 __host__ __device__ inline int64_t td3_smem_floats(int in_dim)
@@ -840,8 +885,9 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         const float loss = block_sum(lead ? e * e / (float)B : 0.0f, red);  // (its barriers publish D3)
         if (threadIdx.x == 0) A.losses[ag * 3 + c] = loss;
         TD3_MARK(3 + 3 * c);
-        net_backward(W, 1, D3, Ab, Bb, B, s, hf, d3, Gc, Gc);
-        wgrad<true>(Ab, X32, kCI, kCI, B, S1c, Gc.W1, Gc.b1);  // (ends with a barrier)
+        net_backward(W, 1, D3, Ab, Bb, B, s, hf, d3, Gc, Gc, Gc.b3 + 4);  // (scratch after the gradient)
+        // W1/b1: the ranges' partial tiles into the dead D2 buffer (Bb) and D3, one pass sums them
+        wgrad<true>(Ab, X32, kCI, kCI, B, S1c, Gc.W1, Gc.b1, -1, true, Bb, D3);  // (ends with a barrier)
         TD3_MARK(4 + 3 * c);
         // prefetch the next phase's shared-memory operands under Adam's HBM traffic: critic 1's
         // net (beside the gradient this Adam reads), or the actor's input rows (free buffers;
@@ -956,7 +1002,7 @@ __global__ void __launch_bounds__(kT, 1) td3_update_kernel(TD3Dev A)
         }
     }
     __syncthreads();
-    net_backward(W, 4, D3, Ab, Bb, B, s, hf, d3a, Gt, Gt);  // (W2/W3 gradients into X32)
+    net_backward(W, 4, D3, Ab, Bb, B, s, hf, d3a, Gt, Gt, Gt.b3 + 4);  // (W2/W3 gradients into X32)
     // the actor net is dead now: its W2/b2/W3/b3 gradient moves next to where W1's goes
     for (int e = threadIdx.x; e < (kH * kH + kH + 4 * kH + 4) / 4; e += blockDim.x) st4(Ga.W2 + 4 * e, ld4(Gt.W2 + 4 * e));
     for (int k0 = 0; k0 < I; k0 += kPW) {  // W1/b1 from staged column parts of o_a (into Bb + X32)
