@@ -2,9 +2,33 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <cstdint>
+
 #include "l2f_device.cuh"
 
 namespace l2f {
+
+// Per-device bookkeeping of host launchers (function attributes and SM counts are per device;
+// a process may drive several).  Device ordinals < 64.
+inline int current_device()
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev & 63;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `func` on the current device once per
+// requested size: `done` holds the largest size set so far on each device.
+template <class F>
+inline cudaError_t ensure_smem_attr(F* func, size_t bytes, std::atomic<size_t> (&done)[64])
+{
+    const int dev = current_device();
+    if (done[dev].load() >= bytes) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done[dev].store(bytes);
+    return e;
+}
 
 #ifndef L2F_STEP_BLOCK
 #define L2F_STEP_BLOCK 128  // step-kernel block (measured at C3: 64 -> 88.2 us, 128 -> 87.0, 256 -> 91.4)

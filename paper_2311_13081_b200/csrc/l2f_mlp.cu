@@ -808,11 +808,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 int sm_count()
 {
-    static int n = 0;
+    static std::atomic<int> cache[64] = {};
+    const int dev = current_device();
+    int n = cache[dev].load();
     if (n == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
         if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+        cache[dev].store(n);
     }
     return n;
 }
@@ -839,16 +840,10 @@ cudaError_t launch_rollout_mlp(const DevParams& P, const DevBufs& B, const Polic
                                const int64_t* trace_ids, int32_t K, cudaStream_t s)
 {
     if (P.n_hist % 4 != 0 || W.hidden != kHid || W.in_dim != 18 + 4 * P.n_hist) return cudaErrorNotSupported;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e =
-            cudaFuncSetAttribute(rollout_mlp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(rollout_mlp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kSmemBytes);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<size_t> attr_t[64] = {}, attr_f[64] = {};
+    cudaError_t e = ensure_smem_attr(rollout_mlp_kernel<true>, kSmemBytes, attr_t);
+    if (e == cudaSuccess) e = ensure_smem_attr(rollout_mlp_kernel<false>, kSmemBytes, attr_f);
+    if (e != cudaSuccess) return e;
     const int n_units = (int)units_for(P.n);
     if (P.flags & F_DOMAIN_RAND)
         rollout_mlp_kernel<true><<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, n_units);
@@ -861,12 +856,9 @@ cudaError_t launch_track_mlp(const DevParams& P, const DevBufs& B, const PolicyD
                              cudaStream_t s)
 {
     if (P.n_hist % 4 != 0 || W.hidden != kHid || W.in_dim != 18 + 4 * P.n_hist) return cudaErrorNotSupported;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(track_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<size_t> attr[64] = {};
+    const cudaError_t e = ensure_smem_attr(track_mlp_kernel, kSmemBytes, attr);
+    if (e != cudaSuccess) return e;
     track_mlp_kernel<<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, S, (int32_t)units_for(P.n));
     return cudaGetLastError();
 }
@@ -874,13 +866,9 @@ cudaError_t launch_track_mlp(const DevParams& P, const DevBufs& B, const PolicyD
 cudaError_t launch_policy_forward(const PolicyDev& W, const float* obs, float* act, int64_t n, cudaStream_t s)
 {
     if ((W.in_dim - 18) % 16 != 0 || W.hidden != kHid) return cudaErrorNotSupported;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e =
-            cudaFuncSetAttribute(policy_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<size_t> attr[64] = {};
+    const cudaError_t e = ensure_smem_attr(policy_forward_kernel, kSmemBytes, attr);
+    if (e != cudaSuccess) return e;
     policy_forward_kernel<<<grid_for(n), kThreads, kSmemBytes, s>>>(W, obs, act, n, (int32_t)units_for(n));
     return cudaGetLastError();
 }

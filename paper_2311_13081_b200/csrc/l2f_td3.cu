@@ -1058,12 +1058,9 @@ cudaError_t launch_td3_update(const TD3Dev& A, cudaStream_t s)
 {
     if (A.B < 1 || A.B > kB || A.in_dim < 1 || A.in_dim > kMaxIn) return cudaErrorNotSupported;
     const size_t smem = (size_t)td3_smem_floats(A.in_dim) * sizeof(float);
-    static size_t attr = 0;
-    if (smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(td3_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = smem;
-    }
+    static std::atomic<size_t> attr[64] = {};
+    const cudaError_t e = ensure_smem_attr(td3_update_kernel, smem, attr);
+    if (e != cudaSuccess) return e;
     td3_update_kernel<<<A.n_agents, kT, smem, s>>>(A);
     return cudaGetLastError();
 }
