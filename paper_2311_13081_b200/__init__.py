@@ -361,8 +361,14 @@ class TD3:
     def update(self, batch: dict, update_actor: bool, stream=None):
         """One update of every agent; batch tensors [A][B][...] fp32 on the device."""
         from .abi import TD3Batch
-        keep = {k: batch[k].to(device=self.device, dtype=torch.float32).contiguous()
-                for k in ("o_a", "o_c", "a", "r", "o_a2", "o_c2", "done", "eps")}
+        A, B, I = self.A, self.B, self.in_dim
+        shapes = {"o_a": (A, B, I), "o_c": (A, B, 28), "a": (A, B, 4), "r": (A, B), "o_a2": (A, B, I),
+                  "o_c2": (A, B, 28), "done": (A, B), "eps": (A, B, 4)}
+        for k, shp in shapes.items():
+            if tuple(batch[k].shape) != shp:
+                raise ValueError(f"TD3 batch[{k!r}] has shape {tuple(batch[k].shape)}, expected {shp}")
+        keep = {k: batch[k].to(device=self.device, dtype=torch.float32).contiguous() for k in shapes}
+        self._keep = keep  # (converted copies stay alive while the asynchronous update reads them)
         b = TD3Batch(**{k: v.data_ptr() for k, v in keep.items()})
         self.t_critic += 1
         if update_actor:

@@ -154,6 +154,11 @@ def test_td3_invalid_arguments(pkg):
         pkg.TD3(1, 146, 257)
     with pytest.raises(Exception):
         pkg.TD3(1, 157, 64)  # beyond the kernel's shared-memory plan
+    td3 = pkg.TD3(2, 34, 16)
+    bt = {k: torch.as_tensor(v) for k, v in make_batch(2, 16, 34, 1).items()}
+    bt["o_c"] = bt["o_c"][:, :8]  # wrong batch size
+    with pytest.raises(ValueError):
+        td3.update(bt, update_actor=True)
 
 
 def test_td3_update_is_deterministic(pkg):
