@@ -270,6 +270,7 @@ class Env:
             trace_ids = trace_ids.to(device=self.device, dtype=torch.int64).contiguous()
             K = int(trace_ids.numel())
             trace = torch.zeros(T, K, TRACE_FIELDS, device=self.device)
+        self._keep = (actions, trace_ids)  # (alive while the asynchronous launch reads them)
         _check(lib().l2f_rollout(self.h, C.byref(policy.s) if policy is not None else None, _ptr(actions), int(T),
                                  _ptr(trace), _ptr(trace_ids), K, _stream(stream)), "l2f_rollout")
         return trace
@@ -295,6 +296,7 @@ class Env:
         sp.clip_vel = float(self.cfg.init_vel if clip_vel is None else clip_vel)
         sp.n_steps = int(n_steps)
         sp.rmse, sp.rmse_xy, sp.steps_ok = (out[k].data_ptr() for k in ("rmse", "rmse_xy", "steps_ok"))
+        self._keep = ct  # (alive while the asynchronous launch reads it)
         _check(lib().l2f_track(self.h, C.byref(policy.s), C.byref(sp), _stream(stream)), "l2f_track")
         return out
 
