@@ -174,9 +174,10 @@ def cpu_baseline(cfg, policy_w, target_s=15.0, nthreads=None):
 
 def main_config(n, T, mode, world):
     """The workload both arms report (the reference arm times a bounded sample of it)."""
-    return {"workload": "C5 per-GPU shard: 2^21 envs/GPU x 1000 steps fused actor-MLP rollout "
-                        "(146-64-64-4 tcgen05, N_H=32), obs/action noise, reward + 4-stage "
-                        "curriculum, termination, auto-reset, disturbance; NCCL stat all-reduce",
+    what = ("fused actor-MLP rollout (146-64-64-4 tcgen05, N_H=32)" if mode == "mlp"
+            else "open-loop rollout (Philox random actions, no actor MLP)")
+    return {"workload": f"C5 per-GPU shard: 2^21 envs/GPU x 1000 steps {what}, obs/action noise, reward + "
+                        "4-stage curriculum, termination, auto-reset, disturbance; NCCL stat all-reduce",
             "envs_per_gpu": n, "steps_per_rollout": T, "mode": mode,
             "l2": "inputs larger than L2: env state+history 1.4 GB per GPU",
             "parallelism": f"env-shard x{world}"}
@@ -330,7 +331,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32+f16mma", "data": "synthetic",
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32+f16mma" if args.mode == "mlp" else "f32", "data": "synthetic",
                 "config": main_config(n, T, args.mode, world),
                 "sim_seconds_per_wall_second": value * DT,
                 "roofline": roof,
