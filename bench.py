@@ -96,8 +96,12 @@ class ClockSampler:
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()  # nvidia-smi takes a moment to start: have it sampling before the region
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.first = len(self.lines)  # samples from here on fall inside the timed region
         return self
 
     def _read(self):
@@ -114,7 +118,10 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], None, set()
-        for l in self.lines:
+        # samples taken inside the region; for a region shorter than the 200 ms sampling period,
+        # the sample just before it (the GPU was already warm)
+        lines = self.lines[self.first:] or self.lines[-1:]
+        for l in lines:
             f = [x.strip() for x in l.split(",")]
             if len(f) < 9:
                 continue

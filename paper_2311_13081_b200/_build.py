@@ -15,6 +15,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-ftz=true", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+# Per-source extra flags (overridable per file with L2F_NVCC_<NAME>, e.g. L2F_NVCC_L2F_TD3): ptxas
+# register-usage levels chosen by measurement (scripts/dbg/all_ab.sh).
+PER_SOURCE = {"l2f_mlp.cu": "-Xptxas --register-usage-level=8",  # rollout +0.5-1 %
+              "l2f_td3.cu": "-Xptxas --register-usage-level=3"}  # TD3 +1 %
 
 
 def _stale() -> bool:
@@ -33,8 +37,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     extra = os.environ.get("L2F_NVCC_DEFS", "").split()  # experiments only, e.g. -DL2F_MLP_TILES=4
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o",
-               obj]
+        per = os.environ.get("L2F_NVCC_" + src.replace(".cu", "").upper(), PER_SOURCE.get(src, "")).split()
+        cmd = [NVCC, *ARCH, *FLAGS, *per, *extra, "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src),
+               "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode:
             sys.stderr.write(r.stdout + r.stderr)
