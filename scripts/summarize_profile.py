@@ -74,6 +74,8 @@ for rep in sorted(f for f in os.listdir(src) if f.endswith(".ncu-rep")):
     lines = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "ncu_lines.py"), path, "1", "25"],
                            capture_output=True, text=True).stdout
     out += ["Top CUDA source lines by executed warp-instructions:", "", "```", lines.rstrip(), "```", ""]
+if os.path.exists(os.path.join(dst, "PHASES.md")):
+    out += ["", "Per-phase cycle breakdowns from the debug builds: `PHASES.md` (same directory)."]
 open(os.path.join(dst, "SUMMARY.md"), "w").write("\n".join(out) + "\n")
 import json  # noqa: E402
 json.dump(traffic, open(os.path.join(dst, "traffic.json"), "w"), indent=1)
