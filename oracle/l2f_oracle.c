@@ -511,9 +511,32 @@ void or_mlp(const or_policy* pol, const double* obs, double a[4])
     }
 }
 
+/* Relative distance of x != 0 to the nearest fp16 rounding midpoint (SURVEY 8(c) parity test
+ * 5): the midpoints around x are those of h = |q16(x)| and its two fp16 neighbours, h + u/2
+ * above and h - d/2 below, where u is the spacing above h and d the spacing below it (d = u/2
+ * when h is a normal power of two, where the binade changes; the subnormal spacing 2^-24 also
+ * holds up to and including 2^-14). */
+static double midpoint_margin(double x)
+{
+    double ax = fabs(x), h = fabs(or_q16(x));
+    if (!(ax > 0.0) || isinf(h)) return INFINITY;
+    double up, down;
+    if (h < 6.103515625e-05) {
+        up = down = ldexp(1.0, -24);
+    } else {
+        int e;
+        double m = frexp(h, &e);          /* h = m 2^e, m in [0.5, 1) */
+        up = ldexp(1.0, e - 11);
+        down = (m == 0.5 && h > 6.103515625e-05) ? 0.5 * up : up;
+    }
+    double above = (h + 0.5 * up) - ax, below = h > 0.0 ? ax - (h - 0.5 * down) : INFINITY;
+    return fmin(above, below) / ax;
+}
+
 /* Pre-activation of the three layers, for the "near an fp16 rounding midpoint" exclusion
- * of the teacher-forced parity test.  Returns, for each quantisation
- * point, the minimum relative distance to an fp16 rounding midpoint. */
+ * of the teacher-forced parity test.  Returns, over every quantisation
+ * point (the observation and the positive layer-1/layer-2 pre-activations), the minimum
+ * relative distance to an fp16 rounding midpoint. */
 double or_mlp_min_midpoint_margin(const or_policy* pol, const double* obs)
 {
     int I = pol->in_dim, H = pol->hidden;
@@ -521,14 +544,8 @@ double or_mlp_min_midpoint_margin(const or_policy* pol, const double* obs)
     double worst = INFINITY;
 #define MARGIN(v)                                                                      \
     do {                                                                               \
-        double _v = fabs(v);                                                           \
-        if (_v > 0) {                                                                  \
-            int _e; frexp(_v < 6.103515625e-05 ? 6.103515625e-05 : _v, &_e);           \
-            double _qn = ldexp(1.0, _e - 11);                                          \
-            double _f = _v / _qn - floor(_v / _qn);                                    \
-            double _m = fabs(_f - 0.5) * _qn / _v;                                     \
-            if (_m < worst) worst = _m;                                                \
-        }                                                                              \
+        double _m = midpoint_margin(v);                                                \
+        if (_m < worst) worst = _m;                                                    \
     } while (0)
     for (int i = 0; i < I; ++i) { MARGIN(obs[i]); x0[i] = or_q16(obs[i]); }
     for (int j = 0; j < H; ++j) {

@@ -90,3 +90,64 @@ def near_threshold(so, cfg, extra: float = 0.0) -> bool:
         if abs(m) <= max(1e-6, REL * abs(t) + ABS) + extra:
             return True
     return False
+
+
+class TolStats:
+    """Accounting of the two single-step tolerance readings (Q27, Q36).
+
+    Every compared value is first judged by north_star's bound |err| <= 1e-5 |x| + 1e-6 on the
+    oracle's value x; a value that misses it must meet the widened bound of its reading, and is
+    counted.  State components (Q27): 1e-5 max(|x_t|, |x_t+1|) + 1e-6.  Rewards: the tests
+    require zero widened rewards (north_star's bound holds for every reward measured); the
+    scale S = 2 sum_k |term_k| of the reward's terms on s' is only reported for a failure.
+    Tests bound the widened fraction (round-2 measurement: <= 8 of 170 000 state components,
+    all body rates), so the reading cannot silently absorb a real discrepancy."""
+
+    def __init__(self):
+        self.n_state = self.w_state = self.n_rew = self.w_rew = 0
+        self.examples = []
+
+    def state(self, gpu, ref, prev, tag=None) -> bool:
+        strict = close(gpu, ref)
+        wide = close_step(gpu, ref, prev)
+        self.n_state += strict.size
+        k = int(np.count_nonzero(~strict & wide))
+        self.w_state += k
+        if k and len(self.examples) < 8:
+            self.examples.append((tag, np.flatnonzero(~strict & wide).tolist()))
+        return bool(np.all(wide))
+
+    def reward(self, gpu, ref, scale) -> bool:
+        self.n_rew += 1
+        if close(gpu, ref):
+            return True
+        self.w_rew += 1
+        return abs(float(gpu) - float(ref)) <= REL * scale + ABS
+
+    def summary(self) -> dict:
+        return {"state_components": self.n_state, "state_widened": self.w_state,
+                "state_widened_frac": self.w_state / max(self.n_state, 1), "rewards": self.n_rew,
+                "rewards_widened": self.w_rew, "rewards_widened_frac": self.w_rew / max(self.n_rew, 1),
+                "examples": self.examples}
+
+    def report(self, name: str):
+        import json
+        import os
+        d = os.environ.get("L2F_TOLSTATS_DIR")
+        if d:
+            os.makedirs(d, exist_ok=True)
+            with open(os.path.join(d, name + ".json"), "w") as f:
+                json.dump(self.summary(), f, indent=1)
+        print(name, self.summary())
+
+
+def reward_scale(cfg, t, s1, a) -> float:
+    """Q36 scale S = 2 sum |term| of the reward at stage t, state s1, action a:
+    a tolerance scale only (the parity value itself is the oracle's reward)."""
+    w, _ = oracle.stage(cfg, t)
+    s1 = np.asarray(s1, dtype=np.float64)
+    a = np.asarray(a, dtype=np.float64)
+    rab = np.array(list(w.C_rab))
+    terms = [w.C_rs, w.C_rp * np.sum(s1[0:3] ** 2), w.C_rq * abs(1 - s1[3] ** 2), w.C_rv * np.sum(s1[7:10] ** 2),
+             w.C_rw * np.sum(s1[10:13] ** 2), w.C_ra * np.sum((a - rab) ** 2)]
+    return 2.0 * float(np.sum(np.abs(terms)))

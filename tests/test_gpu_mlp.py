@@ -2,7 +2,8 @@
 
 Closed-loop rollouts are checked teacher-forced:
 for every traced env-step the oracle re-evaluates the policy on the GPU's own pre-step state
-and history (action agreement |da| <= 2e-3; <= 1e-4 away from fp16 rounding midpoints) and
+and history (action agreement |da| <= 2e-3 always, <= TIGHT = 2e-5 for evaluations whose quantisation
+points are more than MIDPOINT_MARGIN = 1e-6 (relative) from an fp16 rounding midpoint) and
 re-steps the env with the GPU's action (single-step state tolerance).  Free-running
 trajectories are compared only in distribution (episode length / return)."""
 import numpy as np
@@ -11,9 +12,16 @@ import torch
 
 import inputs
 import oracle
-from gpu_helpers import close, close_step, logical_hist, snapshot
+from gpu_helpers import TolStats, close, close_step, logical_hist, reward_scale, snapshot
 
 pytestmark = pytest.mark.gpu
+
+# SURVEY 8(c) parity test 5: an MLP evaluation is held to the tight action bound unless one of
+# its quantisation points (observation, layer-1/2 pre-activations) lies within this relative
+# distance of an fp16 rounding midpoint (where FP32 tensor-core accumulation may round the
+# other way); at least half of the evaluations must be held to it.
+MIDPOINT_MARGIN = 1e-6
+TIGHT = 2e-5  # measured worst 7.1e-6 over the teacher-forced and forward tests (round 2)
 
 
 @pytest.fixture(scope="module")
@@ -44,13 +52,17 @@ def test_policy_forward_matches_oracle(pkg, nh):
     ph = oracle.PolicyHandle(W)
     o32 = obs.astype(np.float32).astype(np.float64)
     worst_ok = 0.0
+    kept = 0
     for i in range(n):
         ref = oracle.mlp(ph, o32[i])
         d = np.max(np.abs(a[i] - ref))
         assert d <= 2e-3, (i, a[i], ref)
-        if oracle.mlp_midpoint_margin(ph, o32[i]) > 1e-5:
+        if oracle.mlp_midpoint_margin(ph, o32[i]) > MIDPOINT_MARGIN:
             worst_ok = max(worst_ok, d)
-    assert worst_ok <= 1e-4, worst_ok
+            kept += 1
+    print("policy_forward nh", nh, "kept", kept / n, "worst", worst_ok)
+    assert kept >= 0.5 * n, kept
+    assert worst_ok <= TIGHT, worst_ok
 
 
 def test_policy_forward_ragged_and_large(pkg):
@@ -80,6 +92,7 @@ def _teacher_forced(pkg, cfg, n, T, K, t0=0, seed=7, check_every=1):
     after = snapshot(env) if full else snapshot(env, ids)
     n_checked = n_excl = 0
     worst = 0.0
+    ts = TolStats()
     for j, i in enumerate(ids):
         c = i if full else j  # column of env i in the snapshots
         e = oracle.new_envs(1)
@@ -103,27 +116,34 @@ def _teacher_forced(pkg, cfg, n, T, K, t0=0, seed=7, check_every=1):
                 a_ref = oracle.mlp(ph, ob)
                 d = np.max(np.abs(a_gpu - a_ref))
                 assert d <= 2e-3, (j, k, a_gpu, a_ref)
-                if oracle.mlp_midpoint_margin(ph, ob) > 1e-5:
+                if oracle.mlp_midpoint_margin(ph, ob) > MIDPOINT_MARGIN:
                     worst = max(worst, d)
                 else:
                     n_excl += 1
                 n_checked += 1
             so = oracle.env_step(cfg, e, int(i), t, a_gpu)
             assert np.all(close(rec[21:25], so.a_applied, abs_=2e-6)), (j, k)
-            assert close(rec[25], so.reward, abs_=1e-5), (j, k, rec[25], so.reward)
+            if not so.flags & oracle.FLAG_DIVERGED:
+                assert ts.reward(rec[25], so.reward, reward_scale(cfg, t, so.final_s, so.a_applied)), \
+                    (j, k, rec[25], so.reward)
             assert int(rec[26]) == so.flags or abs(min(so.margin, key=abs)) < 1e-4, (j, k, rec[26], so.flags)
             if int(rec[26]) != so.flags:
                 break  # near-threshold flip (Q22): stop following this env
             nxt = tr[k + 1, j, :17] if k + 1 < T else after["state"][:, c]
             ref_next = e[0]["s"]
             prev = rec[:17] if not (so.flags & oracle.FLAG_RESET) else ref_next
-            assert np.all(close_step(nxt, ref_next, prev)), (j, k, nxt - ref_next)
+            assert ts.state(nxt, ref_next, prev, tag=(j, k)), (j, k, nxt - ref_next)
             ep, ret = int(e[0]["ep_step"]), float(e[0]["ep_return"])
             if so.flags & oracle.FLAG_RESET:
                 H = [e[0]["hist"][kk].copy() for kk in range(nh)]  # fill of the new episode
             elif nh:
                 H = [np.array(rec[21:25], dtype=np.float64)] + H[:-1]
             # the new episode's dist / dr come from the oracle's own reset (same Philox counter)
+    ts.report(f"teacher_forced_n{n}_T{T}")
+    sm = ts.summary()
+    assert sm["state_widened_frac"] <= 2e-4 and sm["rewards_widened"] == 0, sm
+    print("teacher_forced kept", 1 - n_excl / max(n_checked, 1), "worst", worst)
+    assert n_excl <= 0.5 * n_checked, (n_excl, n_checked)
     return n_checked, n_excl, worst, after, tr, ids
 
 
@@ -131,7 +151,7 @@ def test_mlp_rollout_teacher_forced_c4(pkg):
     cfg = inputs.config_c4()
     n_checked, n_excl, worst, _, _, _ = _teacher_forced(pkg, cfg, n=2000, T=60, K=48)
     assert n_checked > 1000
-    assert worst <= 1e-4, worst
+    assert worst <= TIGHT, worst
 
 
 def test_mlp_rollout_full_size_c5_shard_sampled(pkg):
@@ -142,7 +162,7 @@ def test_mlp_rollout_full_size_c5_shard_sampled(pkg):
     cfg["curriculum"]["interval"] = 12
     n_checked, _, worst, _, _, _ = _teacher_forced(pkg, cfg, n=1 << 21, T=25, K=40, t0=5)
     assert n_checked > 800
-    assert worst <= 1e-4, worst
+    assert worst <= TIGHT, worst
 
 
 def test_mlp_rollout_teacher_forced_c5_curriculum_dr(pkg):
@@ -150,14 +170,14 @@ def test_mlp_rollout_teacher_forced_c5_curriculum_dr(pkg):
     cfg = inputs.config_c5(flags=inputs.ALL_NO_DR | inputs.DOMAIN_RAND)
     cfg["curriculum"]["interval"] = 20
     _, _, worst, _, _, _ = _teacher_forced(pkg, cfg, n=700, T=45, K=32, t0=7)
-    assert worst <= 1e-4
+    assert worst <= TIGHT
 
 
 @pytest.mark.parametrize("nh", [4, 8, 0])
 def test_mlp_rollout_history_lengths(pkg, nh):
     cfg = inputs.config_c4(n_hist=nh)
     _, _, worst, _, _, _ = _teacher_forced(pkg, cfg, n=300, T=40, K=16)
-    assert worst <= 1e-4
+    assert worst <= TIGHT
 
 
 def test_mlp_rollout_history_writeback_and_continuation(pkg):
