@@ -2,7 +2,9 @@
 """Benchmark of the batched quadrotor env hot path (arXiv 2311.13081) on B200.
 
   python bench.py --gpus N --steps K --warmup W [--impl reference]
-  (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...)
+  (N > 1 without a torchrun environment: bench.py re-launches itself as
+   python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 ...
+   one rank per GPU; launched under torchrun it runs as the given rank)
 
 One bench "step" = one pass of the whole hot path over the
 per-GPU batch: l2f_rollout of T = 1000 env-steps with the actor MLP on tensor cores, noise,
@@ -144,9 +146,29 @@ def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N > 1 must be launched with torch.distributed.run (one rank per GPU)")
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: one rank per GPU")
     return world, rank, local
+
+
+def self_launch(args):
+    """--gpus N > 1 outside torchrun: re-run this command as N ranks of one node under
+    torch.distributed.run (rendezvous on 127.0.0.1, a free port) and return its exit code.
+    NCCL's init log (NCCL_DEBUG=INFO, INIT subsystem) goes to stderr so the rank count is
+    visible without touching the one JSON line on stdout."""
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def cpu_baseline(cfg, policy_w, target_s=15.0, nthreads=None):
@@ -235,6 +257,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="mlp", choices=["mlp", "open"])  # open: Philox random actions, no MLP
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(self_launch(args))
     if args.impl == "reference":
         return reference_arm(args)
 

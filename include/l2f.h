@@ -20,7 +20,10 @@
  *  - All functions are extern "C", never throw, and return an l2f_status.  On a non-OK
  *    status l2f_last_error() returns a thread-local message.
  *  - Device pointers ("d_") are caller-owned CUDA device memory on the env's device; host
- *    pointers ("h_") are caller-owned host memory.  The library never allocates device
+ *    pointers ("h_") are caller-owned host memory.  An env's device is the device of its
+ *    workspace; every call on an env launches there whatever device is current in the
+ *    calling thread (the current device is restored on return), so `stream` must be a
+ *    stream of that device (or NULL, its legacy default stream).  The library never allocates device
  *    memory: the caller provides a workspace of l2f_workspace_size() bytes at create time.
  *  - Every call is asynchronous on the caller's stream (a cudaStream_t passed as void*;
  *    NULL = the legacy default stream) unless its comment says it synchronises.  The
@@ -197,8 +200,9 @@ typedef struct {
  * infeasible at the worst DR corner (4 f(rpm_max) <= m g). */
 L2F_API l2f_status l2f_workspace_size(const l2f_config* cfg, size_t* bytes);
 
-/* Creates an env over a caller-owned, 256-byte-aligned device workspace on the current
- * CUDA device.  Copies cfg.  Does not touch the workspace: call l2f_reset before stepping. */
+/* Creates an env over a caller-owned, 256-byte-aligned device workspace; the env's device is
+ * the workspace's (cudaPointerGetAttributes), so no device argument is taken (Q38).
+ * Copies cfg.  Does not touch the workspace: call l2f_reset before stepping. */
 L2F_API l2f_status l2f_create(const l2f_config* cfg, void* d_workspace, size_t bytes, l2f_env** out);
 
 /* Frees host-side resources (never the caller's workspace). */

@@ -32,6 +32,22 @@ l2f_status cuda_fail(cudaError_t e, const char* where)
     return L2F_ERR_CUDA;
 }
 
+// Every env entry point launches on the env's own device (the device of its workspace,
+// recorded at l2f_create), whatever device is current in the calling thread; the caller's
+// current device is restored on return (include/l2f.h conventions).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 int32_t n_slots_for(int64_t n)
@@ -367,6 +383,7 @@ l2f_status l2f_destroy(l2f_env* env)
 l2f_status l2f_reset(l2f_env* env, const uint8_t* d_mask, const l2f_step_out* out, void* stream)
 {
     if (!env) return fail(L2F_ERR_INVALID_ARGUMENT, "env is NULL");
+    const DeviceGuard guard(env->device);
     cudaStream_t s = (cudaStream_t)stream;
     DevParams P;
     params_for(env, env->t, 1, P);
@@ -385,6 +402,7 @@ l2f_status l2f_reset(l2f_env* env, const uint8_t* d_mask, const l2f_step_out* ou
 l2f_status l2f_step(l2f_env* env, const float* d_actions, const l2f_step_out* out, void* stream)
 {
     if (!env || !d_actions) return fail(L2F_ERR_INVALID_ARGUMENT, "env/actions is NULL");
+    const DeviceGuard guard(env->device);
     DevParams P;
     params_for(env, env->t, 1, P);
     l2f_status st = launched(launch_step(P, env->B, d_actions, to_dev(out), (cudaStream_t)stream), "l2f_step");
@@ -399,6 +417,7 @@ l2f_status l2f_rollout(l2f_env* env, const l2f_policy* policy, const float* d_ac
                        const int64_t* d_trace_ids, int32_t K, void* stream)
 {
     if (!env) return fail(L2F_ERR_INVALID_ARGUMENT, "env is NULL");
+    const DeviceGuard guard(env->device);
     if (T < 1) return fail(L2F_ERR_INVALID_ARGUMENT, "T must be >= 1");
     if (d_trace && (!d_trace_ids || K < 1 || K > 4096))
         return fail(L2F_ERR_INVALID_ARGUMENT, "trace needs trace ids and 1 <= K <= 4096");
@@ -441,6 +460,7 @@ l2f_status l2f_rollout(l2f_env* env, const l2f_policy* policy, const float* d_ac
 l2f_status l2f_track(l2f_env* env, const l2f_policy* policy, const l2f_tracking* spec, void* stream)
 {
     if (!env || !policy || !spec) return fail(L2F_ERR_INVALID_ARGUMENT, "env/policy/spec is NULL");
+    const DeviceGuard guard(env->device);
     if (!spec->cycle_time || !spec->rmse || !spec->rmse_xy || !spec->steps_ok)
         return fail(L2F_ERR_INVALID_ARGUMENT, "tracking buffers must not be NULL");
     if (spec->n_steps < 1 || !(spec->clip_pos > 0) || !(spec->clip_vel > 0))
@@ -566,6 +586,7 @@ l2f_status l2f_td3_export_actor(const float* d_params, int32_t agent, int32_t in
 l2f_status l2f_episode_stats(l2f_env* env, double* d_out, int32_t reset_accumulators, void* stream)
 {
     if (!env || !d_out) return fail(L2F_ERR_INVALID_ARGUMENT, "env/out is NULL");
+    const DeviceGuard guard(env->device);
     l2f_status st = launched(launch_stats_finalize(env->B.slots, env->L.n_slots, d_out, reset_accumulators,
                                                    env->steps, (cudaStream_t)stream),
                              "l2f_episode_stats");
@@ -577,6 +598,7 @@ l2f_status l2f_step_host(l2f_env* env, const float* h_actions, float* h_obs_core
                          void* stream)
 {
     if (!env || !h_actions) return fail(L2F_ERR_INVALID_ARGUMENT, "env/actions is NULL");
+    const DeviceGuard guard(env->device);
     cudaStream_t s = (cudaStream_t)stream;
     const size_t N = (size_t)env->cfg.num_envs;
     float* d_act = (float*)(env->ws + env->L.st_act);
@@ -603,6 +625,7 @@ l2f_status l2f_rollout_host(l2f_env* env, const l2f_policy* h_policy, int32_t T,
                             int32_t reset_accumulators, void* stream)
 {
     if (!env || !h_policy) return fail(L2F_ERR_INVALID_ARGUMENT, "env/policy is NULL");
+    const DeviceGuard guard(env->device);
     const int32_t I = h_policy->in_dim, H = h_policy->hidden;
     if (I != 18 + 4 * env->cfg.action_history || H != 64)
         return fail(L2F_ERR_INVALID_ARGUMENT, "policy must be (18 + 4 N_H) -> 64 -> 64 -> 4");
@@ -668,6 +691,7 @@ l2f_status l2f_set_t(l2f_env* env, uint64_t t)
 l2f_status l2f_set_state(l2f_env* env, const l2f_state_view* in, void* stream)
 {
     if (!env || !in) return fail(L2F_ERR_INVALID_ARGUMENT, "env/in is NULL");
+    const DeviceGuard guard(env->device);
     const int64_t N = env->cfg.num_envs;
     const int32_t NH = env->cfg.action_history;
     if (in->num_envs != N || in->action_history != NH)
@@ -716,6 +740,7 @@ l2f_status l2f_recompute_rewards(const l2f_env* env, uint64_t t, const float* d_
 {
     if (!env || !d_next_state || !d_actions || !d_rewards || m <= 0)
         return fail(L2F_ERR_INVALID_ARGUMENT, "bad recompute_rewards arguments");
+    const DeviceGuard guard(env->device);
     const int64_t I = env->cfg.curriculum.interval;
     const int64_t k = I > 0 ? (int64_t)(t / (uint64_t)I) : 0;
     const StageW W = stage_weights(env->cfg, k);

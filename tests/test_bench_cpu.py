@@ -33,3 +33,17 @@ def test_reference_arm_nonzero_rank_is_silent():
     r = run(["--gpus", "2", "--steps", "1", "--warmup", "0"], {"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"})
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip() == ""
+
+
+def test_reference_arm_self_launches_n_ranks():
+    """--gpus 2 outside torchrun: bench.py re-launches itself under torch.distributed.run
+    (2 ranks, 127.0.0.1 rendezvous); rank 0 prints exactly one JSON line with n_gpus 2."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["L2F_REF_TARGET_S"] = "0.3"
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--steps", "1",
+                        "--warmup", "0"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
