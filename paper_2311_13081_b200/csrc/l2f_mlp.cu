@@ -196,7 +196,7 @@ struct NoHook {
 // three warps.  Precondition: A1 rows written by all 128 threads.  `rot` = rotation of the
 // history ring (W1 history row offset in slots).  hook(l) runs on every thread right after
 // layer l's MMAs were issued, i.e. inside the MMA latency (used to draw the next step's noise).
-template <class Hook>
+template <int kNH, class Hook>
 __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_hist, uint32_t rot, float (&a)[kE][4],
                                           const Hook& hook)
 {
@@ -215,12 +215,17 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
             // L1: obs part (K = 32) then history (K = 4 N_H) with the rotated W1 history block
             const uint64_t dA1 = tc::make_desc(c.a1 + k * kA1Bytes, kChunkA, 128);
             const uint32_t d = c.tmem_tile + 64 * k;
-            tc::mma_f16_elect(d, dA1, dW1o, kIdescN64, 0);
-            tc::mma_f16_elect(d, dA1 + 2 * kChunkA / 16, dW1o + 2 * (kHid * 16) / 16, kIdescN64, 1);
+            if constexpr (kNH == 32) {
+                static_assert(2 * kChunkA / 16 == 256 && 2 * (kHid * 16) / 16 == 128, "issue_l1_elect offsets");
+                tc::issue_l1_elect<8>(d, dA1, dW1o, dW1h, kIdescN64, kIdescN64BMN);
+            } else {
+                tc::mma_f16_elect(d, dA1, dW1o, kIdescN64, 0);
+                tc::mma_f16_elect(d, dA1 + 2 * kChunkA / 16, dW1o + 2 * (kHid * 16) / 16, kIdescN64, 1);
 #pragma unroll
-            for (int j = 0; j < kMaxHist / 4; ++j)
-                if (j < n_hist / 4)
-                    tc::mma_f16_elect(d, dA1 + (4 + 2 * j) * (kChunkA / 16), dW1h + 16u * j, kIdescN64BMN, 1);
+                for (int j = 0; j < kMaxHist / 4; ++j)
+                    if (j < n_hist / 4)
+                        tc::mma_f16_elect(d, dA1 + (4 + 2 * j) * (kChunkA / 16), dW1h + 16u * j, kIdescN64BMN, 1);
+            }
         }
         tc::commit_elect(c.mbar);
     }
@@ -238,11 +243,8 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
         tc::fence_after();
         const uint64_t dW2 = tc::make_desc(sbase + OFF_W2, kHid * 16, 128);
 #pragma unroll
-        for (int k = 0; k < kE; ++k)
-#pragma unroll
-            for (int j = 0; j < 5; ++j)  // A from TMEM; j = 4: the ones column (bias row of W2)
-                tc::mma_f16_ts_elect(c.tmem_tile + 64 * k, c.a2_tmem + 40 * k + 8 * j, dW2 + j * (2 * kHid * 16 / 16),
-                               kIdescN64, j);
+        for (int k = 0; k < kE; ++k)  // A from TMEM; K step 4: the ones column (bias row of W2)
+            tc::issue_ts5_elect<2 * kHid * 16 / 16>(c.tmem_tile + 64 * k, c.a2_tmem + 40 * k, dW2, kIdescN64);
         tc::commit_elect(c.mbar);
     }
     hook(2);
@@ -260,10 +262,7 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
         const uint64_t dW3 = tc::make_desc(sbase + OFF_W3, 256, 128);
 #pragma unroll
         for (int k = 0; k < kE; ++k)
-#pragma unroll
-            for (int j = 0; j < 5; ++j)
-                tc::mma_f16_ts_elect(c.tmem_tile + 64 * k, c.a2_tmem + 40 * k + 8 * j, dW3 + j * (2 * 256 / 16),
-                               kIdescN16, j);
+            tc::issue_ts5_elect<2 * 256 / 16>(c.tmem_tile + 64 * k, c.a2_tmem + 40 * k, dW3, kIdescN16);
         tc::commit_elect(c.mbar);
     }
     hook(3);
@@ -400,14 +399,16 @@ __device__ void teardown_cta()
 // thread carries kE envs (one per tile slot) through every phase together, so the two envs'
 // independent dependency chains (Philox, Box-Muller, RK4) interleave in the same basic blocks.
 // -------------------------------------------------------------------------------------------
-template <bool kDR>
+// kNH: N_H as a compile-time constant (32, the benchmark's history) or -1 (any N_H % 4 == 0,
+// read from P at run time).
+template <bool kDR, int kNH>
 __global__ void __launch_bounds__(kThreads, 1)
     rollout_mlp_kernel(const DevParams P, const DevBufs B, const PolicyDev W, int32_t T, float* __restrict__ trace,
                        const int64_t* __restrict__ trace_ids, int32_t K, int32_t n_units)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sbase = tc::smem_u32(smem);
-    const int NH = P.n_hist;
+    const int NH = kNH >= 0 ? kNH : P.n_hist;
     setup_cta(W, sbase, NH, &P);
     GroupCtx c = make_ctx(sbase);
     const int64_t N = P.n;
@@ -488,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             float a[kE][4], za[kE][4];
             // noise draws inside the MMA latency, unconditionally (no flag branch splits the
             // independent Philox chains into separate basic blocks; unused draws are discarded)
-            mlp_group(c, sbase, NH, rot, a, [&](int l) {
+            mlp_group<kNH>(c, sbase, NH, rot, a, [&](int l) {
 #pragma unroll
                 for (int k = 0; k < kE; ++k) {
                     if (l == 1) {
@@ -644,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         float a[kE][4];
-        mlp_group(c, sbase, NH, 0u, a, NoHook{});
+        mlp_group<-1>(c, sbase, NH, 0u, a, NoHook{});
 #pragma unroll
         for (int k = 0; k < kE; ++k)
             if (i[k] < n)
@@ -745,7 +746,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 write_obs_row(c, k, ob);
             }
             float a[kE][4];
-            mlp_group(c, sbase, NH, rot, a, [&](int l) {
+            mlp_group<-1>(c, sbase, NH, rot, a, [&](int l) {
 #pragma unroll
                 for (int k = 0; k < kE; ++k) stash_obs_noise(P, c, k, gid[k], t + 1, l - 1);
             });
@@ -840,15 +841,13 @@ cudaError_t launch_rollout_mlp(const DevParams& P, const DevBufs& B, const Polic
                                const int64_t* trace_ids, int32_t K, cudaStream_t s)
 {
     if (P.n_hist % 4 != 0 || W.hidden != kHid || W.in_dim != 18 + 4 * P.n_hist) return cudaErrorNotSupported;
-    static std::atomic<size_t> attr_t[64] = {}, attr_f[64] = {};
-    cudaError_t e = ensure_smem_attr(rollout_mlp_kernel<true>, kSmemBytes, attr_t);
-    if (e == cudaSuccess) e = ensure_smem_attr(rollout_mlp_kernel<false>, kSmemBytes, attr_f);
+    static std::atomic<size_t> attr[4][64] = {};
+    const bool dr = (P.flags & F_DOMAIN_RAND) != 0, h32 = P.n_hist == 32;
+    auto kern = dr ? (h32 ? rollout_mlp_kernel<true, 32> : rollout_mlp_kernel<true, -1>)
+                   : (h32 ? rollout_mlp_kernel<false, 32> : rollout_mlp_kernel<false, -1>);
+    const cudaError_t e = ensure_smem_attr(kern, kSmemBytes, attr[2 * dr + h32]);
     if (e != cudaSuccess) return e;
-    const int n_units = (int)units_for(P.n);
-    if (P.flags & F_DOMAIN_RAND)
-        rollout_mlp_kernel<true><<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, n_units);
-    else
-        rollout_mlp_kernel<false><<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, n_units);
+    kern<<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, (int32_t)units_for(P.n));
     return cudaGetLastError();
 }
 

@@ -80,6 +80,64 @@ __device__ __forceinline__ void mma_f16_ts_elect(uint32_t d_tmem, uint32_t a_tme
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// Layer-1 MMAs of one 128-row tile in one elected issue: the observation part (K = 32: two
+// K16 steps, A at +0 / +256 descriptor units, B at +0 / +128) then kHist history K16 steps
+// (A at +512 + 256 j, B at + 16 j, MN-major B), accumulating into d.  One elect.sync for the
+// whole sequence; every descriptor is its base plus an immediate.
+template <int kHist>
+__device__ __forceinline__ void issue_l1_elect(uint32_t d, uint64_t a, uint64_t bo, uint64_t bh, uint32_t idesc,
+                                               uint32_t idesc_bmn)
+{
+    static_assert(kHist == 8, "specialised for N_H = 32");
+    asm volatile(
+        "{\n\t.reg .pred e, p0, p1;\n\t.reg .b64 ra, rb;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p0, %5, %5;\n\t"
+        "setp.eq.b32 p1, %5, %5;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p0;\n\t"
+        "add.s64 ra, %1, 256;\n\tadd.s64 rb, %2, 128;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %4, p1;\n\t"
+        "add.s64 ra, %1, 512;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, %3, %5, p1;\n\t"
+        "add.s64 ra, %1, 768;\n\tadd.s64 rb, %3, 16;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %5, p1;\n\t"
+        "add.s64 ra, %1, 1024;\n\tadd.s64 rb, %3, 32;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %5, p1;\n\t"
+        "add.s64 ra, %1, 1280;\n\tadd.s64 rb, %3, 48;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %5, p1;\n\t"
+        "add.s64 ra, %1, 1536;\n\tadd.s64 rb, %3, 64;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %5, p1;\n\t"
+        "add.s64 ra, %1, 1792;\n\tadd.s64 rb, %3, 80;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %5, p1;\n\t"
+        "add.s64 ra, %1, 2048;\n\tadd.s64 rb, %3, 96;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %5, p1;\n\t"
+        "add.s64 ra, %1, 2304;\n\tadd.s64 rb, %3, 112;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %5, p1;\n\t}\n" ::"r"(d),
+        "l"(a), "l"(bo), "l"(bh), "r"(idesc), "r"(idesc_bmn));
+}
+
+// Layers 2 / 3 of one tile in one elected issue: 5 K16 steps with A from TMEM columns
+// a_tmem + 8 j and B at + b_step j descriptor units (K = 80: 64 hidden + the ones column).
+template <int kBStep>
+__device__ __forceinline__ void issue_ts5_elect(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc)
+{
+    asm volatile(
+        "{\n\t.reg .pred e, p0, p1;\n\t.reg .b64 rb;\n\t.reg .b32 ra;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p0, %3, %3;\n\t"
+        "setp.eq.b32 p1, %3, %3;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p0;\n\t"
+        "add.s32 ra, %1, 8;\n\tadd.s64 rb, %2, %4;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ra], rb, %3, p1;\n\t"
+        "add.s32 ra, %1, 16;\n\tadd.s64 rb, %2, %5;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ra], rb, %3, p1;\n\t"
+        "add.s32 ra, %1, 24;\n\tadd.s64 rb, %2, %6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ra], rb, %3, p1;\n\t"
+        "add.s32 ra, %1, 32;\n\tadd.s64 rb, %2, %7;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ra], rb, %3, p1;\n\t}\n" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "n"(kBStep), "n"(2 * kBStep), "n"(3 * kBStep), "n"(4 * kBStep));
+}
+
 __device__ __forceinline__ void commit_elect(uint32_t mbar_saddr)
 {
     asm volatile(
