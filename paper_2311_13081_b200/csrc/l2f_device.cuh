@@ -874,6 +874,56 @@ __device__ __forceinline__ void stat_episode(StatAcc& a, const Trans& o)
     a.ret2 += r * r;
 }
 
+// Compact per-thread accumulator of one rollout unit (at most 65535 steps per thread between
+// flushes): (episodes | terminated << 16), (truncated | diverged << 16), summed lengths, FP64
+// return sums -- 7 registers instead of StatAcc's 9 in the register-bound fused rollout.
+struct StatPk {
+    uint32_t ep_term, trunc_div, len;
+    double ret, ret2;
+};
+
+__device__ __forceinline__ void statpk_zero(StatPk& a)
+{
+    a.ep_term = a.trunc_div = a.len = 0u;
+    a.ret = a.ret2 = 0.0;
+}
+
+__device__ __forceinline__ void statpk_episode(StatPk& a, const Trans& o)
+{
+    a.ep_term += 1u + ((o.flags & D_TERM) ? 0x10000u : 0u);
+    a.trunc_div += ((o.flags & D_TRUNC) ? 1u : 0u) + ((o.flags & D_DIV) ? 0x10000u : 0u);
+    a.len += (uint32_t)o.len;
+    const double r = (double)o.ret;
+    a.ret += r;
+    a.ret2 += r * r;
+}
+
+// Warp-reduce a unit's accumulator (fixed shuffle order) and add it, with `steps` env-steps, to
+// the warp's FP64 row (lane 0 writes).  All 32 lanes must call it.
+__device__ __forceinline__ void statpk_flush(const StatPk& a, double steps, double* row)
+{
+    const unsigned m = 0xffffffffu;
+    const uint32_t ep = __reduce_add_sync(m, a.ep_term & 0xFFFFu), term = __reduce_add_sync(m, a.ep_term >> 16);
+    const uint32_t tr = __reduce_add_sync(m, a.trunc_div & 0xFFFFu), dv = __reduce_add_sync(m, a.trunc_div >> 16);
+    const uint32_t len = __reduce_add_sync(m, a.len);
+    double r = a.ret, r2 = a.ret2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        r += __shfl_xor_sync(m, r, o);
+        r2 += __shfl_xor_sync(m, r2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        row[0] += ep;
+        row[1] += term;
+        row[2] += tr;
+        row[3] += dv;
+        row[4] += len;
+        row[5] += r;
+        row[6] += r2;
+        row[7] += steps;
+    }
+}
+
 // Warp-reduce `a` and write lane 0's result into smem[warp][8] (doubles); returns nothing.
 // All 32 lanes must call it.
 __device__ __forceinline__ void stat_warp_to_smem(const StatAcc& a, double* smem_warp_row)

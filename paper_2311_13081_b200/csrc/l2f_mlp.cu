@@ -62,11 +62,13 @@ constexpr uint32_t OFF_RTAB = (OFF_TMEM + 8 + 15) & ~15u;     // reset sampling 
 constexpr uint32_t OFF_STAT = (OFF_RTAB + 256 + 127) & ~127u;  // reset scratch (40 uint4 per warp); reused by stats
 constexpr uint32_t kScratchBytes = (kThreads / 32) * kResetScratch * 16;
 static_assert(kScratchBytes >= (kThreads / 32) * kStatsLen * 8, "stats rows fit in the scratch");
-constexpr uint32_t kSmemBytes = OFF_STAT + kScratchBytes;
+constexpr uint32_t OFF_WSTAT = OFF_STAT + kScratchBytes;  // per-warp FP64 statistics rows (flushed per unit)
+constexpr uint32_t kSmemBytes = OFF_WSTAT + (kThreads / 32) * kStatsLen * 8;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 constexpr uint32_t kTmemCols = 512;
 // TMEM map: accumulators 64 columns per tile from 0; A2 (h1/h2 as fp16: 32 columns + 8 with the
-// ones column) 40 per tile from 64 kTiles; the per-env noise stash (18 used) 24 per tile after.
+// ones column) 40 per tile from 64 kTiles; the per-env noise stash 24 per tile after (columns
+// 0-17 the next step's observation noise, 20-23 this step's action noise).
 constexpr uint32_t kA2Col = 64 * kTiles;
 constexpr uint32_t kStashCol = kA2Col + 40 * kTiles;
 static_assert(kStashCol + 24 * kTiles <= kTmemCols, "TMEM budget");
@@ -415,13 +417,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = threadIdx.x % kM;
     uint4* const rscratch = reinterpret_cast<uint4*>(smem + OFF_STAT) + (threadIdx.x >> 5) * kResetScratch;
     const float4* const rtab = reinterpret_cast<const float4*>(smem + OFF_RTAB);
-    StatAcc st;
-    stat_zero(st);
-    double steps_done = 0.0;
+    double* const wrow = reinterpret_cast<double*>(smem + OFF_WSTAT) + (threadIdx.x >> 5) * kStatsLen;
+    if ((threadIdx.x & 31) < kStatsLen) wrow[threadIdx.x & 31] = 0.0;
+    __syncwarp();
     const bool obs_noise = (P.flags & F_OBS_NOISE) != 0;
 
     // unit u = tiles u kE .. u kE + kE - 1 (one per tile slot)
     for (int u = blockIdx.x * kG + (int)(threadIdx.x / kM); u < n_units; u += gridDim.x * kG) {
+        StatPk st;
+        statpk_zero(st);
         int64_t i[kE];
         bool active[kE];
         uint32_t gid[kE];
@@ -486,17 +490,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 observe_core_z(P, e[k].s, z, ob);
                 write_obs_row(c, k, ob);
             }
-            float a[kE][4], za[kE][4];
+            float a[kE][4];
             // noise draws inside the MMA latency, unconditionally (no flag branch splits the
             // independent Philox chains into separate basic blocks; unused draws are discarded)
             mlp_group<kNH>(c, sbase, NH, rot, a, [&](int l) {
 #pragma unroll
                 for (int k = 0; k < kE; ++k) {
-                    if (l == 1) {
-                        box_muller2(draw(P, gid[k], t, S_ACT, 0), za[k]);
+                    if (l == 1) {  // this step's action noise, parked in TMEM until the transition
+                        float z[4];
+                        box_muller2(draw(P, gid[k], t, S_ACT, 0), z);
                         const bool an = (P.flags & F_ACTION_NOISE) != 0;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) za[k][q] = an ? za[k][q] : 0.0f;
+                        for (int q = 0; q < 4; ++q) z[q] = an ? z[q] : 0.0f;
+                        tc::tmem_st4(c.stash_row + 24 * k + 20, z);
                     }
                     stash_obs_noise(P, c, k, gid[k], t + 1, l - 1);
                 }
@@ -513,6 +519,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int q = 0; q < 4; ++q) tr[17 + q] = a[k][q];
                 }
             }
+            float za[kE][4];
+#pragma unroll
+            for (int k = 0; k < kE; ++k) {
+                uint32_t v[4];
+                tc::tmem_ld4(c.stash_row + 24 * k + 20, v);
+                tc::tmem_wait_ld();
+#pragma unroll
+                for (int q = 0; q < 4; ++q) za[k][q] = __uint_as_float(v[q]);
+            }
 #pragma unroll
             for (int k = 0; k < kE; ++k) transition<kDR>(P, W, e[k], gid[k], t, a[k], za[k], o[k]);
 #ifdef L2F_PHASE_TIMING
@@ -526,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < kE; ++k) {
                 uint32_t fl = o[k].flags;
                 const bool ended = (fl & (D_TERM | D_TRUNC)) != 0;
-                if (ended && active[k]) stat_episode(st, o[k]);
+                if (ended && active[k]) statpk_episode(st, o[k]);
                 L2F_PHASE(c, 14);
                 bool did_reset = false;
                 float hf[4];
@@ -566,10 +581,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             L2F_PHASE(c, 13);
         }
         }
+        int n_active = 0;
 #pragma unroll
         for (int k = 0; k < kE; ++k) {
-            if (!active[k]) continue;
-            const int64_t ik = i[k];
+            const int64_t ik = ((int64_t)u * kE + k) * kM + r;
+            if (ik >= N) continue;
+            ++n_active;
             grp_store<kStateDim>(B.state, ik, N, e[k].s);
             grp_store<6>(B.dist, ik, N, e[k].dist);
             if (kDR) grp_store<5>(B.dr, ik, N, e[k].dr);
@@ -583,8 +600,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const __half2 x = *reinterpret_cast<__half2*>(&h01), y = *reinterpret_cast<__half2*>(&h23);
                 B.hist[(int64_t)s * N + ik] = make_float4(__low2float(x), __high2float(x), __low2float(y), __high2float(y));
             }
-            steps_done += (double)T;
         }
+        statpk_flush(st, (double)__reduce_add_sync(0xffffffffu, n_active) * (double)T, wrow);
     }
 #ifdef L2F_PHASE_TIMING
     __syncthreads();
@@ -595,20 +612,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             printf("\n");
         }
 #endif
-    // statistics: warp -> fixed-order block sum -> this CTA's slot
-    double* srow = reinterpret_cast<double*>(smem + OFF_STAT);
-    const int warp = threadIdx.x >> 5;
-    __syncthreads();  // the reset scratch is reused for the statistics rows
-    stat_warp_to_smem(st, srow + warp * kStatsLen);
-    double sd = steps_done;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) srow[warp * kStatsLen + 7] = sd;
+    // statistics: per-warp rows (flushed per unit) -> fixed-order block sum -> this CTA's slot
     __syncthreads();
     if (threadIdx.x < kStatsLen) {
+        const double* rows = reinterpret_cast<const double*>(smem + OFF_WSTAT);
         double x = 0.0;
-        for (int w = 0; w < kThreads / 32; ++w) x += srow[w * kStatsLen + threadIdx.x];
+        for (int w = 0; w < kThreads / 32; ++w) x += rows[w * kStatsLen + threadIdx.x];
         B.slots[(size_t)blockIdx.x * kStatsLen + threadIdx.x] += x;
     }
     teardown_cta();

@@ -252,6 +252,12 @@ __device__ __forceinline__ void tmem_st8u(uint32_t taddr, uint32_t a0, uint32_t 
                  "r"(a1), "r"(a2), "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7)
                  : "memory");
 }
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const float (&v)[4])
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3])
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_st2(uint32_t taddr, float a, float b)
 {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "f"(a), "f"(b) : "memory");
