@@ -717,47 +717,47 @@ __device__ __forceinline__ void reset_env(const DevParams& P, EnvReg& e, uint32_
 }
 
 // Warp-cooperative reset (all 32 lanes must call; gids of a warp are consecutive): lane j of a
-// round draws Philox block (j mod nb) of the (j / nb)-th resetting lane and maps it to that
-// slot's four sampled values; the values reach their owner through the warp's shared-memory
-// scratch (kResetScratch uint4: 32 value slots + a 32-int rank->lane table).  A warp with k
-// ending episodes pays ceil(k nb / 32) Philox + sampling rounds instead of nb serial ones, and
-// the owners only assemble the quaternion.  Bitwise identical to reset_env (same integer
-// Philox, same per-value fma).
+// round draws Philox block (j mod kNB) of reset (j / kNB) of the round and maps it to that slot's
+// four sampled values; the values reach their owner through the warp's shared-memory scratch
+// (kResetScratch uint4: 32 value slots + a 32-int rank->lane table).  A warp with k ending
+// episodes pays ceil(k / (32 / kNB)) Philox + sampling rounds instead of kNB serial ones, and the
+// owners only assemble the quaternion.  kNB = the Philox blocks of one reset that are drawn: 8
+// with domain randomisation (RESET 0-3, DIST 0-1, DR 0-1), 6 without (5 resets per round; the
+// DR slots stay unset and reset_finish ignores them).  Bitwise identical to reset_env (same
+// integer Philox, same per-value fma).
+template <int kNB>
 __device__ __forceinline__ bool reset_env_warp(const DevParams& P, const float4* tab, EnvReg& e, uint32_t gid,
                                                uint32_t ctr, bool need, float hfill[4], uint4* scratch)
 {
+    static_assert(kNB == 6 || kNB == 8, "6 or 8 Philox blocks per reset");
     const unsigned m = __ballot_sync(0xffffffffu, need);
     if (m == 0u) return false;
     const int lane = threadIdx.x & 31;
-    const int lnb = (P.flags & (F_DISTURBANCE | F_DOMAIN_RAND)) ? 3 : 2;  // log2(reset_nblocks)
-    const int nb = 1 << lnb;
+    constexpr int kPer = 32 / kNB;  // resets served per round
     const int nr = __popc(m);
     const int rank = __popc(m & ((1u << lane) - 1u));
     // rank -> lane table in the scratch's tail words (entries 32..39 hold 32 ints)
     int* rl = reinterpret_cast<int*>(scratch + 32);
     if (need) rl[rank] = lane;
     __syncwarp();
+    const int my_q = lane / kNB, b = lane - my_q * kNB;  // reset (within the round) and slot of this lane
+    const bool slot_used = b < 4 || (b < 6 && (P.flags & F_DISTURBANCE)) || (b >= 6 && (P.flags & F_DOMAIN_RAND));
     float4 v[8];
-    const int per_round = 32 >> lnb;  // resets served per round
-    for (int round = 0; round * per_round < nr; ++round) {
-        const int j = round * 32 + lane;
+    if constexpr (kNB == 6) v[6] = v[7] = make_float4(1.f, 1.f, 1.f, 1.f);
+    for (int round = 0; round * kPer < nr; ++round) {
+        const int q = round * kPer + my_q;
         float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (j < nr * nb) {
-            const int b = j & (nb - 1);
-            const bool used = b < 4 || (b < 6 && (P.flags & F_DISTURBANCE)) || (b >= 6 && (P.flags & F_DOMAIN_RAND));
-            if (used) {
-                const uint4 blk = reset_block(P, gid - (uint32_t)lane + (uint32_t)rl[j >> lnb], ctr, b);
-                x = tab ? reset_values_tab(tab, b, blk) : reset_values(P, b, blk);
-            }
+        if (my_q < kPer && q < nr && slot_used) {
+            const uint4 blk = reset_block(P, gid - (uint32_t)lane + (uint32_t)rl[q], ctr, b);
+            x = tab ? reset_values_tab(tab, b, blk) : reset_values(P, b, blk);
         }
         __syncwarp();
         reinterpret_cast<float4*>(scratch)[lane] = x;
         __syncwarp();
-        if (need && rank / per_round == round) {
-            const float4* src = reinterpret_cast<const float4*>(scratch) + ((rank - round * per_round) << lnb);
+        if (need && rank / kPer == round) {
+            const float4* src = reinterpret_cast<const float4*>(scratch) + (rank - round * kPer) * kNB;
 #pragma unroll
-            for (int b = 0; b < 8; ++b)
-                if (b < nb) v[b] = src[b];
+            for (int j = 0; j < kNB; ++j) v[j] = src[j];
         }
     }
     __syncwarp();

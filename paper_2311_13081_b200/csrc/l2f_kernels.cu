@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const D
     bool did_reset = false;
     float hf[4];
     if (P.flags & F_AUTO_RESET) {
-        did_reset = reset_env_warp(P, nullptr, e, gid, t + 1, ended, hf, rscratch + (threadIdx.x >> 5) * kResetScratch);
+        did_reset = reset_env_warp<kDR ? 8 : 6>(P, nullptr, e, gid, t + 1, ended, hf, rscratch + (threadIdx.x >> 5) * kResetScratch);
         if (did_reset) fl |= D_RESET;
     } else if (ended) {
         e.ep_step = 0;
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
         bool did_reset = false;
         float hf[4];
         if (P.flags & F_AUTO_RESET) {
-            did_reset = reset_env_warp(P, nullptr, e, gid, t + 1, ended, hf, rscratch + (threadIdx.x >> 5) * kResetScratch);
+            did_reset = reset_env_warp<kDR ? 8 : 6>(P, nullptr, e, gid, t + 1, ended, hf, rscratch + (threadIdx.x >> 5) * kResetScratch);
             if (did_reset) fl |= D_RESET;
         } else if (ended) {
             e.ep_step = 0;

@@ -67,8 +67,8 @@ constexpr uint32_t kSmemBytes = OFF_WSTAT + (kThreads / 32) * kStatsLen * 8;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 constexpr uint32_t kTmemCols = 512;
 // TMEM map: accumulators 64 columns per tile from 0; A2 (h1/h2 as fp16: 32 columns + 8 with the
-// ones column) 40 per tile from 64 kTiles; the per-env noise stash 24 per tile after (columns
-// 0-17 the next step's observation noise, 20-23 this step's action noise).
+// ones column) 40 per tile from 64 kTiles; the per-env noise stash (18 used: the next step's
+// observation noise) 24 per tile after.
 constexpr uint32_t kA2Col = 64 * kTiles;
 constexpr uint32_t kStashCol = kA2Col + 40 * kTiles;
 static_assert(kStashCol + 24 * kTiles <= kTmemCols, "TMEM budget");
@@ -117,8 +117,11 @@ __device__ void stage_weights(const PolicyDev& W, uint32_t sbase, int n_hist)
 
 __device__ __forceinline__ float tanh_fast(float z)
 {
-    // tanh z = 1 - 2 / (exp(2z) + 1); exact limits at +-inf, absolute error ~1e-7
-    return 1.0f - __fdividef(2.0f, __expf(2.0f * z) + 1.0f);
+    // tanh z = 1 - 2 / (exp(2z) + 1); exact limits at +-inf, absolute error ~1e-7.  exp(2z) =
+    // 2^(z * 2 log2 e): one multiply (scaling by 2 is exact, so the product rounds as 2z log2 e).
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(z * 2.8853900817779268f));
+    return 1.0f - __fdividef(2.0f, e + 1.0f);
 }
 
 // Per-thread context of a 128-thread group.  Thread r of group g owns row r of the group's kE
@@ -490,19 +493,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 observe_core_z(P, e[k].s, z, ob);
                 write_obs_row(c, k, ob);
             }
-            float a[kE][4];
+            float a[kE][4], za[kE][4];
             // noise draws inside the MMA latency, unconditionally (no flag branch splits the
             // independent Philox chains into separate basic blocks; unused draws are discarded)
             mlp_group<kNH>(c, sbase, NH, rot, a, [&](int l) {
 #pragma unroll
                 for (int k = 0; k < kE; ++k) {
-                    if (l == 1) {  // this step's action noise, parked in TMEM until the transition
-                        float z[4];
-                        box_muller2(draw(P, gid[k], t, S_ACT, 0), z);
+                    if (l == 3) {  // this step's action noise (two Philox chains per hook: 2 obs / 2 obs / obs + action)
+                        box_muller2(draw(P, gid[k], t, S_ACT, 0), za[k]);
                         const bool an = (P.flags & F_ACTION_NOISE) != 0;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) z[q] = an ? z[q] : 0.0f;
-                        tc::tmem_st4(c.stash_row + 24 * k + 20, z);
+                        for (int q = 0; q < 4; ++q) za[k][q] = an ? za[k][q] : 0.0f;
                     }
                     stash_obs_noise(P, c, k, gid[k], t + 1, l - 1);
                 }
@@ -518,15 +519,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int q = 0; q < 4; ++q) tr[17 + q] = a[k][q];
                 }
-            }
-            float za[kE][4];
-#pragma unroll
-            for (int k = 0; k < kE; ++k) {
-                uint32_t v[4];
-                tc::tmem_ld4(c.stash_row + 24 * k + 20, v);
-                tc::tmem_wait_ld();
-#pragma unroll
-                for (int q = 0; q < 4; ++q) za[k][q] = __uint_as_float(v[q]);
             }
 #pragma unroll
             for (int k = 0; k < kE; ++k) transition<kDR>(P, W, e[k], gid[k], t, a[k], za[k], o[k]);
@@ -546,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bool did_reset = false;
                 float hf[4];
                 if (P.flags & F_AUTO_RESET) {
-                    did_reset = reset_env_warp(P, rtab, e[k], gid[k], t + 1, ended && active[k], hf, rscratch);
+                    did_reset = reset_env_warp<kDR ? 8 : 6>(P, rtab, e[k], gid[k], t + 1, ended && active[k], hf, rscratch);
                     if (did_reset) fl |= D_RESET;
                 }
                 L2F_PHASE(c, 15);
