@@ -406,9 +406,84 @@ def e2e_rollout(args, pkg, torch, l2fdist, env, W, T, n, world, dev, stream, bar
     return e2e_val, h2d
 
 
-def secondary(pkg, inputs, torch, dev, pk, f_clk):
-    """C3 single-step API (HBM roofline), C4 exactly, and the open-loop dynamics mode."""
+def small_configs(pkg, inputs, torch, dev):
+    """BASELINE configs[0, 1] (C1: 64 x 500, C2: 4096 x 1000): latency-bound sizes, reported as
+    absolute env-steps/s and us per step through (a) the open-loop fused rollout (one launch) and
+    (b) l2f_step captured T times in one CUDA graph (the graph replays the captured counters)."""
     out = {}
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for name, cfg, n, T, acts in (
+            ("C1", inputs.config_c1(), 64, 500, inputs.actions_uniform(500, 64, seed=11)),
+            ("C2", inputs.config_c2(), 4096, 1000, inputs.actions_near_hover(1000, 4096, seed=12))):
+        a = torch.tensor(acts, dtype=torch.float32, device=dev).contiguous()
+        env = pkg.Env(cfg, n, device=dev)
+        env.reset()
+        env.rollout(T, actions=a)
+        torch.cuda.synchronize()
+        reps = 5
+        e0.record(stream)
+        for _ in range(reps):
+            env.rollout(T, actions=a)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        out[f"{name}_open_loop_rollout"] = {"value": n * T / (ms / 1e3), "unit": "env-steps/s", "us_per_step": ms * 1e3 / T,
+                                            "workload": f"{n} envs x {T} steps, one l2f_rollout launch, recorded actions"}
+        o = env.make_out(obs_core=True, reward=True, flags=True)
+        s2 = torch.cuda.Stream(device=dev)
+        s2.wait_stream(stream)
+        with torch.cuda.stream(s2):  # warm-up outside capture
+            for k in range(3):
+                env.step(a[k], o)
+        stream.wait_stream(s2)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for k in range(T):
+                env.step(a[k], o)
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        out[f"{name}_step_graph"] = {"value": n * T / (ms / 1e3), "unit": "env-steps/s", "us_per_step": ms * 1e3 / T,
+                                     "workload": f"{n} envs x {T} l2f_step launches in one CUDA graph"}
+        del env, g
+    return out
+
+
+def c4_exact(pkg, inputs, torch, dev):
+    """BASELINE configs[3] exactly: 2^20 envs x 1000 steps, fused MLP rollout (C4 features)."""
+    stream = torch.cuda.current_stream()
+    n, T = 1 << 20, 1000
+    env = pkg.Env(inputs.config_c4(), n, device=dev)
+    env.reset()
+    pol = pkg.Policy(inputs.policy_weights(146, 64, seed=7, out_bias=inputs.hover_policy_bias()), device=dev)
+    env.rollout(50, policy=pol)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    e0.record(stream)
+    for _ in range(reps):
+        env.rollout(T, policy=pol)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"value": n * T / (ms / 1e3), "unit": "env-steps/s", "ms": ms,
+            "workload": "C4: 2^20 envs x 1000 steps fused actor-MLP rollout (146-64-64-4), noise, reward, termination, "
+                        "auto-reset, disturbance"}
+
+
+def secondary(pkg, inputs, torch, dev, pk, f_clk):
+    """C3 single-step API (HBM roofline), C1/C2 (latency-bound), C4 exactly, and the open-loop
+    dynamics mode."""
+    out = small_configs(pkg, inputs, torch, dev)
+    out["C4_mlp_rollout"] = c4_exact(pkg, inputs, torch, dev)
+    torch.cuda.empty_cache()
     stream = torch.cuda.current_stream()
     # C3: 2^20 envs, DR, l2f_step, ring of 8 action buffers (16 MiB each; > L2 in total with state)
     n = 1 << 20

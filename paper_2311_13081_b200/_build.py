@@ -16,7 +16,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-ftz=true", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 # Per-source extra flags (overridable per file with L2F_NVCC_<NAME>, e.g. L2F_NVCC_L2F_TD3): ptxas
-# register-usage levels chosen by measurement (scripts/dbg/all_ab.sh).
+# register-usage levels chosen by measurement (scripts/ab/all_ab.sh).
 PER_SOURCE = {"l2f_mlp.cu": "-Xptxas --register-usage-level=8",  # rollout +0.5-1 %
               "l2f_td3.cu": "-Xptxas --register-usage-level=3"}  # TD3 +1 %
 

@@ -64,8 +64,8 @@ constexpr size_t kPolicyMaxIn = 18 + 4 * L2F_MAX_HIST;
 constexpr size_t kPolicyHalfs = 64 * kPolicyMaxIn + 64 + 64 * 64 + 64 + 4 * 64 + 4;
 
 struct Layout {
-    size_t state, dist, dr, hist, hist_t0, hist_fill, ep_step, ep_return, slots, stats_out, st_act, st_obs, st_rew, st_flags,
-        st_policy, total;
+    size_t state, dist, dr, hist, hist_t0, hist_fill, ep_step, ep_return, slots, stats_out, fin_part, st_act, st_obs,
+        st_rew, st_flags, st_policy, total;
     int32_t n_slots;
 };
 
@@ -90,6 +90,7 @@ Layout layout_for(const l2f_config& c)
     L.ep_return = take(4 * N);
     L.slots = take(8 * (size_t)L.n_slots * L2F_STATS_LEN);
     L.stats_out = take(8 * L2F_STATS_LEN);
+    L.fin_part = take(stats_finalize_scratch_bytes());  // partials + arrival ticket of the finalize reduction
     L.st_act = take(4 * N * 4);
     L.st_obs = take(4 * N * L2F_OBS_CORE);
     L.st_rew = take(4 * N);
@@ -391,6 +392,7 @@ l2f_status l2f_reset(l2f_env* env, const uint8_t* d_mask, const l2f_step_out* ou
         // full reset: statistics and the (lazily overwritten) history ring start from zero, so
         // the whole workspace state is a deterministic function of (config, t, actions)
         cudaError_t e = cudaMemsetAsync(env->B.slots, 0, sizeof(double) * L2F_STATS_LEN * env->L.n_slots, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(env->ws + env->L.fin_part, 0, stats_finalize_scratch_bytes(), s);
         if (e == cudaSuccess && env->cfg.action_history > 0)
             e = cudaMemsetAsync(env->B.hist, 0, sizeof(float) * 4 * (size_t)env->cfg.action_history * env->cfg.num_envs, s);
         if (e != cudaSuccess) return cuda_fail(e, "l2f_reset memset");
@@ -588,7 +590,8 @@ l2f_status l2f_episode_stats(l2f_env* env, double* d_out, int32_t reset_accumula
 {
     if (!env || !d_out) return fail(L2F_ERR_INVALID_ARGUMENT, "env/out is NULL");
     const DeviceGuard guard(env->device);
-    l2f_status st = launched(launch_stats_finalize(env->B.slots, env->L.n_slots, d_out, reset_accumulators,
+    l2f_status st = launched(launch_stats_finalize(env->B.slots, env->L.n_slots, env->ws + env->L.fin_part, d_out,
+                                                   reset_accumulators,
                                                    env->steps, (cudaStream_t)stream),
                              "l2f_episode_stats");
     if (st == L2F_OK && reset_accumulators) env->steps = 0.0;

@@ -63,8 +63,10 @@ cudaError_t launch_philox_selftest(int64_t n, uint64_t seed, uint32_t t, uint32_
                                    cudaStream_t s);
 cudaError_t launch_recompute_rewards(const StageW& W, const float* next_state, const float* actions, int64_t m,
                                      float* rewards, cudaStream_t s);
-cudaError_t launch_stats_finalize(double* slots, int32_t n_slots, double* out, int32_t reset, double host_steps,
-                                  cudaStream_t s);
+// Bytes of workspace scratch the statistics finalize needs (per-block partials + a ticket).
+size_t stats_finalize_scratch_bytes();
+cudaError_t launch_stats_finalize(double* slots, int32_t n_slots, void* scratch, double* out, int32_t reset,
+                                  double host_steps, cudaStream_t s);
 
 // tcgen05 actor-MLP rollout (l2f_mlp.cu).  Returns cudaErrorNotSupported for unsupported shapes.
 int mlp_rollout_grid(int64_t n);

@@ -334,33 +334,62 @@ cudaError_t launch_recompute_rewards(const StageW& W, const float* next_state, c
     return cudaGetLastError();
 }
 
-// Fixed-order reduction of all statistics slots into out[8] (one block of 256 threads).
-__global__ void __launch_bounds__(256) stats_finalize_kernel(double* __restrict__ slots, int32_t n_slots,
-                                                             double* __restrict__ out, int32_t reset,
-                                                             double host_steps)
+// Fixed-order reduction of all statistics slots into out[8], deterministic for a given n_slots:
+// block b of kFinBlocks sums the contiguous slot range [b S / kFinBlocks, (b + 1) S / kFinBlocks)
+// (thread-strided, then a fixed shared-memory tree) into partial b; the block that arrives last
+// (ticket) sums the partials in block order.  (One 256-thread block over 16 384 slots took ~60 us;
+// this takes a few us.)
+constexpr int kFinBlocks = 64;
+constexpr int kFinThreads = 256;
+
+size_t stats_finalize_scratch_bytes() { return sizeof(double) * kStatsLen * kFinBlocks + 256; }
+
+__global__ void __launch_bounds__(kFinThreads) stats_finalize_kernel(double* __restrict__ slots, int32_t n_slots,
+                                                                     double* __restrict__ part,
+                                                                     unsigned int* __restrict__ ticket,
+                                                                     double* __restrict__ out, int32_t reset,
+                                                                     double host_steps)
 {
-    __shared__ double part[256 * kStatsLen];
-    const int tid = threadIdx.x;
+    __shared__ double red[kFinThreads * kStatsLen];
+    __shared__ bool last;
+    const int tid = threadIdx.x, b = blockIdx.x;
+    const int lo = (int)((int64_t)n_slots * b / kFinBlocks), hi = (int)((int64_t)n_slots * (b + 1) / kFinBlocks);
     double acc[kStatsLen];
 #pragma unroll
     for (int j = 0; j < kStatsLen; ++j) acc[j] = 0.0;
-    for (int s = tid; s < n_slots; s += 256)
+    for (int sl = lo + tid; sl < hi; sl += kFinThreads) {
+        double* row = slots + (size_t)sl * kStatsLen;
+        const double4 a = reinterpret_cast<const double4*>(row)[0], c = reinterpret_cast<const double4*>(row)[1];
+        acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
+        acc[4] += c.x, acc[5] += c.y, acc[6] += c.z, acc[7] += c.w;
+        if (reset) {
+            const double4 z = make_double4(0.0, 0.0, 0.0, 0.0);
+            reinterpret_cast<double4*>(row)[0] = z;
+            reinterpret_cast<double4*>(row)[1] = z;
+        }
+    }
 #pragma unroll
-        for (int j = 0; j < kStatsLen; ++j) acc[j] += slots[(size_t)s * kStatsLen + j];
-#pragma unroll
-    for (int j = 0; j < kStatsLen; ++j) part[tid * kStatsLen + j] = acc[j];
+    for (int j = 0; j < kStatsLen; ++j) red[j * kFinThreads + tid] = acc[j];
     __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
+    for (int w = kFinThreads / 2; w > 0; w >>= 1) {
         if (tid < w)
 #pragma unroll
-            for (int j = 0; j < kStatsLen; ++j) part[tid * kStatsLen + j] += part[(tid + w) * kStatsLen + j];
+            for (int j = 0; j < kStatsLen; ++j) red[j * kFinThreads + tid] += red[j * kFinThreads + tid + w];
         __syncthreads();
     }
-    if (tid < kStatsLen) out[tid] = tid == kStatsLen - 1 ? host_steps : part[tid];
-    if (reset) {
-        __syncthreads();
-        for (int s = tid; s < n_slots * kStatsLen; s += 256) slots[s] = 0.0;
+    if (tid < kStatsLen) part[b * kStatsLen + tid] = red[tid * kFinThreads];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(ticket, 1u) == kFinBlocks - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (tid < kStatsLen) {
+        double x = 0.0;
+        for (int k = 0; k < kFinBlocks; ++k) x += __ldcg(part + k * kStatsLen + tid);
+        out[tid] = tid == kStatsLen - 1 ? host_steps : x;
     }
+    if (tid == 0) *ticket = 0u;  // ready for the next call (the next launch is stream-ordered)
 }
 
 // Self-test: our Philox4x32-10 vs curand's curand_Philox4x32_10 (an independent library
@@ -427,10 +456,12 @@ cudaError_t launch_rollout_open(const DevParams& P, const DevBufs& B, const floa
     return cudaGetLastError();
 }
 
-cudaError_t launch_stats_finalize(double* slots, int32_t n_slots, double* out, int32_t reset, double host_steps,
-                                  cudaStream_t s)
+cudaError_t launch_stats_finalize(double* slots, int32_t n_slots, void* scratch, double* out, int32_t reset,
+                                  double host_steps, cudaStream_t s)
 {
-    stats_finalize_kernel<<<1, 256, 0, s>>>(slots, n_slots, out, reset, host_steps);
+    double* part = static_cast<double*>(scratch);
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(part + kStatsLen * kFinBlocks);
+    stats_finalize_kernel<<<kFinBlocks, kFinThreads, 0, s>>>(slots, n_slots, part, ticket, out, reset, host_steps);
     return cudaGetLastError();
 }
 

@@ -1,8 +1,8 @@
 #!/bin/bash
-# A/B of library builds scripts/dbg/libl2f_<tag>.so: main MLP line + C3 step (alternating twice)
+# A/B of library builds build/ab/libl2f_<tag>.so: main MLP line + C3 step (alternating twice)
 for rep in 1 2; do
 for t in "$@"; do
-  cp scripts/dbg/libl2f_$t.so paper_2311_13081_b200/libl2f.so
+  cp build/ab/libl2f_$t.so paper_2311_13081_b200/libl2f.so
   python bench.py --steps 3 --warmup 2 --no-secondary --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$t mlp', d['value'], d['ms_per_step'])"
   python scripts/time_step.py | sed "s/^/$t /"
 done

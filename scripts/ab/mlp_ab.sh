@@ -1,8 +1,8 @@
 #!/bin/bash
-# MLP-rollout A/B: bench value for each scripts/dbg/libl2f_<tag>.so, alternating twice
+# MLP-rollout A/B: bench value for each build/ab/libl2f_<tag>.so, alternating twice
 for rep in 1 2; do
 for t in "$@"; do
-  cp scripts/dbg/libl2f_$t.so paper_2311_13081_b200/libl2f.so
+  cp build/ab/libl2f_$t.so paper_2311_13081_b200/libl2f.so
   python bench.py --steps 3 --warmup 2 --no-secondary --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$t', d['value'])"
 done
 done
