@@ -5,7 +5,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libl2f.so")
+# L2F_LIB_PATH: another build of the same library (e.g. the -DL2F_DEBUG_CHECKS build of
+# scripts/debug_checks.sh); default the in-tree libl2f.so
+LIB_PATH = os.environ.get("L2F_LIB_PATH") or os.path.join(HERE, "libl2f.so")
 
 ABI_VERSION = 2
 STATE_DIM, OBS_CORE, MAX_HIST, STATS_LEN, TRACE_FIELDS = 17, 18, 32, 8, 32

@@ -7,7 +7,26 @@
 // This file is independent of oracle/ (no shared code, tables or constants).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
+
+// Debug build (-DL2F_DEBUG_CHECKS, scripts/debug_checks.sh): bounds and protocol checks on every
+// global / shared / tensor-memory index the kernels form, and bounded mbarrier waits; a failed
+// check prints and traps.  (compute-sanitizer is not available on the measurement pool.)
+#ifdef L2F_DEBUG_CHECKS
+#define L2F_CHECK(cond, what)                                                                          \
+    do {                                                                                               \
+        if (!(cond)) {                                                                                 \
+            printf("L2F_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,      \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                 \
+            __trap();                                                                                  \
+        }                                                                                              \
+    } while (0)
+#else
+#define L2F_CHECK(cond, what) \
+    do {                      \
+    } while (0)
+#endif
 
 namespace l2f {
 
@@ -325,6 +344,7 @@ template <int C>
 __device__ __forceinline__ void grp_load(const float4* base, int64_t i, int64_t N, float* out)
 {
     constexpr int G = C / 4, R = C % 4;
+    L2F_CHECK(i >= 0 && i < N, "grp_load index");
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         const float4 v = base[g * N + i];
@@ -344,6 +364,7 @@ template <int C>
 __device__ __forceinline__ void grp_load_scalar(const float4* base4, int64_t i, int64_t N, float* out)
 {
     constexpr int G = C / 4, R = C % 4;
+    L2F_CHECK(i >= 0 && i < N, "grp_load_scalar index");
     const float* base = reinterpret_cast<const float*>(base4);
 #pragma unroll
     for (int c = 0; c < 4 * G; ++c) out[c] = base[((c / 4) * N + i) * 4 + (c % 4)];
@@ -355,6 +376,7 @@ template <int C>
 __device__ __forceinline__ void grp_store(float4* base, int64_t i, int64_t N, const float* v)
 {
     constexpr int G = C / 4, R = C % 4;
+    L2F_CHECK(i >= 0 && i < N, "grp_store index");
 #pragma unroll
     for (int g = 0; g < G; ++g) base[g * N + i] = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
     if constexpr (R == 1) {
@@ -370,6 +392,7 @@ __device__ __forceinline__ void grp_store(float4* base, int64_t i, int64_t N, co
 template <int C, class T>
 __device__ __forceinline__ void soa_load(const T* base, int64_t i, uint32_t n, T* out)
 {
+    L2F_CHECK(i >= 0 && i < (int64_t)n, "soa index");
     const T* q = base + i;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -380,6 +403,7 @@ __device__ __forceinline__ void soa_load(const T* base, int64_t i, uint32_t n, T
 template <int C, class T>
 __device__ __forceinline__ void soa_load_ro(const T* __restrict__ base, int64_t i, uint32_t n, T* out)
 {
+    L2F_CHECK(i >= 0 && i < (int64_t)n, "soa index");
     const T* q = base + i;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -390,6 +414,7 @@ __device__ __forceinline__ void soa_load_ro(const T* __restrict__ base, int64_t 
 template <int C, class T>
 __device__ __forceinline__ void soa_store(T* base, int64_t i, uint32_t n, const T* v)
 {
+    L2F_CHECK(i >= 0 && i < (int64_t)n, "soa index");
     T* q = base + i;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -747,7 +772,9 @@ __device__ __forceinline__ bool reset_env_warp(const DevParams& P, const float4*
     for (int round = 0; round * kPer < nr; ++round) {
         const int q = round * kPer + my_q;
         float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        L2F_CHECK(nr <= 32 && rank < 32, "reset rank");
         if (my_q < kPer && q < nr && slot_used) {
+            L2F_CHECK(q >= 0 && q < 32 && rl[q] >= 0 && rl[q] < 32, "reset rank->lane table");
             const uint4 blk = reset_block(P, gid - (uint32_t)lane + (uint32_t)rl[q], ctr, b);
             x = tab ? reset_values_tab(tab, b, blk) : reset_values(P, b, blk);
         }
@@ -827,6 +854,7 @@ __device__ __forceinline__ void hist_entry(const DevBufs& B, int64_t N, int n_hi
                                            int32_t t0, float h[4])
 {
     const int64_t tau = t - 1 - k;
+    L2F_CHECK(i >= 0 && i < N && k >= 0 && k < n_hist, "hist_entry index");
     if (tau >= (int64_t)t0) {
         const int slot = (int)(((tau % n_hist) + n_hist) % n_hist);
         const float4 v = B.hist[(int64_t)slot * N + i];

@@ -88,6 +88,7 @@ __device__ __forceinline__ void write_dense(const DevParams& P, const DevBufs& B
 
 __device__ __forceinline__ void stats_block_end(const StatAcc& st, double* srow, double steps, double* slot)
 {
+    L2F_CHECK(blockIdx.x < gridDim.x, "statistics slot");
     const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const bool any = __any_sync(0xffffffffu, st.ep > 0);
     if (any) {
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const D
     if (active) {
         if (P.n_hist > 0) {
             const int slot = P.hist_slot0;  // t0 mod N_H (written for every env: deterministic ring)
+            L2F_CHECK(slot >= 0 && slot < P.n_hist, "history slot");
             B.hist[(int64_t)slot * N + i] = make_float4(o.a[0], o.a[1], o.a[2], o.a[3]);
             if (did_reset) hist_restart(P, B, i, t + 1, hf);
         }
@@ -257,6 +259,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
         } else {
             random_action(P, gid, t, a);
         }
+        L2F_CHECK(tslot < K && k >= 0 && k < T, "trace index");
         float* tr = (tslot >= 0) ? trace + ((int64_t)k * K + tslot) * kTraceFields : nullptr;
         if (tr) {
 #pragma unroll
@@ -281,6 +284,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
             e.ep_return = 0.0f;
         }
         if (active && P.n_hist > 0) {
+            L2F_CHECK(slot >= 0 && slot < P.n_hist, "history slot");
             B.hist[(int64_t)slot * N + i] = make_float4(o.a[0], o.a[1], o.a[2], o.a[3]);
             if (did_reset) hist_restart(P, B, i, t + 1, hf);
         }

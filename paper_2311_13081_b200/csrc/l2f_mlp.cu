@@ -79,8 +79,23 @@ constexpr uint32_t kIdescN16 = tc::make_idesc(128, 16, 0, 0);
 
 __device__ __forceinline__ uint16_t h16(const uint16_t* p, int i) { return __ldg(p + i); }
 
+// Debug build: a shared-memory access of `bytes` at saddr lies inside this kernel's dynamic
+// shared memory.
+__device__ __forceinline__ void smem_check(uint32_t saddr, uint32_t bytes)
+{
+#ifdef L2F_DEBUG_CHECKS
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t base = tc::smem_u32(smem);
+    L2F_CHECK(saddr >= base && saddr + bytes <= base + kSmemBytes, "shared-memory address");
+#else
+    (void)saddr;
+    (void)bytes;
+#endif
+}
+
 __device__ __forceinline__ void st_u16(uint32_t saddr, uint16_t v)
 {
+    smem_check(saddr, 2);
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(saddr), "h"(v) : "memory");
 }
 
@@ -325,6 +340,8 @@ __device__ __forceinline__ uint32_t a1_row(const GroupCtx& c, int k) { return c.
 __device__ __forceinline__ void write_obs_row(const GroupCtx& c, int k, const float o[kObsCore])
 {
     const uint32_t row = a1_row(c, k);
+    smem_check(row, 16);
+    smem_check(row + 2 * kChunkA, 16);
     tc::sts128(row, tc::pack_h2(o[0], o[1]), tc::pack_h2(o[2], o[3]), tc::pack_h2(o[4], o[5]),
                tc::pack_h2(o[6], o[7]));
     tc::sts128(row + kChunkA, tc::pack_h2(o[8], o[9]), tc::pack_h2(o[10], o[11]), tc::pack_h2(o[12], o[13]),
@@ -335,7 +352,10 @@ __device__ __forceinline__ void write_obs_row(const GroupCtx& c, int k, const fl
 // history ring position p of tile slot k -> A1 address (8 bytes: 4 fp16)
 __device__ __forceinline__ uint32_t hist_addr(const GroupCtx& c, int k, int p)
 {
-    return a1_row(c, k) + (4 + (p >> 1)) * kChunkA + (p & 1) * 8;
+    L2F_CHECK(p >= 0 && p < kMaxHist, "history ring position");
+    const uint32_t a = a1_row(c, k) + (4 + (p >> 1)) * kChunkA + (p & 1) * 8;
+    smem_check(a, 8);
+    return a;
 }
 
 __device__ void setup_cta(const PolicyDev& W, uint32_t sbase, int n_hist, const DevParams* P = nullptr)
@@ -513,6 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < kE; ++k) {
                 if (tslot[k] >= 0) {  // (traced envs only: the address is not formed otherwise)
+                    L2F_CHECK(tslot[k] < K && ks >= 0 && ks < T, "trace index");
                     float* tr = trace + ((int64_t)ks * K + tslot[k]) * kTraceFields;
 #pragma unroll
                     for (int q = 0; q < kStateDim; ++q) tr[q] = e[k].s[q];
@@ -606,6 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     // statistics: per-warp rows (flushed per unit) -> fixed-order block sum -> this CTA's slot
     __syncthreads();
+    L2F_CHECK((int)blockIdx.x < B.n_slots, "statistics slot");
     if (threadIdx.x < kStatsLen) {
         const double* rows = reinterpret_cast<const double*>(smem + OFF_WSTAT);
         double x = 0.0;

@@ -8,6 +8,18 @@
 namespace l2f {
 namespace tc {
 
+// Debug build: a TMEM access of `ncols` columns at taddr stays inside the 512 allocated columns
+// and addresses the 32-lane quadrant of the calling warp (tcgen05.ld/st 32x32b access rule).
+#ifdef L2F_DEBUG_CHECKS
+#define L2F_TMEM_CHECK(taddr, ncols)                                                             \
+    L2F_CHECK(((taddr) & 0xFFFFu) + (ncols) <= 512u && ((taddr) >> 16) == 32u * ((threadIdx.x >> 5) & 3u), \
+              "tmem address")
+#else
+#define L2F_TMEM_CHECK(taddr, ncols) \
+    do {                             \
+    } while (0)
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // UMMA shared-memory matrix descriptor, SWIZZLE_NONE ("interleaved" canonical layout):
@@ -178,6 +190,20 @@ __device__ __forceinline__ void mbar_arrive(uint32_t mbar_saddr)
 #endif
 __device__ __forceinline__ void mbar_wait(uint32_t mbar_saddr, uint32_t parity)
 {
+#ifdef L2F_DEBUG_CHECKS
+    // bounded wait: a phase that never completes (lost commit, wrong parity) traps instead of hanging
+    uint32_t done = 0;
+    for (uint32_t it = 0; it < (1u << 24) && !done; ++it)
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n\t}\n"
+            : "=r"(done)
+            : "r"(mbar_saddr), "r"(parity)
+            : "memory");
+    L2F_CHECK(done, "mbarrier wait timed out");
+    return;
+#endif
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "WAIT_%=:\n\t"
@@ -213,6 +239,7 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols)
 // 32 lanes x 32-bit, 16 consecutive columns: thread t of the warp gets row (lane base + t).
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16])
 {
+    L2F_TMEM_CHECK(taddr, 16u);
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
@@ -221,6 +248,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16])
 }
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4])
 {
+    L2F_TMEM_CHECK(taddr, 4u);
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                  : "r"(taddr));
@@ -231,6 +259,7 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 // 32 lanes x 32-bit stores of consecutive columns (thread t -> its own lane).
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v, int off)
 {
+    L2F_TMEM_CHECK(taddr, 8u);
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
                  "f"(v[off + 0]), "f"(v[off + 1]), "f"(v[off + 2]), "f"(v[off + 3]), "f"(v[off + 4]),
                  "f"(v[off + 5]), "f"(v[off + 6]), "f"(v[off + 7])
@@ -238,6 +267,7 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v, int off
 }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16])
 {
+    L2F_TMEM_CHECK(taddr, 16u);
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
             taddr),
@@ -248,18 +278,21 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
 __device__ __forceinline__ void tmem_st8u(uint32_t taddr, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                           uint32_t a4, uint32_t a5, uint32_t a6, uint32_t a7)
 {
+    L2F_TMEM_CHECK(taddr, 8u);
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(a0),
                  "r"(a1), "r"(a2), "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7)
                  : "memory");
 }
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, const float (&v)[4])
 {
+    L2F_TMEM_CHECK(taddr, 4u);
     asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "f"(v[0]), "f"(v[1]),
                  "f"(v[2]), "f"(v[3])
                  : "memory");
 }
 __device__ __forceinline__ void tmem_st2(uint32_t taddr, float a, float b)
 {
+    L2F_TMEM_CHECK(taddr, 2u);
     asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "f"(a), "f"(b) : "memory");
 }
 
