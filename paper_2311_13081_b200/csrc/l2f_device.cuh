@@ -433,6 +433,16 @@ __device__ __forceinline__ bool state_finite(const float* s)
     return isfinite(sum);
 }
 
+// The same decision for a state just produced by rk4_step from a step's inputs, from p, q, w
+// alone: a non-finite v or w_m (or f_r, tau_r, action) cannot leave p' = p + h v + h^2/6 (a1 +
+// a2 + a3), q' and w' all finite -- v enters p' directly, and w_m (before its clamp, which would
+// map NaN to a bound) enters every stage's thrust, hence v' and w' (non-finite or overflowing).
+__device__ __forceinline__ bool stepped_state_finite(const float* s)
+{
+    const float sum = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[10])) + (s[11] + s[12]);
+    return isfinite(sum);
+}
+
 // out = a * h + b over the 7 coupled components: 3 packed FFMA2 pairs + 1 scalar FFMA.
 __device__ __forceinline__ void pair_fma(const float* a, float h, const float* b, float* out)
 {
@@ -521,7 +531,7 @@ __device__ __forceinline__ bool rk4_step(const DevParams& P, const Phys& ph, con
     for (int i = 0; i < 3; ++i) s[10 + i] = y0[4 + i];
 #pragma unroll
     for (int i = 13; i < 17; ++i) s[i] = fminf(fmaxf(s[i], P.rpm_min), P.rpm_max);
-    return !state_finite(s);
+    return !stepped_state_finite(s);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -686,7 +696,8 @@ __device__ __forceinline__ void reset_finish(const DevParams& P, const float4 (&
     e.s[1] = v[0].y;
     e.s[2] = v[0].z;
     const float cz = v[0].w, phi = v[1].x, th = v[1].y;
-    const float sxy = sqrtf(fmaxf(fmaf(-cz, cz, 1.0f), 0.0f));
+    float sxy;  // sqrt(1 - cz^2): MUFU.SQRT (relative error ~2^-23; no IEEE slow path)
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sxy) : "f"(fmaxf(fmaf(-cz, cz, 1.0f), 0.0f)));
     float sp, cp, sh, ch;
     __sincosf(phi, &sp, &cp);
     __sincosf(0.5f * th, &sh, &ch);
@@ -903,27 +914,30 @@ __device__ __forceinline__ void stat_episode(StatAcc& a, const Trans& o)
 }
 
 // Compact per-thread accumulator of one rollout unit (at most 65535 steps per thread between
-// flushes): (episodes | terminated << 16), (truncated | diverged << 16), summed lengths, FP64
-// return sums -- 7 registers instead of StatAcc's 9 in the register-bound fused rollout.
+// flushes): (episodes | terminated << 16), (truncated | diverged << 16), summed lengths, and the
+// unit's return sums in FP32 (a unit of T <= 65535 steps ends at most T episodes per env; the
+// per-unit sums go to FP64 at the flush, so FP32 only carries one env's ~T / 9 returns: relative
+// error ~1e-6 in the reported return moments) -- 5 registers, no FP64 in the step loop.
 struct StatPk {
     uint32_t ep_term, trunc_div, len;
-    double ret, ret2;
+    float ret, ret2;
 };
 
 __device__ __forceinline__ void statpk_zero(StatPk& a)
 {
     a.ep_term = a.trunc_div = a.len = 0u;
-    a.ret = a.ret2 = 0.0;
+    a.ret = a.ret2 = 0.0f;
 }
 
-__device__ __forceinline__ void statpk_episode(StatPk& a, const Trans& o)
+// Branch-free update: `ended` selects whether the transition closed an episode.
+__device__ __forceinline__ void statpk_episode(StatPk& a, const Trans& o, bool ended)
 {
-    a.ep_term += 1u + ((o.flags & D_TERM) ? 0x10000u : 0u);
-    a.trunc_div += ((o.flags & D_TRUNC) ? 1u : 0u) + ((o.flags & D_DIV) ? 0x10000u : 0u);
-    a.len += (uint32_t)o.len;
-    const double r = (double)o.ret;
+    a.ep_term += ended ? 1u + ((o.flags & D_TERM) ? 0x10000u : 0u) : 0u;
+    a.trunc_div += ended ? ((o.flags & D_TRUNC) ? 1u : 0u) + ((o.flags & D_DIV) ? 0x10000u : 0u) : 0u;
+    a.len += ended ? (uint32_t)o.len : 0u;
+    const float r = ended ? o.ret : 0.0f;
     a.ret += r;
-    a.ret2 += r * r;
+    a.ret2 = fmaf(r, r, a.ret2);
 }
 
 // Warp-reduce a unit's accumulator (fixed shuffle order) and add it, with `steps` env-steps, to
@@ -934,7 +948,7 @@ __device__ __forceinline__ void statpk_flush(const StatPk& a, double steps, doub
     const uint32_t ep = __reduce_add_sync(m, a.ep_term & 0xFFFFu), term = __reduce_add_sync(m, a.ep_term >> 16);
     const uint32_t tr = __reduce_add_sync(m, a.trunc_div & 0xFFFFu), dv = __reduce_add_sync(m, a.trunc_div >> 16);
     const uint32_t len = __reduce_add_sync(m, a.len);
-    double r = a.ret, r2 = a.ret2;
+    double r = (double)a.ret, r2 = (double)a.ret2;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         r += __shfl_xor_sync(m, r, o);

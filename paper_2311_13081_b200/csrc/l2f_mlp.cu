@@ -425,8 +425,9 @@ __device__ void teardown_cta()
 // independent dependency chains (Philox, Box-Muller, RK4) interleave in the same basic blocks.
 // -------------------------------------------------------------------------------------------
 // kNH: N_H as a compile-time constant (32, the benchmark's history) or -1 (any N_H % 4 == 0,
-// read from P at run time).
-template <bool kDR, int kNH>
+// read from P at run time).  kTrace: the per-step trace of selected envs is compiled in only
+// when one is requested (its per-step branches cost ~2.5 % of the untraced rollout).
+template <bool kDR, int kNH, bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
     rollout_mlp_kernel(const DevParams P, const DevBufs B, const PolicyDev W, int32_t T, float* __restrict__ trace,
                        const int64_t* __restrict__ trace_ids, int32_t K, int32_t n_units)
@@ -490,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::sts64(hist_addr(c, k, p), tc::pack_h2(h[0], h[1]), tc::pack_h2(h[2], h[3]));
             }
             tslot[k] = -1;
-            if (trace && active[k])
+            if (kTrace && active[k])
                 for (int q = 0; q < K; ++q)
                     if (trace_ids[q] == i[k]) tslot[k] = q;
             if (obs_noise) stash_obs_noise(P, c, k, gid[k], P.t0, 3);
@@ -532,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             Trans o[kE];
 #pragma unroll
             for (int k = 0; k < kE; ++k) {
-                if (tslot[k] >= 0) {  // (traced envs only: the address is not formed otherwise)
+                if (kTrace && tslot[k] >= 0) {  // (traced envs only: the address is not formed otherwise)
                     L2F_CHECK(tslot[k] < K && ks >= 0 && ks < T, "trace index");
                     float* tr = trace + ((int64_t)ks * K + tslot[k]) * kTraceFields;
 #pragma unroll
@@ -554,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < kE; ++k) {
                 uint32_t fl = o[k].flags;
                 const bool ended = (fl & (D_TERM | D_TRUNC)) != 0;
-                if (ended && active[k]) statpk_episode(st, o[k]);
+                statpk_episode(st, o[k], ended && active[k]);
                 L2F_PHASE(c, 14);
                 bool did_reset = false;
                 float hf[4];
@@ -574,13 +575,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // new episode: the lane's whole history row takes the fill value (Q10):
                     // N_H/2 16-byte stores by the resetting lanes only
                     if (did_reset) {
+                        // one register quad stored N_H / 2 times (C++ stores: asm operands made the
+                        // compiler build a fresh quad per store)
                         const uint32_t h01 = tc::pack_h2(hf[0], hf[1]), h23 = tc::pack_h2(hf[2], hf[3]);
+                        const uint4 hv = make_uint4(h01, h23, h01, h23);
+                        uint8_t* const row = smem + (a1_row(c, k) - sbase);
 #pragma unroll
                         for (int q = 0; q < kMaxHist / 2; ++q)
-                            if (q < NH / 2) tc::sts128(a1_row(c, k) + (4 + q) * kChunkA, h01, h23, h01, h23);
+                            if (q < NH / 2) {
+                                smem_check(a1_row(c, k) + (4 + q) * kChunkA, 16);
+                                *reinterpret_cast<uint4*>(row + (4 + q) * kChunkA) = hv;
+                            }
                     }
                 }
-                if (tslot[k] >= 0) {
+                if (kTrace && tslot[k] >= 0) {
                     float* tr = trace + ((int64_t)ks * K + tslot[k]) * kTraceFields;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) tr[21 + q] = o[k].a[q];
@@ -864,11 +872,16 @@ cudaError_t launch_rollout_mlp(const DevParams& P, const DevBufs& B, const Polic
                                const int64_t* trace_ids, int32_t K, cudaStream_t s)
 {
     if (P.n_hist % 4 != 0 || W.hidden != kHid || W.in_dim != 18 + 4 * P.n_hist) return cudaErrorNotSupported;
-    static std::atomic<size_t> attr[4][64] = {};
-    const bool dr = (P.flags & F_DOMAIN_RAND) != 0, h32 = P.n_hist == 32;
-    auto kern = dr ? (h32 ? rollout_mlp_kernel<true, 32> : rollout_mlp_kernel<true, -1>)
-                   : (h32 ? rollout_mlp_kernel<false, 32> : rollout_mlp_kernel<false, -1>);
-    const cudaError_t e = ensure_smem_attr(kern, kSmemBytes, attr[2 * dr + h32]);
+    static std::atomic<size_t> attr[8][64] = {};
+    const bool dr = (P.flags & F_DOMAIN_RAND) != 0, h32 = P.n_hist == 32, tr = trace != nullptr;
+    using Kern = decltype(&rollout_mlp_kernel<true, 32, true>);
+    static const Kern table[8] = {rollout_mlp_kernel<false, -1, false>, rollout_mlp_kernel<false, -1, true>,
+                                  rollout_mlp_kernel<false, 32, false>, rollout_mlp_kernel<false, 32, true>,
+                                  rollout_mlp_kernel<true, -1, false>,  rollout_mlp_kernel<true, -1, true>,
+                                  rollout_mlp_kernel<true, 32, false>,  rollout_mlp_kernel<true, 32, true>};
+    const int sel = 4 * dr + 2 * h32 + tr;
+    const Kern kern = table[sel];
+    const cudaError_t e = ensure_smem_attr(kern, kSmemBytes, attr[sel]);
     if (e != cudaSuccess) return e;
     kern<<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, (int32_t)units_for(P.n));
     return cudaGetLastError();
