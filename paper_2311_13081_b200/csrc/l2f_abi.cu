@@ -436,8 +436,8 @@ l2f_status l2f_rollout(l2f_env* env, const l2f_policy* policy, const float* d_ac
     // split so every launch sees at most kMaxStages curriculum stages
     int32_t done = 0;
     while (done < T) {
-        // (the MLP rollout's packed per-thread statistics hold <= 65535 steps per launch)
-        int32_t chunk = policy ? (T - done < 65535 ? T - done : 65535) : T - done;
+        // (the rollouts' packed per-thread statistics hold <= 65535 steps per launch)
+        int32_t chunk = T - done < 65535 ? T - done : 65535;
         DevParams P;
         while (!params_for(env, env->t, chunk, P)) chunk = chunk / 2 > 0 ? chunk / 2 : 1;
         float* tr = d_trace ? d_trace + (size_t)done * K * L2F_TRACE_FIELDS : nullptr;

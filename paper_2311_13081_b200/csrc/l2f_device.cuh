@@ -940,6 +940,19 @@ __device__ __forceinline__ void statpk_episode(StatPk& a, const Trans& o, bool e
     a.ret2 = fmaf(r, r, a.ret2);
 }
 
+__device__ __forceinline__ StatAcc statpk_unpack(const StatPk& a)
+{
+    StatAcc r;
+    r.ep = (int32_t)(a.ep_term & 0xFFFFu);
+    r.term = (int32_t)(a.ep_term >> 16);
+    r.trunc = (int32_t)(a.trunc_div & 0xFFFFu);
+    r.div = (int32_t)(a.trunc_div >> 16);
+    r.len = (int32_t)a.len;
+    r.ret = (double)a.ret;
+    r.ret2 = (double)a.ret2;
+    return r;
+}
+
 // Warp-reduce a unit's accumulator (fixed shuffle order) and add it, with `steps` env-steps, to
 // the warp's FP64 row (lane 0 writes).  All 32 lanes must call it.
 __device__ __forceinline__ void statpk_flush(const StatPk& a, double steps, double* row)
@@ -963,6 +976,32 @@ __device__ __forceinline__ void statpk_flush(const StatPk& a, double steps, doub
         row[5] += r;
         row[6] += r2;
         row[7] += steps;
+    }
+}
+
+// Warp-reduce a StatPk (integer REDUX, FP32 shuffles in a fixed order) and write lane 0's
+// result as FP64 into smem row[8]; row[7] = 0.  All 32 lanes must call it.
+__device__ __forceinline__ void statpk_warp_to_smem(const StatPk& a, double* row)
+{
+    const unsigned m = 0xffffffffu;
+    const uint32_t ep = __reduce_add_sync(m, a.ep_term & 0xFFFFu), term = __reduce_add_sync(m, a.ep_term >> 16);
+    const uint32_t tr = __reduce_add_sync(m, a.trunc_div & 0xFFFFu), dv = __reduce_add_sync(m, a.trunc_div >> 16);
+    const uint32_t len = __reduce_add_sync(m, a.len);
+    float r = a.ret, r2 = a.ret2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        r += __shfl_xor_sync(m, r, o);
+        r2 += __shfl_xor_sync(m, r2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        row[0] = ep;
+        row[1] = term;
+        row[2] = tr;
+        row[3] = dv;
+        row[4] = len;
+        row[5] = r;
+        row[6] = r2;
+        row[7] = 0.0;
     }
 }
 

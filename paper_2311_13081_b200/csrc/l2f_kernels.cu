@@ -86,13 +86,13 @@ __device__ __forceinline__ void write_dense(const DevParams& P, const DevBufs& B
     }
 }
 
-__device__ __forceinline__ void stats_block_end(const StatAcc& st, double* srow, double steps, double* slot)
+__device__ __forceinline__ void stats_block_end(const StatPk& st, double* srow, double steps, double* slot)
 {
     L2F_CHECK(blockIdx.x < gridDim.x, "statistics slot");
     const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const bool any = __any_sync(0xffffffffu, st.ep > 0);
+    const bool any = __any_sync(0xffffffffu, st.ep_term != 0u);
     if (any) {
-        stat_warp_to_smem(st, srow + warp * kStatsLen);
+        statpk_warp_to_smem(st, srow + warp * kStatsLen);
     } else if ((threadIdx.x & 31) == 0) {
 #pragma unroll
         for (int j = 0; j < kStatsLen; ++j) srow[warp * kStatsLen + j] = 0.0;
@@ -122,8 +122,8 @@ __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const D
     const bool active = i < N;
     const uint32_t t = P.t0;
     const uint32_t gid = P.id_offset + (uint32_t)i;
-    StatAcc st;
-    stat_zero(st);
+    StatPk st;
+    statpk_zero(st);
     EnvReg e;
     float a[4] = {0.f, 0.f, 0.f, 0.f};
     if (active) {
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const D
         soa_store<kStateDim>(O.final_state, i, (uint32_t)N, e.s);
     }
     const bool ended = active && (fl & (D_TERM | D_TRUNC));
-    if (ended) stat_episode(st, o);
+    statpk_episode(st, o, ended);
     bool did_reset = false;
     float hf[4];
     if (P.flags & F_AUTO_RESET) {
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kStepBlock) reset_kernel(const DevParams P, co
 // Open-loop fused rollout: T transitions with the state in registers (N3).  Actions from a
 // [T][4][N] buffer or the Philox RAND_ACT stream.  The history ring stays in HBM.
 // ---------------------------------------------------------------------------------------
-template <bool kDR>
+template <bool kDR, bool kTrace>
 __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevParams P, const DevBufs B,
                                                                      const float* __restrict__ act, int32_t T,
                                                                      float* __restrict__ trace,
@@ -234,10 +234,10 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
     const int64_t i = (int64_t)blockIdx.x * kRolloutBlock + threadIdx.x;
     const bool active = i < N;
     const uint32_t gid = P.id_offset + (uint32_t)i;
-    StatAcc st;
-    stat_zero(st);
+    StatPk st;  // T <= 65535 per launch (l2f_rollout splits longer rollouts)
+    statpk_zero(st);
     int tslot = -1;
-    if (trace && active)
+    if (kTrace && active)
         for (int k = 0; k < K; ++k)
             if (trace_ids[k] == i) tslot = k;
     EnvReg e;
@@ -260,8 +260,8 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
             random_action(P, gid, t, a);
         }
         L2F_CHECK(tslot < K && k >= 0 && k < T, "trace index");
-        float* tr = (tslot >= 0) ? trace + ((int64_t)k * K + tslot) * kTraceFields : nullptr;
-        if (tr) {
+        float* tr = (kTrace && tslot >= 0) ? trace + ((int64_t)k * K + tslot) * kTraceFields : nullptr;
+        if (kTrace && tr) {
 #pragma unroll
             for (int c = 0; c < kStateDim; ++c) tr[c] = e.s[c];
 #pragma unroll
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
         transition<kDR>(P, W, e, gid, t, a, za, o);
         uint32_t fl = o.flags;
         const bool ended = active && (fl & (D_TERM | D_TRUNC));
-        if (ended) stat_episode(st, o);
+        statpk_episode(st, o, ended);
         bool did_reset = false;
         float hf[4];
         if (P.flags & F_AUTO_RESET) {
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
             if (did_reset) hist_restart(P, B, i, t + 1, hf);
         }
         if (++slot == P.n_hist) slot = 0;
-        if (tr) {
+        if (kTrace && tr) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) tr[21 + c] = o.a[c];
             tr[25] = o.reward;
@@ -453,10 +453,10 @@ cudaError_t launch_rollout_open(const DevParams& P, const DevBufs& B, const floa
                                 const int64_t* trace_ids, int32_t K, cudaStream_t s)
 {
     const int64_t grid = (P.n + kRolloutBlock - 1) / kRolloutBlock;
-    if (P.flags & F_DOMAIN_RAND)
-        rollout_open_kernel<true><<<(unsigned)grid, kRolloutBlock, 0, s>>>(P, B, act, T, trace, trace_ids, K);
-    else
-        rollout_open_kernel<false><<<(unsigned)grid, kRolloutBlock, 0, s>>>(P, B, act, T, trace, trace_ids, K);
+    const bool dr = (P.flags & F_DOMAIN_RAND) != 0, tr = trace != nullptr;
+    auto kern = dr ? (tr ? rollout_open_kernel<true, true> : rollout_open_kernel<true, false>)
+                   : (tr ? rollout_open_kernel<false, true> : rollout_open_kernel<false, false>);
+    kern<<<(unsigned)grid, kRolloutBlock, 0, s>>>(P, B, act, T, trace, trace_ids, K);
     return cudaGetLastError();
 }
 

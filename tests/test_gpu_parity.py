@@ -228,7 +228,8 @@ def test_c2_subset_parity(pkg):
 # ------------------------------------------------------------------------------------------
 def test_T_steps_equal_rollout_bitwise(pkg):
     """T x l2f_step and l2f_rollout(T) run the same device arithmetic: bitwise equal state,
-    history, counters and statistics."""
+    history, counters and statistic counts; the return sums agree to FP32 partial-sum rounding
+    (per-step warp sums vs a per-thread FP32 sum over the launch)."""
     cfg = inputs.config_c3()  # C2 features + DR
     n, T = 5000, 40
     acts = inputs.actions_near_hover(T, n, seed=3)
@@ -247,7 +248,7 @@ def test_T_steps_equal_rollout_bitwise(pkg):
     for k in s1:
         assert np.array_equal(s1[k], s2[k]), k
     assert np.array_equal(st1[[0, 1, 2, 3, 4, 7]], st2[[0, 1, 2, 3, 4, 7]])
-    assert np.allclose(st1, st2, rtol=1e-12)
+    assert np.allclose(st1[[5, 6]], st2[[5, 6]], rtol=2e-6)
     assert e1.t == e2.t == T
 
 
