@@ -559,19 +559,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 L2F_PHASE(c, 14);
                 bool did_reset = false;
                 float hf[4];
-                if (P.flags & F_AUTO_RESET) {
+                if (P.flags & F_AUTO_RESET)
                     did_reset = reset_env_warp<kDR ? 8 : 6>(P, rtab, e[k], gid[k], t + 1, ended && active[k], hf, rscratch);
-                    if (did_reset) fl |= D_RESET;
-                }
+                fl |= did_reset ? D_RESET : 0u;
                 L2F_PHASE(c, 15);
-                if (ended && !did_reset) {
-                    e[k].ep_step = 0;
-                    e[k].ep_return = 0.0f;
-                }
+                // an episode that ended without auto-reset restarts its counters (selects, no branch)
+                const bool restart = ended && !did_reset;
+                e[k].ep_step = restart ? 0 : e[k].ep_step;
+                e[k].ep_return = restart ? 0.0f : e[k].ep_return;
                 if (NH > 0) {
-                    if (!did_reset)
-                        tc::sts64(hist_addr(c, k, wpos), tc::pack_h2(o[k].a[0], o[k].a[1]),
-                                  tc::pack_h2(o[k].a[2], o[k].a[3]));
+                    // the applied action into its ring slot, for every lane (a reset's refill below
+                    // overwrites it, in program order)
+                    tc::sts64(hist_addr(c, k, wpos), tc::pack_h2(o[k].a[0], o[k].a[1]), tc::pack_h2(o[k].a[2], o[k].a[3]));
                     // new episode: the lane's whole history row takes the fill value (Q10):
                     // N_H/2 16-byte stores by the resetting lanes only
                     if (did_reset) {
