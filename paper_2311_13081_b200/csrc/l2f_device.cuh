@@ -91,6 +91,15 @@ struct DevParams {
     StageW stage[kMaxStages];
 };
 
+// Feature flags of a launch: the run-time P.flags, or a compile-time set kF for kernels
+// specialised on one feature mix (kAnyFlags = read P.flags), so flag tests fold away.
+constexpr uint32_t kAnyFlags = 0xFFFFFFFFu;
+template <uint32_t kF>
+__device__ __forceinline__ uint32_t flags_of(const DevParams& P)
+{
+    return kF == kAnyFlags ? P.flags : kF;
+}
+
 // Workspace views: structure of arrays of float4 groups plus a tail (grp_load): a warp moves each
 // group as 512 contiguous bytes with one 128-bit access per thread, and no byte is padding.
 struct DevBufs {
@@ -606,14 +615,15 @@ __device__ __forceinline__ void observe_critic(const float* s, const float* dist
 // W: the curriculum stage of step t (stage_of), hoisted by the callers' stage loops.
 // kDR: per-env domain-randomised parameters (compile-time so the DR-free path keeps the
 // nominal parameters in the constant bank instead of registers).
-template <bool kDR>
+template <bool kDR, uint32_t kF = kAnyFlags>
 __device__ __forceinline__ void transition(const DevParams& P, const StageW& W, EnvReg& e, uint32_t gid,
                                            uint32_t t, const float a_in[4], const float z[4], Trans& o)
 {
+    const uint32_t flags = flags_of<kF>(P);
     // branch-free on the feature flags (selects), so several envs' transitions can share one
     // basic block and interleave their dependency chains
-    const bool act_noise = (P.flags & F_ACTION_NOISE) != 0;
-    const bool no_delay = (P.flags & F_NO_ROTOR_DELAY) != 0;
+    const bool act_noise = (flags & F_ACTION_NOISE) != 0;
+    const bool no_delay = (flags & F_NO_ROTOR_DELAY) != 0;
     float u[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -634,7 +644,7 @@ __device__ __forceinline__ void transition(const DevParams& P, const StageW& W, 
     const float r = div ? 0.0f : rw;  // Q26
     const float pinf = fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2])));
     const bool out = (pinf > P.term_pos) | (vv > P.term_vel2) | (ww > P.term_angvel2);
-    const bool term = div | (((P.flags & F_TERMINATION) != 0) & out);
+    const bool term = div | (((flags & F_TERMINATION) != 0) & out);
     e.ep_step += 1;
     e.ep_return += r;
     const bool trunc = (!term) & (P.max_ep > 0) & (e.ep_step >= P.max_ep);
@@ -690,8 +700,10 @@ __device__ __forceinline__ float4 reset_values_tab(const float4* tab, int b, uin
 // Assemble the new episode from the sampled values of its 8 slots: state (uniform axis-angle
 // quaternion, Q17), disturbance, DR factors, episode counters; the history fill value per
 // rotor (Q10) in hfill.
+template <uint32_t kF = kAnyFlags>
 __device__ __forceinline__ void reset_finish(const DevParams& P, const float4 (&v)[8], EnvReg& e, float hfill[4])
 {
+    const uint32_t flags = flags_of<kF>(P);
     e.s[0] = v[0].x;
     e.s[1] = v[0].y;
     e.s[2] = v[0].z;
@@ -715,7 +727,7 @@ __device__ __forceinline__ void reset_finish(const DevParams& P, const float4 (&
     e.s[14] = v[3].y;
     e.s[15] = v[3].z;
     e.s[16] = v[3].w;
-    if (P.flags & F_DISTURBANCE) {
+    if (flags & F_DISTURBANCE) {
         e.dist[0] = v[4].x;
         e.dist[1] = v[4].y;
         e.dist[2] = v[4].z;
@@ -726,7 +738,7 @@ __device__ __forceinline__ void reset_finish(const DevParams& P, const float4 (&
 #pragma unroll
         for (int j = 0; j < 6; ++j) e.dist[j] = 0.0f;
     }
-    if (P.flags & F_DOMAIN_RAND) {
+    if (flags & F_DOMAIN_RAND) {
         e.dr[0] = v[6].x;
         e.dr[1] = v[6].y;
         e.dr[2] = v[6].z;
@@ -761,10 +773,11 @@ __device__ __forceinline__ void reset_env(const DevParams& P, EnvReg& e, uint32_
 // with domain randomisation (RESET 0-3, DIST 0-1, DR 0-1), 6 without (5 resets per round; the
 // DR slots stay unset and reset_finish ignores them).  Bitwise identical to reset_env (same
 // integer Philox, same per-value fma).
-template <int kNB>
+template <int kNB, uint32_t kF = kAnyFlags>
 __device__ __forceinline__ bool reset_env_warp(const DevParams& P, const float4* tab, EnvReg& e, uint32_t gid,
                                                uint32_t ctr, bool need, float hfill[4], uint4* scratch)
 {
+    const uint32_t flags = flags_of<kF>(P);
     static_assert(kNB == 6 || kNB == 8, "6 or 8 Philox blocks per reset");
     const unsigned m = __ballot_sync(0xffffffffu, need);
     if (m == 0u) return false;
@@ -777,7 +790,7 @@ __device__ __forceinline__ bool reset_env_warp(const DevParams& P, const float4*
     if (need) rl[rank] = lane;
     __syncwarp();
     const int my_q = lane / kNB, b = lane - my_q * kNB;  // reset (within the round) and slot of this lane
-    const bool slot_used = b < 4 || (b < 6 && (P.flags & F_DISTURBANCE)) || (b >= 6 && (P.flags & F_DOMAIN_RAND));
+    const bool slot_used = b < 4 || (b < 6 && (flags & F_DISTURBANCE)) || (b >= 6 && (flags & F_DOMAIN_RAND));
     float4 v[8];
     if constexpr (kNB == 6) v[6] = v[7] = make_float4(1.f, 1.f, 1.f, 1.f);
     for (int round = 0; round * kPer < nr; ++round) {
@@ -799,7 +812,7 @@ __device__ __forceinline__ bool reset_env_warp(const DevParams& P, const float4*
         }
     }
     __syncwarp();
-    if (need) reset_finish(P, v, e, hfill);
+    if (need) reset_finish<kF>(P, v, e, hfill);
     return need;
 }
 
@@ -820,6 +833,7 @@ __device__ __forceinline__ void obs_noise_blocks(const DevParams& P, uint32_t gi
 }
 
 // Noisy core observation {p, R(q) row-major, v, w} (Q8) from given normals.
+template <uint32_t kF = kAnyFlags>
 __device__ __forceinline__ void observe_core_z(const DevParams& P, const float* s, const float z[20],
                                                float o[kObsCore])
 {
@@ -842,7 +856,7 @@ __device__ __forceinline__ void observe_core_z(const DevParams& P, const float* 
     o[15] = s[10];
     o[16] = s[11];
     o[17] = s[12];
-    if (P.flags & F_OBS_NOISE) {
+    if (flags_of<kF>(P) & F_OBS_NOISE) {
 #pragma unroll
         for (int i = 0; i < kObsCore; ++i) {
             const int g = i < 3 ? 0 : (i < 12 ? 1 : (i < 15 ? 2 : 3));

@@ -427,7 +427,7 @@ __device__ void teardown_cta()
 // kNH: N_H as a compile-time constant (32, the benchmark's history) or -1 (any N_H % 4 == 0,
 // read from P at run time).  kTrace: the per-step trace of selected envs is compiled in only
 // when one is requested (its per-step branches cost ~2.5 % of the untraced rollout).
-template <bool kDR, int kNH, bool kTrace>
+template <bool kDR, int kNH, bool kTrace, uint32_t kF = kAnyFlags>
 __global__ void __launch_bounds__(kThreads, 1)
     rollout_mlp_kernel(const DevParams P, const DevBufs B, const PolicyDev W, int32_t T, float* __restrict__ trace,
                        const int64_t* __restrict__ trace_ids, int32_t K, int32_t n_units)
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     double* const wrow = reinterpret_cast<double*>(smem + OFF_WSTAT) + (threadIdx.x >> 5) * kStatsLen;
     if ((threadIdx.x & 31) < kStatsLen) wrow[threadIdx.x & 31] = 0.0;
     __syncwarp();
-    const bool obs_noise = (P.flags & F_OBS_NOISE) != 0;
+    const bool obs_noise = (flags_of<kF>(P) & F_OBS_NOISE) != 0;
 
     // unit u = tiles u kE .. u kE + kE - 1 (one per tile slot)
     for (int u = blockIdx.x * kG + (int)(threadIdx.x / kM); u < n_units; u += gridDim.x * kG) {
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float ob[kObsCore];
                 float z[20];
                 if (obs_noise) load_obs_noise(c, k, z);
-                observe_core_z(P, e[k].s, z, ob);
+                observe_core_z<kF>(P, e[k].s, z, ob);
                 write_obs_row(c, k, ob);
             }
             float a[kE][4], za[kE][4];
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int k = 0; k < kE; ++k) {
                     if (l == 3) {  // this step's action noise (two Philox chains per hook: 2 obs / 2 obs / obs + action)
                         box_muller2(draw(P, gid[k], t, S_ACT, 0), za[k]);
-                        const bool an = (P.flags & F_ACTION_NOISE) != 0;
+                        const bool an = (flags_of<kF>(P) & F_ACTION_NOISE) != 0;
 #pragma unroll
                         for (int q = 0; q < 4; ++q) za[k][q] = an ? za[k][q] : 0.0f;
                     }
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
 #pragma unroll
-            for (int k = 0; k < kE; ++k) transition<kDR>(P, W, e[k], gid[k], t, a[k], za[k], o[k]);
+            for (int k = 0; k < kE; ++k) transition<kDR, kF>(P, W, e[k], gid[k], t, a[k], za[k], o[k]);
 #ifdef L2F_PHASE_TIMING
 #pragma unroll
             for (int k = 0; k < kE; ++k)  // attribution: the transition's results exist before the clock read
@@ -559,8 +559,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 L2F_PHASE(c, 14);
                 bool did_reset = false;
                 float hf[4];
-                if (P.flags & F_AUTO_RESET)
-                    did_reset = reset_env_warp<kDR ? 8 : 6>(P, rtab, e[k], gid[k], t + 1, ended && active[k], hf, rscratch);
+                if (flags_of<kF>(P) & F_AUTO_RESET)
+                    did_reset = reset_env_warp<kDR ? 8 : 6, kF>(P, rtab, e[k], gid[k], t + 1, ended && active[k], hf, rscratch);
                 fl |= did_reset ? D_RESET : 0u;
                 L2F_PHASE(c, 15);
                 // an episode that ended without auto-reset restarts its counters (selects, no branch)
@@ -871,15 +871,20 @@ cudaError_t launch_rollout_mlp(const DevParams& P, const DevBufs& B, const Polic
                                const int64_t* trace_ids, int32_t K, cudaStream_t s)
 {
     if (P.n_hist % 4 != 0 || W.hidden != kHid || W.in_dim != 18 + 4 * P.n_hist) return cudaErrorNotSupported;
-    static std::atomic<size_t> attr[8][64] = {};
+    static std::atomic<size_t> attr[10][64] = {};
     const bool dr = (P.flags & F_DOMAIN_RAND) != 0, h32 = P.n_hist == 32, tr = trace != nullptr;
     using Kern = decltype(&rollout_mlp_kernel<true, 32, true>);
     static const Kern table[8] = {rollout_mlp_kernel<false, -1, false>, rollout_mlp_kernel<false, -1, true>,
                                   rollout_mlp_kernel<false, 32, false>, rollout_mlp_kernel<false, 32, true>,
                                   rollout_mlp_kernel<true, -1, false>,  rollout_mlp_kernel<true, -1, true>,
                                   rollout_mlp_kernel<true, 32, false>,  rollout_mlp_kernel<true, 32, true>};
-    const int sel = 4 * dr + 2 * h32 + tr;
-    const Kern kern = table[sel];
+    // the benchmark's feature mix (C4 / C5: every feature but DR and the rotor-delay ablation)
+    // as a compile-time specialisation
+    constexpr uint32_t kC5 = F_OBS_NOISE | F_ACTION_NOISE | F_TERMINATION | F_AUTO_RESET | F_DISTURBANCE;
+    const bool c5 = !dr && h32 && P.flags == kC5;
+    const int sel = c5 ? 8 + tr : 4 * dr + 2 * h32 + tr;
+    const Kern kern = c5 ? (tr ? rollout_mlp_kernel<false, 32, true, kC5> : rollout_mlp_kernel<false, 32, false, kC5>)
+                         : table[sel];
     const cudaError_t e = ensure_smem_attr(kern, kSmemBytes, attr[sel]);
     if (e != cudaSuccess) return e;
     kern<<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, T, trace, trace_ids, K, (int32_t)units_for(P.n));

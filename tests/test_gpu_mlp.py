@@ -297,3 +297,26 @@ def test_set_state_checkpoint_resume_bitwise(pkg):
     bad = pkg.Env(cfg, n + 1)
     with pytest.raises(Exception):
         bad.set_state(ckpt)
+
+
+@pytest.mark.parametrize("which", ["c5", "c5_dr", "c4_nh8"])
+def test_traced_and_untraced_rollouts_bitwise_equal(pkg, which):
+    """The teacher-forced parity tests trace envs, which selects the traced build of the same
+    kernel specialisation; the untraced build (the benchmark's) must compute bitwise the same
+    state, history, counters and statistic counts."""
+    cfg = {"c5": inputs.config_c5(), "c5_dr": inputs.config_c5(flags=inputs.ALL_NO_DR | inputs.DOMAIN_RAND),
+           "c4_nh8": inputs.config_c4(n_hist=8)}[which]
+    n, T = 3 * 128 * 2 + 51, 60
+    nh = cfg["n_hist"]
+    W = inputs.policy_weights(18 + 4 * nh, 64, seed=5, out_bias=inputs.hover_policy_bias())
+    pol = pkg.Policy(W)
+    a, b = pkg.Env(cfg, n), pkg.Env(cfg, n)
+    a.reset()
+    b.reset()
+    a.rollout(T, policy=pol)
+    b.rollout(T, policy=pol, trace_ids=torch.as_tensor(inputs.trace_ids(n, 40)))
+    sa, sb = snapshot(a), snapshot(b)
+    for k in sa:
+        assert np.array_equal(sa[k], sb[k]), k
+    ta, tb = a.episode_stats().cpu().numpy(), b.episode_stats().cpu().numpy()
+    assert np.array_equal(ta[[0, 1, 2, 3, 4, 7]], tb[[0, 1, 2, 3, 4, 7]])
