@@ -558,10 +558,11 @@ struct Trans {
 // action map, RK4 dynamics, reward on s' (Q12), termination (Q14),
 // truncation (Q15).  Episode counters are advanced; the caller handles history and reset.
 // Exploration-noise normals of step t (stream ACT, Q20); zeros when the feature is off.
+template <uint32_t kF = kAnyFlags>
 __device__ __forceinline__ void action_noise(const DevParams& P, uint32_t gid, uint32_t t, float z[4])
 {
     z[0] = z[1] = z[2] = z[3] = 0.0f;
-    if (P.flags & F_ACTION_NOISE) {
+    if (flags_of<kF>(P) & F_ACTION_NOISE) {
         box_muller2(draw(P, gid, t, S_ACT, 0), z);
     }
 }
@@ -865,12 +866,13 @@ __device__ __forceinline__ void observe_core_z(const DevParams& P, const float* 
     }
 }
 
+template <uint32_t kF = kAnyFlags>
 __device__ __forceinline__ void observe_core(const DevParams& P, const float* s, uint32_t gid, uint32_t t,
                                              float o[kObsCore])
 {
     float z[20];
-    if (P.flags & F_OBS_NOISE) obs_noise_blocks(P, gid, t, 0, 5, z);
-    observe_core_z(P, s, z, o);
+    if (flags_of<kF>(P) & F_OBS_NOISE) obs_noise_blocks(P, gid, t, 0, 5, z);
+    observe_core_z<kF>(P, s, z, o);
 }
 
 // Logical history entry H[k] (k-th most recent action, most recent first) at step t:

@@ -111,10 +111,16 @@ __device__ __forceinline__ void stats_block_end(const StatPk& st, double* srow, 
 // ---------------------------------------------------------------------------------------
 // l2f_step: one transition for every env.
 // ---------------------------------------------------------------------------------------
-template <bool kDR>
+// kF: the feature flags as a compile-time set (kAnyFlags: read P.flags).  kStdOut: the outputs are
+// exactly obs_core + reward + flags (the common request), so the output tests fold away.
+template <bool kDR, uint32_t kF = kAnyFlags, bool kStdOut = false>
 __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const DevParams P, const DevBufs B,
                                                           const float* __restrict__ act, const StepOutDev O)
 {
+    const uint32_t flags = flags_of<kF>(P);
+    const bool want_final = !kStdOut && O.final_state, want_core = kStdOut || O.obs_core;
+    const bool want_dense = !kStdOut && O.obs_dense, want_critic = !kStdOut && O.obs_critic;
+    const bool want_reward = kStdOut || O.reward, want_flags = kStdOut || O.flags;
     __shared__ double srow[(kStepBlock / 32) * kStatsLen];
     __shared__ uint4 rscratch[(kStepBlock / 32) * kResetScratch];  // cooperative reset scratch per warp
     const int64_t N = P.n;
@@ -134,18 +140,19 @@ __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const D
     }
     Trans o;
     float za[4];
-    action_noise(P, gid, t, za);
-    transition<kDR>(P, stage_of(P, t), e, gid, t, a, za, o);
+    action_noise<kF>(P, gid, t, za);
+    transition<kDR, kF>(P, stage_of(P, t), e, gid, t, a, za, o);
     uint32_t fl = o.flags;
-    if (active && O.final_state) {
+    if (active && want_final) {
         soa_store<kStateDim>(O.final_state, i, (uint32_t)N, e.s);
     }
     const bool ended = active && (fl & (D_TERM | D_TRUNC));
     statpk_episode(st, o, ended);
     bool did_reset = false;
     float hf[4];
-    if (P.flags & F_AUTO_RESET) {
-        did_reset = reset_env_warp<kDR ? 8 : 6>(P, nullptr, e, gid, t + 1, ended, hf, rscratch + (threadIdx.x >> 5) * kResetScratch);
+    if (flags & F_AUTO_RESET) {
+        did_reset = reset_env_warp<kDR ? 8 : 6, kF>(P, nullptr, e, gid, t + 1, ended, hf,
+                                                    rscratch + (threadIdx.x >> 5) * kResetScratch);
         if (did_reset) fl |= D_RESET;
     } else if (ended) {
         e.ep_step = 0;
@@ -160,21 +167,21 @@ __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const D
         }
         store_state(P, B, i, e);
         if (did_reset) store_episode_consts(P, B, i, e);
-        if (O.obs_core || O.obs_dense) {
+        if (want_core || want_dense) {
             float ob[kObsCore];
-            observe_core(P, e.s, gid, t + 1, ob);
-            if (O.obs_core) {
+            observe_core<kF>(P, e.s, gid, t + 1, ob);
+            if (want_core) {
                 soa_store<kObsCore>(O.obs_core, i, (uint32_t)N, ob);
             }
-            if (O.obs_dense) write_dense(P, B, i, ob, t + 1, O.obs_dense + i * (kObsCore + 4 * P.n_hist));
+            if (want_dense) write_dense(P, B, i, ob, t + 1, O.obs_dense + i * (kObsCore + 4 * P.n_hist));
         }
-        if (O.obs_critic) {
+        if (want_critic) {
             float oc[kObsCritic];
             observe_critic(e.s, e.dist, oc);
             soa_store<kObsCritic>(O.obs_critic, i, (uint32_t)N, oc);
         }
-        if (O.reward) O.reward[i] = o.reward;
-        if (O.flags) O.flags[i] = (uint8_t)fl;
+        if (want_reward) O.reward[i] = o.reward;
+        if (want_flags) O.flags[i] = (uint8_t)fl;
     }
     stats_block_end(st, srow, 0.0, B.slots + (size_t)blockIdx.x * kStatsLen);
 }
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(kStepBlock) reset_kernel(const DevParams P, co
 // Open-loop fused rollout: T transitions with the state in registers (N3).  Actions from a
 // [T][4][N] buffer or the Philox RAND_ACT stream.  The history ring stays in HBM.
 // ---------------------------------------------------------------------------------------
-template <bool kDR, bool kTrace>
+template <bool kDR, bool kTrace, uint32_t kF = kAnyFlags>
 __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevParams P, const DevBufs B,
                                                                      const float* __restrict__ act, int32_t T,
                                                                      float* __restrict__ trace,
@@ -269,15 +276,15 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
         }
         Trans o;
         float za[4];
-        action_noise(P, gid, t, za);
-        transition<kDR>(P, W, e, gid, t, a, za, o);
+        action_noise<kF>(P, gid, t, za);
+        transition<kDR, kF>(P, W, e, gid, t, a, za, o);
         uint32_t fl = o.flags;
         const bool ended = active && (fl & (D_TERM | D_TRUNC));
         statpk_episode(st, o, ended);
         bool did_reset = false;
         float hf[4];
-        if (P.flags & F_AUTO_RESET) {
-            did_reset = reset_env_warp<kDR ? 8 : 6>(P, nullptr, e, gid, t + 1, ended, hf, rscratch + (threadIdx.x >> 5) * kResetScratch);
+        if (flags_of<kF>(P) & F_AUTO_RESET) {
+            did_reset = reset_env_warp<kDR ? 8 : 6, kF>(P, nullptr, e, gid, t + 1, ended, hf, rscratch + (threadIdx.x >> 5) * kResetScratch);
             if (did_reset) fl |= D_RESET;
         } else if (ended) {
             e.ep_step = 0;
@@ -434,7 +441,14 @@ cudaError_t launch_step_plain(const DevParams& P, const DevBufs& B, const float*
                               cudaStream_t s)
 {
     const int64_t grid = (P.n + kStepBlock - 1) / kStepBlock;
-    if (P.flags & F_DOMAIN_RAND)
+    // compile-time specialisations for the configs' feature mixes with the common outputs
+    constexpr uint32_t kC2 = F_OBS_NOISE | F_ACTION_NOISE | F_TERMINATION | F_AUTO_RESET | F_DISTURBANCE;
+    const bool std_out = O.obs_core && O.reward && O.flags && !O.obs_dense && !O.obs_critic && !O.final_state;
+    if (std_out && P.flags == (kC2 | F_DOMAIN_RAND))
+        step_kernel<true, kC2 | F_DOMAIN_RAND, true><<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, act, O);
+    else if (std_out && P.flags == kC2)
+        step_kernel<false, kC2, true><<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, act, O);
+    else if (P.flags & F_DOMAIN_RAND)
         step_kernel<true><<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, act, O);
     else
         step_kernel<false><<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, act, O);
@@ -454,8 +468,12 @@ cudaError_t launch_rollout_open(const DevParams& P, const DevBufs& B, const floa
 {
     const int64_t grid = (P.n + kRolloutBlock - 1) / kRolloutBlock;
     const bool dr = (P.flags & F_DOMAIN_RAND) != 0, tr = trace != nullptr;
+    constexpr uint32_t kC5 = F_OBS_NOISE | F_ACTION_NOISE | F_TERMINATION | F_AUTO_RESET | F_DISTURBANCE;
     auto kern = dr ? (tr ? rollout_open_kernel<true, true> : rollout_open_kernel<true, false>)
                    : (tr ? rollout_open_kernel<false, true> : rollout_open_kernel<false, false>);
+    // compile-time feature mixes: dynamics only (C1, the paper's benchmark mode) and C2/C5 features
+    if (!tr && P.flags == 0u) kern = rollout_open_kernel<false, false, 0u>;
+    if (!tr && P.flags == kC5) kern = rollout_open_kernel<false, false, kC5>;
     kern<<<(unsigned)grid, kRolloutBlock, 0, s>>>(P, B, act, T, trace, trace_ids, K);
     return cudaGetLastError();
 }

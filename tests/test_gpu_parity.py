@@ -500,3 +500,27 @@ def test_rollout_split_across_many_curriculum_stages(pkg):
         assert np.array_equal(s1[k], s2[k]), k
     for j, i in enumerate(range(0, n, 97)):
         assert np.array_equal(tr[:, j, 25], np.array([r[i] for r in rew], dtype=np.float32)), i
+
+
+@pytest.mark.parametrize("cfg_name", ["c2", "c3"])
+def test_specialised_step_equals_generic_bitwise(pkg, cfg_name):
+    """l2f_step with exactly obs_core + reward + flags requested runs a build specialised at
+    compile time on the config's feature mix; requesting an extra output selects the generic
+    build.  Both must produce bitwise-identical state, observation, reward and flags (the
+    parity tests above exercise the generic build against the oracle)."""
+    cfg = {"c2": inputs.config_c2(), "c3": inputs.config_c3()}[cfg_name]
+    n, T = 3000, 12
+    acts = dev_actions(inputs.actions_near_hover(T, n, seed=9))
+    a, b = pkg.Env(cfg, n), pkg.Env(cfg, n)
+    a.reset()
+    b.reset()
+    oa = a.make_out(obs_core=True, reward=True, flags=True)
+    ob = b.make_out(obs_core=True, reward=True, flags=True, final_state=True)
+    for k in range(T):
+        a.step(acts[k].contiguous(), oa)
+        b.step(acts[k].contiguous(), ob)
+        for key in ("obs_core", "reward", "flags"):
+            assert torch.equal(oa[key], ob[key]), (k, key)
+    sa, sb = snapshot(a), snapshot(b)
+    for key in sa:
+        assert np.array_equal(sa[key], sb[key]), key
