@@ -577,14 +577,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                         // one register quad stored N_H / 2 times (C++ stores: asm operands made the
                         // compiler build a fresh quad per store)
                         const uint32_t h01 = tc::pack_h2(hf[0], hf[1]), h23 = tc::pack_h2(hf[2], hf[3]);
-                        const uint4 hv = make_uint4(h01, h23, h01, h23);
-                        uint8_t* const row = smem + (a1_row(c, k) - sbase);
+                        if constexpr (kNH == 32) {
+                            smem_check(a1_row(c, k) + 4 * kChunkA, 16 * kChunkA);
+                            tc::sts128_x16<kChunkA>(a1_row(c, k) + 4 * kChunkA, h01, h23, h01, h23);
+                        } else {
+                            const uint4 hv = make_uint4(h01, h23, h01, h23);
+                            uint8_t* const row = smem + (a1_row(c, k) - sbase);
 #pragma unroll
-                        for (int q = 0; q < kMaxHist / 2; ++q)
-                            if (q < NH / 2) {
-                                smem_check(a1_row(c, k) + (4 + q) * kChunkA, 16);
-                                *reinterpret_cast<uint4*>(row + (4 + q) * kChunkA) = hv;
-                            }
+                            for (int q = 0; q < kMaxHist / 2; ++q)
+                                if (q < NH / 2) {
+                                    smem_check(a1_row(c, k) + (4 + q) * kChunkA, 16);
+                                    *reinterpret_cast<uint4*>(row + (4 + q) * kChunkA) = hv;
+                                }
+                        }
                     }
                 }
                 if (kTrace && tslot[k] >= 0) {

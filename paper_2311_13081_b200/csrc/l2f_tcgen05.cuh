@@ -300,6 +300,20 @@ __device__ __forceinline__ void sts128(uint32_t saddr, uint32_t a, uint32_t b, u
 {
     asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
+// The same 16 bytes at saddr + k * stride for k = 0..15, as 32 volatile 8-byte stores of one
+// register pair (ptxas otherwise fuses them into 16-byte stores and copies the quad for each).
+template <uint32_t kStride>
+__device__ __forceinline__ void sts128_x16(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+{
+#define L2F_ST16(k) "st.volatile.shared.v2.b32 [%0+" #k "*%5], {%1,%2};\n\tst.volatile.shared.v2.b32 [%0+" #k "*%5+8], {%3,%4};\n\t"
+    asm volatile(L2F_ST16(0) L2F_ST16(1) L2F_ST16(2) L2F_ST16(3) L2F_ST16(4) L2F_ST16(5) L2F_ST16(6) L2F_ST16(7)
+                     L2F_ST16(8) L2F_ST16(9) L2F_ST16(10) L2F_ST16(11) L2F_ST16(12) L2F_ST16(13) L2F_ST16(14)
+                         L2F_ST16(15)::"r"(saddr),
+                 "r"(a), "r"(b), "r"(c), "r"(d), "n"(kStride)
+                 : "memory");
+#undef L2F_ST16
+}
+
 __device__ __forceinline__ void sts64(uint32_t saddr, uint32_t a, uint32_t b)
 {
     asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(saddr), "r"(a), "r"(b) : "memory");
