@@ -43,16 +43,22 @@ DT = 0.01
 STEP_BYTES_DR = 68 + 16 + 24 + 20 + 8 + 68 + 8 + 16 + 72 + 4 + 1
 #  tensor-core FLOPs of the actor MLP 146 -> 64 -> 64 -> 4 per env-step
 MLP_FLOPS = 2 * (146 * 64 + 64 * 64 + 64 * 4)
-#  scalar (non-tensor) operations of one env-step, counted from the method's arithmetic with a
-#  fused multiply-add or a transcendental counted as one op (DESIGN.md section 5.5 table):
-#  fused MLP rollout (obs noise, obs, MLP epilogue, action noise, RK4, reward, amortised reset)
-ALU_OPS_PER_ENV_STEP = 1071
-#  open-loop rollout with Philox random actions (no observation, no MLP)
-ALU_OPS_PER_ENV_STEP_OPEN = 657
-#  the same with every feature off (C1 flags 0: no noise, termination, reset): random action 56,
-#  clip + RPM map 12, RK4 428, reward/termination/counters 32, history + statistics 4
-ALU_OPS_PER_ENV_STEP_DYN = 532
+#  Scalar (non-tensor) work of one env-step for the ALU (issue) roofline: the method's arithmetic
+#  instructions per env-step counted mechanically from the kernel's SASS (scripts/alu_ops.py over
+#  the committed ncu --set full capture -> profiles/alu_ops.json).  The
+#  round-1 hand table is kept beside it for comparison (it counted packed FFMA2 pairs as two).
+ALU_OPS_HAND = {"mlp": 1071, "open_c5": 657, "open_dyn": 532}
 SMS = 148
+
+
+def alu_ops(kind):
+    """(method ops per env-step, source) of kernel kind 'mlp' / 'open_c5' / 'open_dyn' / 'step'."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "alu_ops.json")) as f:
+            d = json.load(f)[kind]
+        return d["method_ops_per_env_step"], d["source"]
+    except Exception:
+        return ALU_OPS_HAND[kind], "hand count (DESIGN.md section 5.5; profiles/alu_ops.json missing)"
 
 
 def traffic(key):
@@ -336,13 +342,15 @@ def main():
     f_clk = (clocks["sm_mhz"] or pk["sm_max_mhz"]) * 1e6
     k_rate = n * T / (k_ms / 1e3)
     alu_peak = SMS * 128 * f_clk / 1e12
-    ops = ALU_OPS_PER_ENV_STEP if args.mode == "mlp" else ALU_OPS_PER_ENV_STEP_OPEN
+    kind = "mlp" if args.mode == "mlp" else "open_c5"
+    ops, ops_src = alu_ops(kind)
     roof = {"bound": "alu", "kernel": "rollout_mlp_kernel" if args.mode == "mlp" else "rollout_open_kernel",
             "achieved": ops * k_rate / 1e12, "peak": alu_peak, "unit": "Tops/s",
-            "frac": ops * k_rate / 1e12 / alu_peak, "ops_per_env_step": ops,
-            "traffic": traffic("mlp" if args.mode == "mlp" else "open"),
-            "traffic_note": "DRAM read+write bytes per launch, ncu --set full (profiles/latest_traffic.json; "
-                            "captured at T=100: the rollout moves state once per tile, independent of T)",
+            "frac": ops * k_rate / 1e12 / alu_peak, "ops_per_env_step": ops, "ops_source": ops_src,
+            "frac_round1_hand_count": ALU_OPS_HAND[kind] * k_rate / 1e12 / alu_peak,
+            "traffic": traffic(kind),
+            "traffic_note": "DRAM read+write bytes of one launch of the same kernel and workload (ncu --set full, "
+                            "profiles/latest_traffic.json): state and history move once per env per launch",
             "peak_source": f"148 SMs x 128 lanes x {f_clk / 1e6:.0f} MHz (median SM clock sampled in the timed region)",
             "tensor": {"achieved": MLP_FLOPS * k_rate / 1e12, "peak": pk["bf16_tflops_sustained"],
                        "unit": "TFLOP/s", "frac": MLP_FLOPS * k_rate / 1e12 / pk["bf16_tflops_sustained"],
@@ -510,6 +518,7 @@ def secondary(pkg, inputs, torch, dev, pk, f_clk):
                           "sim_seconds_per_wall_second": rate * DT,
                           "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                                        "frac": gbs / pk["hbm_gbs"], "traffic": traffic("step"),
+                                       "traffic_note": "DRAM read+write bytes of one launch (ncu --set full)",
                                        "bytes_per_env_step": STEP_BYTES_DR, "peak_source": pk["source"]}}
     # e2e of the step API through host buffers (pinned): H2D actions, D2H obs/reward/flags
     ha = acts[0].cpu().pin_memory()
@@ -557,13 +566,14 @@ def secondary(pkg, inputs, torch, dev, pk, f_clk):
     ms = e0.elapsed_time(e1)
     rate = n * 1000 / (ms / 1e3)
     alu = SMS * 128 * f_clk / 1e12
+    ops_dyn, ops_dyn_src = alu_ops("open_dyn")
     out["open_loop_dynamics"] = {"value": rate, "unit": "env-steps/s", "ms": ms,
                                  "workload": "2^20 envs x 1000 steps, Philox random actions, no noise/termination",
                                  "vs_paper_T2000": rate / 1.284e9,
-                                 "roofline": {"bound": "alu", "achieved": ALU_OPS_PER_ENV_STEP_DYN * rate / 1e12,
+                                 "roofline": {"bound": "alu", "achieved": ops_dyn * rate / 1e12,
                                               "peak": alu, "unit": "Tops/s",
-                                              "frac": ALU_OPS_PER_ENV_STEP_DYN * rate / 1e12 / alu,
-                                              "ops_per_env_step": ALU_OPS_PER_ENV_STEP_DYN}}
+                                              "frac": ops_dyn * rate / 1e12 / alu,
+                                              "ops_per_env_step": ops_dyn, "ops_source": ops_dyn_src}}
     del env
     # the full C5 env step without the actor MLP (Philox random actions), for the MLP's share
     n = 1 << 21
