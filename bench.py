@@ -277,10 +277,18 @@ def main():
     from paper_2311_13081_b200 import dist as l2fdist
 
     world, rank, local = dist_setup(args)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # One rank per GPU over NCCL.  L2F_DIST_BACKEND=gloo (tests only) runs the same multi-rank
+    # path with host-side collectives, so several ranks can share the one GPU of a test box (the
+    # ranks' kernels never wait on one another: the only exchange is the stats all-reduce).
+    backend = os.environ.get("L2F_DIST_BACKEND", "nccl")
+    gpu = local if backend == "nccl" else local % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     pk = peaks()
     n = args.envs_per_gpu
     T = args.T
@@ -314,7 +322,7 @@ def main():
     stats_buf.zero_()
     l0 = pkg.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(gpu) as clk:
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
