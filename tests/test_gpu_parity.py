@@ -524,3 +524,25 @@ def test_specialised_step_equals_generic_bitwise(pkg, cfg_name):
     sa, sb = snapshot(a), snapshot(b)
     for key in sa:
         assert np.array_equal(sa[key], sb[key]), key
+
+
+@pytest.mark.parametrize("cfg_name", ["c1", "c5"])
+def test_open_loop_specialised_equals_traced_bitwise(pkg, cfg_name):
+    """The untraced open-loop rollout of the C1 (dynamics only) and C2/C5 feature mixes runs a
+    build specialised at compile time on the flags; the traced build (the one the trajectory
+    parity tests above check against the oracle) must compute bitwise the same state, history,
+    counters and statistic counts, with recorded and with Philox random actions."""
+    cfg = {"c1": inputs.config_c1(), "c5": inputs.config_c5()}[cfg_name]
+    n, T = 1000, 80
+    acts = dev_actions(inputs.actions_near_hover(T, n, seed=4))
+    for a_in in (acts, None):
+        e1, e2 = pkg.Env(cfg, n), pkg.Env(cfg, n)
+        e1.reset()
+        e2.reset()
+        e1.rollout(T, actions=a_in)
+        e2.rollout(T, actions=a_in, trace_ids=torch.arange(0, n, 53, device="cuda"))
+        s1, s2 = snapshot(e1), snapshot(e2)
+        for k in s1:
+            assert np.array_equal(s1[k], s2[k]), k
+        t1, t2 = e1.episode_stats().cpu().numpy(), e2.episode_stats().cpu().numpy()
+        assert np.array_equal(t1[[0, 1, 2, 3, 4, 7]], t2[[0, 1, 2, 3, 4, 7]])
