@@ -382,7 +382,9 @@ __device__ __forceinline__ GroupCtx make_ctx(uint32_t sbase)
     // per-MMA R2UR waterfall loop in the issuing thread)
     const int g = __shfl_sync(0xffffffffu, (int)(threadIdx.x / kM), 0), r = threadIdx.x % kM;
     const uint32_t tbase = __shfl_sync(0xffffffffu, *reinterpret_cast<const uint32_t*>(smem + OFF_TMEM), 0);
-    const uint32_t lane_off = (uint32_t)(32 * (r / 32)) << 16;
+    // the warp's TMEM lane quadrant, also from a broadcast (so the per-warp TMEM row addresses
+    // of the epilogues and the noise stash are uniform too)
+    const uint32_t lane_off = (uint32_t)(32 * __shfl_sync(0xffffffffu, (int)((threadIdx.x / 32) % 4), 0)) << 16;
     GroupCtx c;
     c.a1 = sbase + OFF_A1 + g * kE * kA1Bytes;
     c.a1_row = c.a1 + r * 16;
