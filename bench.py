@@ -583,6 +583,25 @@ def secondary(pkg, inputs, torch, dev, pk, f_clk):
                                               "frac": ops_dyn * rate / 1e12 / alu,
                                               "ops_per_env_step": ops_dyn, "ops_source": ops_dyn_src}}
     del env
+    # the paper's own simulator benchmark shape: 8192 envs (64 blocks x 128 threads) x
+    # 10^6 steps of forward dynamics, 100 Hz; here with Philox random actions, one rollout call
+    n, T = 8192, 1_000_000
+    env = pkg.Env(cfg, n, device=dev)
+    env.reset()
+    env.rollout(1000)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    env.rollout(T)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    rate = n * T / (ms / 1e3)
+    out["paper_P165_shape"] = {"value": rate, "unit": "env-steps/s", "ms": ms,
+                               "workload": "8192 envs x 1e6 steps, dynamics only (C1 flags), Philox random actions: "
+                                           "the shape of the paper's T2000 measurement (P:165); latency-bound "
+                                           "(256 warps on 592 schedulers)",
+                               "vs_paper_T2000": rate / 1.284e9}
+    del env
     # the full C5 env step without the actor MLP (Philox random actions), for the MLP's share
     n = 1 << 21
     env = pkg.Env(inputs.config_c5(), n, device=dev)
