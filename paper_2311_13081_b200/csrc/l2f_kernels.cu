@@ -228,7 +228,10 @@ __global__ void __launch_bounds__(kStepBlock) reset_kernel(const DevParams P, co
 // Open-loop fused rollout: T transitions with the state in registers (N3).  Actions from a
 // [T][4][N] buffer or the Philox RAND_ACT stream.  The history ring stays in HBM.
 // ---------------------------------------------------------------------------------------
-template <bool kDR, bool kTrace, uint32_t kF = kAnyFlags>
+// kPhilox: actions from the Philox RAND_ACT stream (act == nullptr); the next step's draw is then
+// issued before this step's transition, so its integer chain overlaps the RK4's FP chain (the
+// latency-bound small configs gain most).
+template <bool kDR, bool kTrace, uint32_t kF = kAnyFlags, bool kPhilox = false>
 __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevParams P, const DevBufs B,
                                                                      const float* __restrict__ act, int32_t T,
                                                                      float* __restrict__ trace,
@@ -255,12 +258,18 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
     int slot = P.hist_slot0;  // (t mod N_H), advanced incrementally
     const uint32_t t_last = P.t0 + (uint32_t)T;
     uint32_t t = P.t0;
+    float a_next[4];
+    if constexpr (kPhilox) random_action(P, gid, t, a_next);
     for (int sg = 0; sg < P.n_stages; ++sg) {  // curriculum stages of this launch
     const StageW& W = P.stage[sg];
     for (const uint32_t t_stop = stage_stop(P, sg, t_last); t < t_stop; ++t) {
         const int32_t k = (int32_t)(t - P.t0);
         float a[4];
-        if (act) {
+        if constexpr (kPhilox) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) a[c] = a_next[c];
+            random_action(P, gid, t + 1, a_next);
+        } else if (act) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) a[c] = active ? __ldg(act + ((int64_t)k * 4 + c) * N + i) : 0.0f;
         } else {
@@ -471,9 +480,20 @@ cudaError_t launch_rollout_open(const DevParams& P, const DevBufs& B, const floa
     constexpr uint32_t kC5 = F_OBS_NOISE | F_ACTION_NOISE | F_TERMINATION | F_AUTO_RESET | F_DISTURBANCE;
     auto kern = dr ? (tr ? rollout_open_kernel<true, true> : rollout_open_kernel<true, false>)
                    : (tr ? rollout_open_kernel<false, true> : rollout_open_kernel<false, false>);
-    // compile-time feature mixes: dynamics only (C1, the paper's benchmark mode) and C2/C5 features
-    if (!tr && P.flags == 0u) kern = rollout_open_kernel<false, false, 0u>;
-    if (!tr && P.flags == kC5) kern = rollout_open_kernel<false, false, kC5>;
+    // compile-time feature mixes: dynamics only (C1, the paper's benchmark mode) and C2/C5 features.
+    // The early Philox draw pays off when the launch is latency-bound (at most ~4 warps per
+    // scheduler: C1, C2, the paper's 8192-env shape: +13-15 %) and costs issue slots when it is
+    // throughput-bound (2^20 envs: -2.6 %), so it is used for the small launches only.
+    static std::atomic<int> sms_cache[64] = {};
+    const int dev = current_device();
+    int sms = sms_cache[dev].load();
+    if (sms == 0) {
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+        sms_cache[dev].store(sms);
+    }
+    const bool ph = act == nullptr && P.n <= (int64_t)sms * 512;
+    if (!tr && P.flags == 0u) kern = ph ? rollout_open_kernel<false, false, 0u, true> : rollout_open_kernel<false, false, 0u>;
+    if (!tr && P.flags == kC5) kern = ph ? rollout_open_kernel<false, false, kC5, true> : rollout_open_kernel<false, false, kC5>;
     kern<<<(unsigned)grid, kRolloutBlock, 0, s>>>(P, B, act, T, trace, trace_ids, K);
     return cudaGetLastError();
 }
