@@ -228,10 +228,11 @@ __global__ void __launch_bounds__(kStepBlock) reset_kernel(const DevParams P, co
 // Open-loop fused rollout: T transitions with the state in registers (N3).  Actions from a
 // [T][4][N] buffer or the Philox RAND_ACT stream.  The history ring stays in HBM.
 // ---------------------------------------------------------------------------------------
-// kPhilox: actions from the Philox RAND_ACT stream (act == nullptr); the next step's draw is then
-// issued before this step's transition, so its integer chain overlaps the RK4's FP chain (the
-// latency-bound small configs gain most).
-template <bool kDR, bool kTrace, uint32_t kF = kAnyFlags, bool kPhilox = false>
+// kPipe (small, latency-bound launches): the next step's action inputs -- the recorded action's
+// loads, or the Philox RAND_ACT draw, and the exploration-noise draw -- are issued before this
+// step's transition, so the load latency and the integer chains overlap the RK4's FP chain.
+// (kPipe = 1: recorded actions, 2: Philox actions; 0: no prefetch)
+template <bool kDR, bool kTrace, uint32_t kF = kAnyFlags, int kPipe = 0>
 __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevParams P, const DevBufs B,
                                                                      const float* __restrict__ act, int32_t T,
                                                                      float* __restrict__ trace,
@@ -258,17 +259,31 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
     int slot = P.hist_slot0;  // (t mod N_H), advanced incrementally
     const uint32_t t_last = P.t0 + (uint32_t)T;
     uint32_t t = P.t0;
-    float a_next[4];
-    if constexpr (kPhilox) random_action(P, gid, t, a_next);
+    const float* act_i = act ? act + i : nullptr;  // (kPipe: act_i[(k * 4 + c) N] = a_c of step k)
+    float a_next[4], za_next[4];
+    if constexpr (kPipe == 1) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a_next[c] = active ? __ldg(act_i + (int64_t)c * N) : 0.0f;
+    } else if constexpr (kPipe == 2) {
+        random_action(P, gid, t, a_next);
+    }
+    if constexpr (kPipe != 0) action_noise<kF>(P, gid, t, za_next);
     for (int sg = 0; sg < P.n_stages; ++sg) {  // curriculum stages of this launch
     const StageW& W = P.stage[sg];
     for (const uint32_t t_stop = stage_stop(P, sg, t_last); t < t_stop; ++t) {
         const int32_t k = (int32_t)(t - P.t0);
-        float a[4];
-        if constexpr (kPhilox) {
+        float a[4], za[4];
+        if constexpr (kPipe != 0) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) a[c] = a_next[c];
-            random_action(P, gid, t + 1, a_next);
+            for (int c = 0; c < 4; ++c) a[c] = a_next[c], za[c] = za_next[c];
+            if constexpr (kPipe == 1) {
+                const int64_t kn = k + 1 < T ? k + 1 : k;  // (the last step re-reads its own row)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) a_next[c] = active ? __ldg(act_i + (kn * 4 + c) * N) : 0.0f;
+            } else {
+                random_action(P, gid, t + 1, a_next);
+            }
+            action_noise<kF>(P, gid, t + 1, za_next);
         } else if (act) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) a[c] = active ? __ldg(act + ((int64_t)k * 4 + c) * N + i) : 0.0f;
@@ -284,8 +299,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_open_kernel(const DevPa
             for (int c = 0; c < 4; ++c) tr[17 + c] = a[c];
         }
         Trans o;
-        float za[4];
-        action_noise<kF>(P, gid, t, za);
+        if constexpr (kPipe == 0) action_noise<kF>(P, gid, t, za);
         transition<kDR, kF>(P, W, e, gid, t, a, za, o);
         uint32_t fl = o.flags;
         const bool ended = active && (fl & (D_TERM | D_TRUNC));
@@ -481,9 +495,9 @@ cudaError_t launch_rollout_open(const DevParams& P, const DevBufs& B, const floa
     auto kern = dr ? (tr ? rollout_open_kernel<true, true> : rollout_open_kernel<true, false>)
                    : (tr ? rollout_open_kernel<false, true> : rollout_open_kernel<false, false>);
     // compile-time feature mixes: dynamics only (C1, the paper's benchmark mode) and C2/C5 features.
-    // The early Philox draw pays off when the launch is latency-bound (at most ~4 warps per
-    // scheduler: C1, C2, the paper's 8192-env shape: +13-15 %) and costs issue slots when it is
-    // throughput-bound (2^20 envs: -2.6 %), so it is used for the small launches only.
+    // Prefetching the next step's action inputs pays off when the launch is latency-bound (at
+    // most ~4 warps per scheduler: C1, C2, the paper's 8192-env shape) and costs issue slots when
+    // it is throughput-bound (2^20 envs with Philox actions: -2.6 %), so small launches only.
     static std::atomic<int> sms_cache[64] = {};
     const int dev = current_device();
     int sms = sms_cache[dev].load();
@@ -491,9 +505,13 @@ cudaError_t launch_rollout_open(const DevParams& P, const DevBufs& B, const floa
         if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
         sms_cache[dev].store(sms);
     }
-    const bool ph = act == nullptr && P.n <= (int64_t)sms * 512;
-    if (!tr && P.flags == 0u) kern = ph ? rollout_open_kernel<false, false, 0u, true> : rollout_open_kernel<false, false, 0u>;
-    if (!tr && P.flags == kC5) kern = ph ? rollout_open_kernel<false, false, kC5, true> : rollout_open_kernel<false, false, kC5>;
+    const bool pipe = P.n <= (int64_t)sms * 512;
+    if (!tr && P.flags == 0u)
+        kern = !pipe ? rollout_open_kernel<false, false, 0u> : act ? rollout_open_kernel<false, false, 0u, 1>
+                                                                   : rollout_open_kernel<false, false, 0u, 2>;
+    if (!tr && P.flags == kC5)
+        kern = !pipe ? rollout_open_kernel<false, false, kC5> : act ? rollout_open_kernel<false, false, kC5, 1>
+                                                                    : rollout_open_kernel<false, false, kC5, 2>;
     kern<<<(unsigned)grid, kRolloutBlock, 0, s>>>(P, B, act, T, trace, trace_ids, K);
     return cudaGetLastError();
 }
