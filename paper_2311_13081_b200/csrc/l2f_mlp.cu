@@ -714,17 +714,20 @@ __device__ __forceinline__ void lissajous_ref(const TrackDev& S, double dt_over_
     v[2] = 0.0f;
 }
 
+// kF / kNH: compile-time flags and N_H for the common tracking setup (observation noise on,
+// N_H = 32), as for the rollout; kAnyFlags / -1 read them at run time.
+template <uint32_t kF = kAnyFlags, int kNH = -1>
 __global__ void __launch_bounds__(kThreads, 1)
     track_mlp_kernel(const DevParams P, const DevBufs B, const PolicyDev W, const TrackDev S, int32_t n_units)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t sbase = tc::smem_u32(smem);
-    const int NH = P.n_hist;
+    const int NH = kNH >= 0 ? kNH : P.n_hist;
     setup_cta(W, sbase, NH, &P);
     GroupCtx c = make_ctx(sbase);
     const int64_t N = P.n;
     const int r = threadIdx.x % kM;
-    const bool obs_noise = (P.flags & F_OBS_NOISE) != 0;
+    const bool obs_noise = (flags_of<kF>(P) & F_OBS_NOISE) != 0;
     const StageW& SW = P.stage[0];
     for (int u = blockIdx.x * kG + (int)(threadIdx.x / kM); u < n_units; u += gridDim.x * kG) {
         int64_t i[kE];
@@ -773,7 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < kE; ++k) {
                 float ob[kObsCore], z[20], pr[3], vr[3];
                 if (obs_noise) load_obs_noise(c, k, z);
-                observe_core_z(P, e[k].s, z, ob);
+                observe_core_z<kF>(P, e[k].s, z, ob);
                 lissajous_ref(S, dtT[k], w[k], ks, pr, vr);
 #pragma unroll
                 for (int j = 0; j < 3; ++j) {  // setpoint shift with clipping (Q29)
@@ -783,7 +786,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 write_obs_row(c, k, ob);
             }
             float a[kE][4];
-            mlp_group<-1>(c, sbase, NH, rot, a, [&](int l) {
+            mlp_group<kNH>(c, sbase, NH, rot, a, [&](int l) {
 #pragma unroll
                 for (int k = 0; k < kE; ++k) stash_obs_noise(P, c, k, gid[k], t + 1, l - 1);
             });
@@ -792,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < kE; ++k) {
                 const float za[4] = {0.f, 0.f, 0.f, 0.f};
                 Trans o;
-                transition<false>(P, SW, e[k], gid[k], t, a[k], za, o);
+                transition<false, kF>(P, SW, e[k], gid[k], t, a[k], za, o);
                 if (NH > 0)
                     tc::sts64(hist_addr(c, k, wpos), tc::pack_h2(o.a[0], o.a[1]), tc::pack_h2(o.a[2], o.a[3]));
                 float pr[3], vr[3];
@@ -902,10 +905,12 @@ cudaError_t launch_track_mlp(const DevParams& P, const DevBufs& B, const PolicyD
                              cudaStream_t s)
 {
     if (P.n_hist % 4 != 0 || W.hidden != kHid || W.in_dim != 18 + 4 * P.n_hist) return cudaErrorNotSupported;
-    static std::atomic<size_t> attr[64] = {};
-    const cudaError_t e = ensure_smem_attr(track_mlp_kernel, kSmemBytes, attr);
+    static std::atomic<size_t> attr[2][64] = {};
+    const bool spec = P.flags == F_OBS_NOISE && P.n_hist == 32;
+    const auto kern = spec ? track_mlp_kernel<F_OBS_NOISE, 32> : track_mlp_kernel<>;
+    const cudaError_t e = ensure_smem_attr(kern, kSmemBytes, attr[spec]);
     if (e != cudaSuccess) return e;
-    track_mlp_kernel<<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, S, (int32_t)units_for(P.n));
+    kern<<<grid_for(P.n), kThreads, kSmemBytes, s>>>(P, B, W, S, (int32_t)units_for(P.n));
     return cudaGetLastError();
 }
 
