@@ -154,6 +154,7 @@ struct GroupCtx {
     uint32_t bar_id;
     uint32_t phase;
     uint32_t r;          // thread index within the group
+    uint32_t wig;        // warp index within the group (broadcast: uniform, so the issue branches are too)
 #ifdef L2F_PHASE_TIMING
     uint32_t ph_last;    // debug build only: clock() at the last phase boundary
 #endif
@@ -226,7 +227,7 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
     rot = __shfl_sync(0xffffffffu, rot, 0);  // warp-uniform for the compiler (uniform registers)
     handoff_to_mma(c);
     L2F_PHASE(c, 1);
-    if (c.r / 32 == 0) {  // the whole warp, converged; elect.sync picks the issuing lane
+    if (c.wig == 0) {  // the whole warp, converged; elect.sync picks the issuing lane
         tc::fence_after();
         const uint64_t dW1o = tc::make_desc(sbase + OFF_W1O, kHid * 16, 128);
         const uint64_t dW1h = tc::make_desc(sbase + OFF_W1H, 128, 2u * 4u * (uint32_t)n_hist * 16u) + 4u * rot;
@@ -259,7 +260,7 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
     L2F_PHASE(c, 4);
     handoff_to_mma(c);
     L2F_PHASE(c, 5);
-    if (c.r / 32 == 1) {
+    if (c.wig == 1) {
         tc::fence_after();
         const uint64_t dW2 = tc::make_desc(sbase + OFF_W2, kHid * 16, 128);
 #pragma unroll
@@ -277,7 +278,7 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
     L2F_PHASE(c, 8);
     handoff_to_mma(c);
     L2F_PHASE(c, 9);
-    if (c.r / 32 == 2) {
+    if (c.wig == 2) {
         tc::fence_after();
         const uint64_t dW3 = tc::make_desc(sbase + OFF_W3, 256, 128);
 #pragma unroll
@@ -404,6 +405,7 @@ __device__ __forceinline__ GroupCtx make_ctx(uint32_t sbase)
     c.bar_id = 1 + g;
     c.phase = 0;
     c.r = r;
+    c.wig = (uint32_t)__shfl_sync(0xffffffffu, (int)((threadIdx.x / 32) % 4), 0);
 #ifdef L2F_PHASE_TIMING
     if ((threadIdx.x & 31) == 0)
         for (int k = 0; k < 16; ++k) g_ph[threadIdx.x >> 5][k] = 0ull;
