@@ -90,13 +90,7 @@ __device__ __forceinline__ void stats_block_end(const StatPk& st, double* srow, 
 {
     L2F_CHECK(blockIdx.x < gridDim.x, "statistics slot");
     const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const bool any = __any_sync(0xffffffffu, st.ep_term != 0u);
-    if (any) {
-        statpk_warp_to_smem(st, srow + warp * kStatsLen);
-    } else if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-        for (int j = 0; j < kStatsLen; ++j) srow[warp * kStatsLen + j] = 0.0;
-    }
+    statpk_warp_to_smem(st, srow + warp * kStatsLen);  // (unconditional: straight-line code)
     // producer/consumer named barrier: warps 1.. arrive and retire at once, warp 0 waits for
     // the rows and writes the block's slot (the block's SM slot frees up sooner than with a
     // full __syncthreads)
