@@ -26,6 +26,9 @@
 #include "l2f_internal.h"
 #include "l2f_tcgen05.cuh"
 
+#ifndef L2F_HANDOFF_ARRIVE
+#define L2F_HANDOFF_ARRIVE 1  // only the issuing warp waits at each hand-off (0: all four)
+#endif
 #ifndef L2F_MLP_E
 #define L2F_MLP_E 1  // envs (tiles) per thread
 #endif
@@ -191,14 +194,25 @@ __device__ __forceinline__ void epilogue_hidden(const GroupCtx& c, int k)
 }
 
 // The group's 128 threads hand their freshly written A rows (and finished TMEM reads) to the
-// MMA issuer: proxy fence + tcgen05 fence + a 128-thread named barrier (id 1 + group).  (Variants
-// where only the issuing warp waits -- mbarrier arrive/wait, or bar.arrive for the other three
-// warps -- measured no faster.)
-__device__ __forceinline__ void handoff_to_mma(GroupCtx& c)
+// MMA issuer: proxy fence + tcgen05 fence + a 128-thread named barrier (id 1 + group) on which
+// only the issuing warp waits; the other three arrive (bar.arrive) and run on into their hook.
+// Safe to reuse the barrier: every warp next waits on this layer's MMA, which the issuer starts
+// only after the barrier completed.  (+0.7 % once the issue branches were uniform; round 1
+// measured no gain with the divergent ones.)
+__device__ __forceinline__ void handoff_to_mma(GroupCtx& c, uint32_t issuer_warp)
 {
     tc::fence_proxy_async();
     tc::fence_before();
+#if L2F_HANDOFF_ARRIVE
+    // only the issuing warp waits
+    if (c.wig == issuer_warp)
+        tc::named_sync(c.bar_id, kM);
+    else
+        tc::named_arrive(c.bar_id, kM);
+#else
+    (void)issuer_warp;
     tc::named_sync(c.bar_id, kM);
+#endif
 }
 
 __device__ __forceinline__ void wait_mma(GroupCtx& c)
@@ -225,7 +239,7 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
     // stay below 256 KB, so the 14-bit field never carries)
     L2F_PHASE(c, 0);
     rot = __shfl_sync(0xffffffffu, rot, 0);  // warp-uniform for the compiler (uniform registers)
-    handoff_to_mma(c);
+    handoff_to_mma(c, 0);
     L2F_PHASE(c, 1);
     if (c.wig == 0) {  // the whole warp, converged; elect.sync picks the issuing lane
         tc::fence_after();
@@ -258,7 +272,7 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
     for (int k = 0; k < kE; ++k) epilogue_hidden(c, k);
     tc::tmem_wait_st();
     L2F_PHASE(c, 4);
-    handoff_to_mma(c);
+    handoff_to_mma(c, 1);
     L2F_PHASE(c, 5);
     if (c.wig == 1) {
         tc::fence_after();
@@ -276,7 +290,7 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
     for (int k = 0; k < kE; ++k) epilogue_hidden(c, k);
     tc::tmem_wait_st();
     L2F_PHASE(c, 8);
-    handoff_to_mma(c);
+    handoff_to_mma(c, 2);
     L2F_PHASE(c, 9);
     if (c.wig == 2) {
         tc::fence_after();
