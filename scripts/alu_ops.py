@@ -153,9 +153,18 @@ def main():
            "overhead_by_opcode": {k: v / units for k, v in overhead.most_common(25)},
            "sass_histogram_per_env_step": {k: hist[k] / units for k in SASS_CLASSES},
            "sass_histogram_executed": {k: hist[k] for k in SASS_CLASSES}}
+    # the whole-kernel executed-instruction metric of the same capture (the per-PC counts above come
+    # from an instrumented replay, where mbarrier / barrier wait loops spin more often)
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    try:
+        res["smsp_inst_executed_per_env_step"] = float(rr[2][rr[0].index("smsp__inst_executed.sum")]) / units
+    except (ValueError, IndexError):
+        pass
     os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
     json.dump(res, open(out, "w"), indent=1)
-    print(json.dumps({k: res[k] for k in ("method_ops_per_env_step", "overhead_per_env_step", "total_per_env_step")}))
+    print(json.dumps({k: res.get(k) for k in ("method_ops_per_env_step", "overhead_per_env_step", "total_per_env_step",
+                                              "smsp_inst_executed_per_env_step")}))
 
 
 if __name__ == "__main__":
