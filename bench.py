@@ -286,6 +286,10 @@ def main():
     dev = torch.device("cuda", gpu)
     if world > 1:
         if backend == "nccl":
+            # NCCL's init log (ranks, devices, transports) on stderr, whoever launched the ranks
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
