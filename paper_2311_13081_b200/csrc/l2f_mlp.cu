@@ -180,16 +180,25 @@ __shared__ unsigned long long g_ph[kThreads / 32][16];
 #endif
 
 // Epilogue of L1 / L2 for tile k: accumulator row -> relu -> fp16 -> this lane's A2 row in TMEM.
+#ifndef L2F_EPI_LOADS
+#define L2F_EPI_LOADS 2  // 16-column TMEM loads in flight per wait (measured: 1 -2 %, 4 -2.7 % vs 2)
+#endif
 __device__ __forceinline__ void epilogue_hidden(const GroupCtx& c, int k)
 {
+    constexpr int kL = L2F_EPI_LOADS;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        uint32_t v[16];
-        tc::tmem_ld16(c.tmem_row + 64 * k + 16 * q, v);
+    for (int q0 = 0; q0 < 4; q0 += kL) {
+        uint32_t v[kL][16];
+#pragma unroll
+        for (int j = 0; j < kL; ++j) tc::tmem_ld16(c.tmem_row + 64 * k + 16 * (q0 + j), v[j]);
         tc::tmem_wait_ld();
-        tc::tmem_st8u(c.a2_trow + 40 * k + 8 * q, tc::relu_pack(v[0], v[1]), tc::relu_pack(v[2], v[3]),
-                      tc::relu_pack(v[4], v[5]), tc::relu_pack(v[6], v[7]), tc::relu_pack(v[8], v[9]),
-                      tc::relu_pack(v[10], v[11]), tc::relu_pack(v[12], v[13]), tc::relu_pack(v[14], v[15]));
+#pragma unroll
+        for (int j = 0; j < kL; ++j)
+            tc::tmem_st8u(c.a2_trow + 40 * k + 8 * (q0 + j), tc::relu_pack(v[j][0], v[j][1]),
+                          tc::relu_pack(v[j][2], v[j][3]), tc::relu_pack(v[j][4], v[j][5]),
+                          tc::relu_pack(v[j][6], v[j][7]), tc::relu_pack(v[j][8], v[j][9]),
+                          tc::relu_pack(v[j][10], v[j][11]), tc::relu_pack(v[j][12], v[j][13]),
+                          tc::relu_pack(v[j][14], v[j][15]));
     }
 }
 
