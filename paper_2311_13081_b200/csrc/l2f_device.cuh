@@ -833,6 +833,16 @@ __device__ __forceinline__ void obs_noise_blocks(const DevParams& P, uint32_t gi
     }
 }
 
+// o += sigma (block of each component) * z: the observation noise (Q8).
+__device__ __forceinline__ void add_obs_noise(const DevParams& P, const float z[20], float o[kObsCore])
+{
+#pragma unroll
+    for (int i = 0; i < kObsCore; ++i) {
+        const int g = i < 3 ? 0 : (i < 12 ? 1 : (i < 15 ? 2 : 3));
+        o[i] = fmaf(P.obs_sigma[g], z[i], o[i]);
+    }
+}
+
 // Noisy core observation {p, R(q) row-major, v, w} (Q8) from given normals.
 template <uint32_t kF = kAnyFlags>
 __device__ __forceinline__ void observe_core_z(const DevParams& P, const float* s, const float z[20],
@@ -857,13 +867,7 @@ __device__ __forceinline__ void observe_core_z(const DevParams& P, const float* 
     o[15] = s[10];
     o[16] = s[11];
     o[17] = s[12];
-    if (flags_of<kF>(P) & F_OBS_NOISE) {
-#pragma unroll
-        for (int i = 0; i < kObsCore; ++i) {
-            const int g = i < 3 ? 0 : (i < 12 ? 1 : (i < 15 ? 2 : 3));
-            o[i] = fmaf(P.obs_sigma[g], z[i], o[i]);
-        }
-    }
+    if (flags_of<kF>(P) & F_OBS_NOISE) add_obs_noise(P, z, o);
 }
 
 template <uint32_t kF = kAnyFlags>

@@ -536,9 +536,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < kE; ++k) {
                 float ob[kObsCore];
-                float z[20];
-                if (obs_noise) load_obs_noise(c, k, z);
-                observe_core_z<kF>(P, e[k].s, z, ob);
+                if (obs_noise) {
+                    // the noise-free observation is formed while the stashed normals load from TMEM
+                    uint32_t v[16], w[4];
+                    tc::tmem_ld16(c.stash_row + 24 * k, v);
+                    tc::tmem_ld4(c.stash_row + 24 * k + 16, w);
+                    float z0[20];
+#pragma unroll
+                    for (int j = 0; j < 20; ++j) z0[j] = 0.0f;
+                    observe_core_z<0u>(P, e[k].s, z0, ob);
+                    tc::tmem_wait_ld();
+                    float z[20];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) z[j] = __uint_as_float(v[j]);
+                    z[16] = __uint_as_float(w[0]);
+                    z[17] = __uint_as_float(w[1]);
+                    z[18] = z[19] = 0.0f;
+                    add_obs_noise(P, z, ob);
+                } else {
+                    float z[20];
+                    observe_core_z<kF>(P, e[k].s, z, ob);
+                }
                 write_obs_row(c, k, ob);
             }
             float a[kE][4], za[kE][4];
