@@ -11,13 +11,8 @@
 #define L2F_STEP_MINB 6  // resident 128-thread blocks per SM the register budget targets (4: 96 us, 5: 88, 6: 87, 7: 91, 8: 97 at C3)
 #endif
 
-#ifndef L2F_STEP_BULK
-#define L2F_STEP_BULK 0  // bulk-staged (TMA engine) l2f_step: measured slower, off
-#endif
-
 #include "l2f_device.cuh"
 #include "l2f_internal.h"
-#include "l2f_tcgen05.cuh"
 
 namespace l2f {
 
@@ -183,214 +178,6 @@ __global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_kernel(const D
         if (want_flags) O.flags[i] = (uint8_t)fl;
     }
     stats_block_end(st, srow, 0.0, B.slots + (size_t)blockIdx.x * kStatsLen);
-}
-
-// ---------------------------------------------------------------------------------------
-// l2f_step, bulk-staged variant (standard outputs, the C2 / C3 feature mixes): the block's
-// inputs arrive in shared memory as 1-D bulk copies on the TMA engine (one per 128-env chunk of
-// each array, completing on an mbarrier), the outputs leave the same way (bulk stores of the
-// staged chunks).  Each thread then reads and writes its own env's slots with 32-bit shared
-// addresses and immediate offsets: the per-env 64-bit address arithmetic of ~40 global
-// accesses and the pointer loads become ~28 bulk copies per 128 envs.  Several blocks per SM
-// overlap one block's copies with the others' arithmetic.  The ragged last block (fewer than
-// 128 envs) loads and stores per thread.  Same device functions in the same order as
-// step_kernel: bitwise identical results (test_specialised_step_equals_generic_bitwise).
-// ---------------------------------------------------------------------------------------
-namespace sb {  // shared-memory map of one block's 128 envs (bytes)
-constexpr uint32_t kT = kStepBlock;
-constexpr uint32_t STATE = 0;                     // 4 float4 groups + w_m3: read, then rewritten in place
-constexpr uint32_t DIST = STATE + 4 * kStateDim * kT;  // float4 group + float2 tail (read only)
-constexpr uint32_t DR = DIST + 4 * 6 * kT;            // float4 group + float tail (read only)
-constexpr uint32_t EP_STEP = DR + 4 * 5 * kT;         // read, rewritten in place
-constexpr uint32_t EP_RET = EP_STEP + 4 * kT;         // read, rewritten in place
-constexpr uint32_t ACT = EP_RET + 4 * kT;             // [4] x kT floats (read only)
-constexpr uint32_t HIST = ACT + 16 * kT;              // out: float4 per env
-constexpr uint32_t OBS = HIST + 16 * kT;              // out: [18] x kT floats
-constexpr uint32_t REW = OBS + 4 * kObsCore * kT;     // out
-constexpr uint32_t FLG = REW + 4 * kT;                // out: bytes
-constexpr uint32_t BYTES = FLG + kT;
-constexpr int kLoads = 15, kStores = 28;
-static_assert(kStateDim == 17 && kT == 128, "map assumes the 17-D state and 128-env blocks");
-}  // namespace sb
-
-// Shared-memory slot views of one env (grouped layout of grp_load, chunk = kT envs).
-template <int C>
-__device__ __forceinline__ void grp_lds(const unsigned char* sm, uint32_t off, int t, float* out)
-{
-    constexpr int G = C / 4, R = C % 4;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        const float4 v = reinterpret_cast<const float4*>(sm + off + 16 * sb::kT * g)[t];
-        out[4 * g] = v.x, out[4 * g + 1] = v.y, out[4 * g + 2] = v.z, out[4 * g + 3] = v.w;
-    }
-    if constexpr (R == 1) {
-        out[4 * G] = reinterpret_cast<const float*>(sm + off + 16 * sb::kT * G)[t];
-    } else if constexpr (R == 2) {
-        const float2 v = reinterpret_cast<const float2*>(sm + off + 16 * sb::kT * G)[t];
-        out[4 * G] = v.x, out[4 * G + 1] = v.y;
-    }
-}
-template <int C>
-__device__ __forceinline__ void grp_sts(unsigned char* sm, uint32_t off, int t, const float* v)
-{
-    constexpr int G = C / 4, R = C % 4;
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-        reinterpret_cast<float4*>(sm + off + 16 * sb::kT * g)[t] =
-            make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
-    if constexpr (R == 1) reinterpret_cast<float*>(sm + off + 16 * sb::kT * G)[t] = v[4 * G];
-    static_assert(R < 2, "store tails of 0 or 1 components");
-}
-
-// Bulk copy k of a full block (chunk of kT envs starting at env i0), one per lane of warp 0,
-// formed branch-free (selects): global byte offset = row_bytes * N + esz * i0, size esz * kT.
-// Loads: state groups 0-3 + tail, dist group + tail, dr group + tail, ep_step, ep_return, the
-// 4 action rows.  Stores: state groups 0-3 + tail, ep_step, ep_return, history slot, 18 obs
-// rows, reward, flags.
-__device__ __forceinline__ void bulk_load_lane(int k, const DevBufs& B, const float* act, int64_t N, int64_t i0,
-                                               uint32_t sbase, uint32_t mbar)
-{
-    constexpr uint32_t T = sb::kT;
-    const char* base = k < 5 ? (const char*)B.state
-                     : k < 7 ? (const char*)B.dist
-                     : k < 9 ? (const char*)B.dr
-                     : k == 9 ? (const char*)B.ep_step
-                     : k == 10 ? (const char*)B.ep_return : (const char*)act;
-    const uint32_t row = k < 4 ? 16u * k : k == 4 ? 64u : (k == 6 || k == 8) ? 16u : k >= 11 ? 4u * (k - 11) : 0u;
-    const uint32_t esz = (k < 4 || k == 5 || k == 7) ? 16u : k == 6 ? 8u : 4u;
-    const uint32_t soff = k < 4 ? sb::STATE + 16 * T * k : k == 4 ? sb::STATE + 64 * T
-                        : k == 5 ? sb::DIST : k == 6 ? sb::DIST + 16 * T
-                        : k == 7 ? sb::DR : k == 8 ? sb::DR + 16 * T
-                        : k == 9 ? sb::EP_STEP : k == 10 ? sb::EP_RET : sb::ACT + 4 * T * (k - 11);
-    tc::bulk_g2s(sbase + soff, base + (int64_t)row * N + (int64_t)esz * i0, esz * T, mbar);
-}
-
-__device__ __forceinline__ void bulk_store_lane(int k, const DevBufs& B, const StepOutDev& O, int slot, int64_t N,
-                                                int64_t i0, uint32_t sbase)
-{
-    constexpr uint32_t T = sb::kT;
-    char* base = k < 5 ? (char*)B.state
-               : k == 5 ? (char*)B.ep_step
-               : k == 6 ? (char*)B.ep_return
-               : k == 7 ? (char*)B.hist
-               : k < 8 + kObsCore ? (char*)O.obs_core
-               : k == 8 + kObsCore ? (char*)O.reward : (char*)O.flags;
-    const uint32_t row = k < 4 ? 16u * k : k == 4 ? 64u : k == 7 ? 16u * slot : (k >= 8 && k < 8 + kObsCore) ? 4u * (k - 8) : 0u;
-    const uint32_t esz = (k < 4 || k == 7) ? 16u : k == 9 + kObsCore ? 1u : 4u;
-    const uint32_t soff = k < 4 ? sb::STATE + 16 * T * k : k == 4 ? sb::STATE + 64 * T
-                        : k == 5 ? sb::EP_STEP : k == 6 ? sb::EP_RET : k == 7 ? sb::HIST
-                        : k < 8 + kObsCore ? sb::OBS + 4 * T * (k - 8)
-                        : k == 8 + kObsCore ? sb::REW : sb::FLG;
-    tc::bulk_s2g(base + (int64_t)row * N + (int64_t)esz * i0, sbase + soff, esz * T);
-}
-
-template <bool kDR, uint32_t kF>
-__global__ void __launch_bounds__(kStepBlock, L2F_STEP_MINB) step_bulk_kernel(const DevParams P, const DevBufs B,
-                                                               const float* __restrict__ act, const StepOutDev O)
-{
-    __shared__ __align__(128) unsigned char sm[sb::BYTES];
-    __shared__ double srow[(kStepBlock / 32) * kStatsLen];
-    __shared__ uint4 rscratch[(kStepBlock / 32) * kResetScratch];
-    __shared__ __align__(8) uint64_t mbar;
-    const uint32_t flags = flags_of<kF>(P);
-    const int64_t N = P.n;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t i0 = (int64_t)blockIdx.x * kStepBlock, i = i0 + tid;
-    const bool full = i0 + kStepBlock <= N;
-    const bool active = i < N;
-    const uint32_t t = P.t0;
-    const uint32_t gid = P.id_offset + (uint32_t)i;
-    const uint32_t sbase = tc::smem_u32(sm), mb = tc::smem_u32(&mbar);
-    const int slot = P.hist_slot0;  // t0 mod N_H (written for every env: deterministic ring)
-    L2F_CHECK(P.n_hist == 0 || (slot >= 0 && slot < P.n_hist), "history slot");
-    if (full) {
-        if (tid == 0) {
-            tc::mbar_init(mb, 1);
-            tc::fence_mbar_init();
-            constexpr uint32_t bytes = sb::kT * 4 * (kStateDim + 6 + (kDR ? 5 : 0) + 2 + 4);
-            tc::mbar_expect_tx(mb, bytes);
-        }
-        __syncthreads();
-        if (warp == 0 && lane < sb::kLoads && (kDR || lane < 7 || lane > 8)) bulk_load_lane(lane, B, act, N, i0, sbase, mb);
-    }
-    StatPk st;
-    statpk_zero(st);
-    EnvReg e;
-    float a[4];
-    if (full) {
-        tc::mbar_wait(mb, 0);
-        grp_lds<kStateDim>(sm, sb::STATE, tid, e.s);
-        grp_lds<6>(sm, sb::DIST, tid, e.dist);
-        if (kDR) {
-            grp_lds<5>(sm, sb::DR, tid, e.dr);
-        } else {
-#pragma unroll
-            for (int c = 0; c < 5; ++c) e.dr[c] = 1.0f;
-        }
-        e.ep_step = reinterpret_cast<const int32_t*>(sm + sb::EP_STEP)[tid];
-        e.ep_return = reinterpret_cast<const float*>(sm + sb::EP_RET)[tid];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) a[c] = reinterpret_cast<const float*>(sm + sb::ACT + 4 * sb::kT * c)[tid];
-    } else if (active) {
-        load_env<kDR>(P, B, i, e);
-        soa_load_ro<4>(act, i, (uint32_t)N, a);
-    } else {
-        dummy_env(e);
-        a[0] = a[1] = a[2] = a[3] = 0.0f;
-    }
-    Trans o;
-    float za[4];
-    action_noise<kF>(P, gid, t, za);
-    transition<kDR, kF>(P, stage_of(P, t), e, gid, t, a, za, o);
-    uint32_t fl = o.flags;
-    const bool ended = active && (fl & (D_TERM | D_TRUNC));
-    statpk_episode(st, o, ended);
-    bool did_reset = false;
-    float hf[4];
-    if (flags & F_AUTO_RESET) {
-        did_reset = reset_env_warp<kDR ? 8 : 6, kF>(P, nullptr, e, gid, t + 1, ended, hf,
-                                                    rscratch + warp * kResetScratch);
-        if (did_reset) fl |= D_RESET;
-    } else if (ended) {
-        e.ep_step = 0;
-        e.ep_return = 0.0f;
-    }
-    float ob[kObsCore];
-    observe_core<kF>(P, e.s, gid, t + 1, ob);
-    if (active) {
-        if (P.n_hist > 0 && did_reset) hist_restart(P, B, i, t + 1, hf);
-        if (did_reset) store_episode_consts(P, B, i, e);  // (rare: direct stores)
-    }
-    if (full) {
-        grp_sts<kStateDim>(sm, sb::STATE, tid, e.s);
-        reinterpret_cast<int32_t*>(sm + sb::EP_STEP)[tid] = e.ep_step;
-        reinterpret_cast<float*>(sm + sb::EP_RET)[tid] = e.ep_return;
-        reinterpret_cast<float4*>(sm + sb::HIST)[tid] = make_float4(o.a[0], o.a[1], o.a[2], o.a[3]);
-#pragma unroll
-        for (int j = 0; j < kObsCore; ++j) reinterpret_cast<float*>(sm + sb::OBS + 4 * sb::kT * j)[tid] = ob[j];
-        reinterpret_cast<float*>(sm + sb::REW)[tid] = o.reward;
-        sm[sb::FLG + tid] = (uint8_t)fl;
-        tc::fence_proxy_async();  // generic-proxy writes -> visible to the bulk copies
-        statpk_warp_to_smem(st, srow + warp * kStatsLen);
-        __syncthreads();
-        if (warp == 0) {
-            if (lane < sb::kStores && (lane != 7 || P.n_hist > 0)) {
-                bulk_store_lane(lane, B, O, slot, N, i0, sbase);
-                tc::bulk_commit();
-            }
-            stat_rows_to_slot(srow, kStepBlock / 32, 0.0, B.slots + (size_t)blockIdx.x * kStatsLen);
-            tc::bulk_wait_read();  // the block's shared memory stays until the copies have read it
-        }
-    } else {
-        if (active) {
-            if (P.n_hist > 0) B.hist[(int64_t)slot * N + i] = make_float4(o.a[0], o.a[1], o.a[2], o.a[3]);
-            store_state(P, B, i, e);
-            soa_store<kObsCore>(O.obs_core, i, (uint32_t)N, ob);
-            O.reward[i] = o.reward;
-            O.flags[i] = (uint8_t)fl;
-        }
-        stats_block_end(st, srow, 0.0, B.slots + (size_t)blockIdx.x * kStatsLen);
-    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -674,16 +461,7 @@ cudaError_t launch_step_plain(const DevParams& P, const DevBufs& B, const float*
     // compile-time specialisations for the configs' feature mixes with the common outputs
     constexpr uint32_t kC2 = F_OBS_NOISE | F_ACTION_NOISE | F_TERMINATION | F_AUTO_RESET | F_DISTURBANCE;
     const bool std_out = O.obs_core && O.reward && O.flags && !O.obs_dense && !O.obs_critic && !O.final_state;
-    // bulk-staged variant: the [C][N] output / action rows of a 128-env chunk start on 16-byte
-    // boundaries (N % 4 == 0, 16-byte aligned buffers)
-    auto a16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
-    const bool bulk = L2F_STEP_BULK && std_out && P.n % 4 == 0 && a16(act) && a16(O.obs_core) && a16(O.reward) &&
-                      a16(O.flags);
-    if (bulk && P.flags == (kC2 | F_DOMAIN_RAND))
-        step_bulk_kernel<true, kC2 | F_DOMAIN_RAND><<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, act, O);
-    else if (bulk && P.flags == kC2)
-        step_bulk_kernel<false, kC2><<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, act, O);
-    else if (std_out && P.flags == (kC2 | F_DOMAIN_RAND))
+    if (std_out && P.flags == (kC2 | F_DOMAIN_RAND))
         step_kernel<true, kC2 | F_DOMAIN_RAND, true><<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, act, O);
     else if (std_out && P.flags == kC2)
         step_kernel<false, kC2, true><<<(unsigned)grid, kStepBlock, 0, s>>>(P, B, act, O);

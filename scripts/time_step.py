@@ -5,7 +5,7 @@ import torch
 import inputs
 import paper_2311_13081_b200 as pkg
 
-n = 1 << 20
+n = int(os.environ.get("L2F_N", 1 << 20))
 env = pkg.Env(inputs.config_c3(), n)
 env.reset()
 acts = [torch.tensor(inputs.actions_near_hover(1, n, seed=100 + k)[0], dtype=torch.float32, device="cuda") for k in range(8)]
@@ -19,4 +19,5 @@ for k in range(400):
     env.step(acts[k % 8], o)
 e1.record()
 torch.cuda.synchronize()
-print("step_us %.2f" % (e0.elapsed_time(e1) / 400 * 1e3))
+us = e0.elapsed_time(e1) / 400 * 1e3
+print("step_us %.2f n %d ns_per_kenv %.3f" % (us, n, us / n * 1e6))
