@@ -180,6 +180,9 @@ __shared__ unsigned long long g_ph[kThreads / 32][16];
 #endif
 
 // Epilogue of L1 / L2 for tile k: accumulator row -> relu -> fp16 -> this lane's A2 row in TMEM.
+#ifndef L2F_SKIP_TMEM_PROXY_FENCE
+#define L2F_SKIP_TMEM_PROXY_FENCE 1  // no shared-memory proxy fence before the TMEM-operand layers
+#endif
 #ifndef L2F_EPI_LOADS
 #define L2F_EPI_LOADS 2  // 16-column TMEM loads in flight per wait (measured: 1 -2 %, 4 -2.7 % vs 2)
 #endif
@@ -208,9 +211,14 @@ __device__ __forceinline__ void epilogue_hidden(const GroupCtx& c, int k)
 // Safe to reuse the barrier: every warp next waits on this layer's MMA, which the issuer starts
 // only after the barrier completed.  (+0.7 % once the issue branches were uniform; round 1
 // measured no gain with the divergent ones.)
+// kSmemA: the MMA reads an A operand the threads wrote to shared memory (layer 1: generic-proxy
+// stores -> async-proxy reads need the proxy fence, a MEMBAR.ALL.CTA in SASS); layers 2 / 3
+// take A from TMEM (tcgen05.st + wait::st + the thread-sync fence suffice) and B from weights
+// fenced once at kernel start, so their hand-offs skip it.
+template <bool kSmemA = true>
 __device__ __forceinline__ void handoff_to_mma(GroupCtx& c, uint32_t issuer_warp)
 {
-    tc::fence_proxy_async();
+    if (kSmemA || !L2F_SKIP_TMEM_PROXY_FENCE) tc::fence_proxy_async();
     tc::fence_before();
 #if L2F_HANDOFF_ARRIVE
     // only the issuing warp waits
@@ -281,7 +289,7 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
     for (int k = 0; k < kE; ++k) epilogue_hidden(c, k);
     tc::tmem_wait_st();
     L2F_PHASE(c, 4);
-    handoff_to_mma(c, 1);
+    handoff_to_mma<false>(c, 1);
     L2F_PHASE(c, 5);
     if (c.wig == 1) {
         tc::fence_after();
@@ -299,7 +307,7 @@ __device__ __forceinline__ void mlp_group(GroupCtx& c, uint32_t sbase, int n_his
     for (int k = 0; k < kE; ++k) epilogue_hidden(c, k);
     tc::tmem_wait_st();
     L2F_PHASE(c, 8);
-    handoff_to_mma(c, 2);
+    handoff_to_mma<false>(c, 2);
     L2F_PHASE(c, 9);
     if (c.wig == 2) {
         tc::fence_after();
