@@ -38,7 +38,7 @@ METHOD_FUNCTIONS = {
     "philox", "philox_rk", "draw", "unif", "ln_unit", "box_muller", "box_muller2", "obs_noise_blocks",
     "action_noise", "random_action", "uab",
     # observation, actor MLP activations / fp16 quantisation (Q21)
-    "observe_core_z", "observe_core", "observe_critic", "tanh_fast", "relu_pack", "pack_h2",
+    "observe_core_z", "observe_core", "observe_critic", "add_obs_noise", "tanh_fast", "relu_pack", "pack_h2",
     # dynamics, RK4, reward, termination
     "make_phys", "deriv", "pair_fma", "rk4_step", "state_finite", "stepped_state_finite", "transition",
     "reward_of", "stage_of",
