@@ -598,15 +598,20 @@ __device__ __forceinline__ void observe_critic(const float* s, const float* dist
     o[0] = s[0];
     o[1] = s[1];
     o[2] = s[2];
-    o[3] = 1.0f - 2.0f * (qy * qy + qz * qz);
-    o[4] = 2.0f * (qx * qy - qw * qz);
-    o[5] = 2.0f * (qx * qz + qw * qy);
-    o[6] = 2.0f * (qx * qy + qw * qz);
-    o[7] = 1.0f - 2.0f * (qx * qx + qz * qz);
-    o[8] = 2.0f * (qy * qz - qw * qx);
-    o[9] = 2.0f * (qx * qz - qw * qy);
-    o[10] = 2.0f * (qy * qz + qw * qx);
-    o[11] = 1.0f - 2.0f * (qx * qx + qy * qy);
+    // R(q) with every multiply-add written out as fmaf: the compiler's own contraction of
+    // a*b +- c*d may pick either product, and differently in two builds of this function
+    // (seen between the debug-check build's specialised and generic step kernels)
+    const float x2 = qx + qx, y2 = qy + qy, z2 = qz + qz;  // exact doublings
+    const float wx2 = qw * x2, wy2 = qw * y2, wz2 = qw * z2;
+    o[3] = fmaf(-qy, y2, fmaf(-qz, z2, 1.0f));
+    o[4] = fmaf(qx, y2, -wz2);
+    o[5] = fmaf(qx, z2, wy2);
+    o[6] = fmaf(qx, y2, wz2);
+    o[7] = fmaf(-qx, x2, fmaf(-qz, z2, 1.0f));
+    o[8] = fmaf(qy, z2, -wx2);
+    o[9] = fmaf(qx, z2, -wy2);
+    o[10] = fmaf(qy, z2, wx2);
+    o[11] = fmaf(-qx, x2, fmaf(-qy, y2, 1.0f));
 #pragma unroll
     for (int j = 0; j < 10; ++j) o[12 + j] = s[7 + j];  // v, w, w_m
 #pragma unroll
@@ -852,15 +857,20 @@ __device__ __forceinline__ void observe_core_z(const DevParams& P, const float* 
     o[0] = s[0];
     o[1] = s[1];
     o[2] = s[2];
-    o[3] = 1.0f - 2.0f * (qy * qy + qz * qz);
-    o[4] = 2.0f * (qx * qy - qw * qz);
-    o[5] = 2.0f * (qx * qz + qw * qy);
-    o[6] = 2.0f * (qx * qy + qw * qz);
-    o[7] = 1.0f - 2.0f * (qx * qx + qz * qz);
-    o[8] = 2.0f * (qy * qz - qw * qx);
-    o[9] = 2.0f * (qx * qz - qw * qy);
-    o[10] = 2.0f * (qy * qz + qw * qx);
-    o[11] = 1.0f - 2.0f * (qx * qx + qy * qy);
+    // R(q) with every multiply-add written out as fmaf: the compiler's own contraction of
+    // a*b +- c*d may pick either product, and differently in two builds of this function
+    // (seen between the debug-check build's specialised and generic step kernels)
+    const float x2 = qx + qx, y2 = qy + qy, z2 = qz + qz;  // exact doublings
+    const float wx2 = qw * x2, wy2 = qw * y2, wz2 = qw * z2;
+    o[3] = fmaf(-qy, y2, fmaf(-qz, z2, 1.0f));
+    o[4] = fmaf(qx, y2, -wz2);
+    o[5] = fmaf(qx, z2, wy2);
+    o[6] = fmaf(qx, y2, wz2);
+    o[7] = fmaf(-qx, x2, fmaf(-qz, z2, 1.0f));
+    o[8] = fmaf(qy, z2, -wx2);
+    o[9] = fmaf(qx, z2, -wy2);
+    o[10] = fmaf(qy, z2, wx2);
+    o[11] = fmaf(-qx, x2, fmaf(-qy, y2, 1.0f));
     o[12] = s[7];
     o[13] = s[8];
     o[14] = s[9];
