@@ -532,6 +532,31 @@ def secondary(pkg, inputs, torch, dev, pk, f_clk):
                                        "frac": gbs / pk["hbm_gbs"], "traffic": traffic("step"),
                                        "traffic_note": "DRAM read+write bytes of one launch (ncu --set full)",
                                        "bytes_per_env_step": STEP_BYTES_DR, "peak_source": pk["source"]}}
+    # the same 400 steps replayed from a CUDA graph of 50 l2f_step launches (what a training loop
+    # that captures its step does): no per-call launch gap, consecutive kernels back to back
+    gs = torch.cuda.Stream(device=dev)
+    gs.wait_stream(stream)
+    with torch.cuda.stream(gs):
+        env.step(acts[0], o)
+    stream.wait_stream(gs)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for k in range(50):
+            env.step(acts[k % 8], o)
+    graph.replay()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(reps // 50):
+        graph.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_g = e0.elapsed_time(e1) / (reps // 50 * 50)
+    gbs_g = STEP_BYTES_DR * n / (ms_g / 1e3) / 1e9
+    out["C3_step_api"]["graph"] = {"value": n / (ms_g / 1e3), "unit": "env-steps/s", "us_per_step": ms_g * 1e3,
+                                   "roofline_frac": gbs_g / pk["hbm_gbs"], "achieved_gbs": gbs_g,
+                                   "workload": "the same steps replayed from a CUDA graph of 50 l2f_step launches"}
+    del graph
     # e2e of the step API through host buffers (pinned): H2D actions, D2H obs/reward/flags
     ha = acts[0].cpu().pin_memory()
     hobs = torch.empty(18, n).pin_memory()
