@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool obs_noise = (flags_of<kF>(P) & F_OBS_NOISE) != 0;
 
     // unit u = tiles u kE .. u kE + kE - 1 (one per tile slot)
-    for (int u = blockIdx.x * kG + (int)(threadIdx.x / kM); u < n_units; u += gridDim.x * kG) {
+    for (int u = (int)(threadIdx.x / kM) * (int)gridDim.x + blockIdx.x; u < n_units; u += gridDim.x * kG) {
         StatPk st;
         statpk_zero(st);
         int64_t i[kE];
@@ -713,7 +713,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     setup_cta(W, sbase, NH);
     GroupCtx c = make_ctx(sbase);
     const int r = threadIdx.x % kM;
-    for (int u = blockIdx.x * kG + (int)(threadIdx.x / kM); u < n_units; u += gridDim.x * kG) {
+    for (int u = (int)(threadIdx.x / kM) * (int)gridDim.x + blockIdx.x; u < n_units; u += gridDim.x * kG) {
         int64_t i[kE];
 #pragma unroll
         for (int k = 0; k < kE; ++k) {
@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = threadIdx.x % kM;
     const bool obs_noise = (flags_of<kF>(P) & F_OBS_NOISE) != 0;
     const StageW& SW = P.stage[0];
-    for (int u = blockIdx.x * kG + (int)(threadIdx.x / kM); u < n_units; u += gridDim.x * kG) {
+    for (int u = (int)(threadIdx.x / kM) * (int)gridDim.x + blockIdx.x; u < n_units; u += gridDim.x * kG) {
         int64_t i[kE];
         bool active[kE];
         uint32_t gid[kE];
@@ -915,17 +915,21 @@ int64_t units_for(int64_t n) { return ((n + kM - 1) / kM + kE - 1) / kE; }
 }  // namespace
 
 // Upper bound of the rollout grid (statistics slots are sized with it; host-only arithmetic).
-int mlp_rollout_grid(int64_t n)
+int mlp_rollout_grid(int64_t n)  // upper bound of grid_for on any device (statistics slots)
 {
-    const int64_t g = (units_for(n) + kG - 1) / kG;
-    return (int)(g < 1024 ? g : 1024);
+    const int64_t g = units_for(n);
+    return (int)(g < 1 ? 1 : (g < 1024 ? g : 1024));
 }
 
+// One CTA per SM (or one per unit when there are fewer units than SMs).  Units are dealt
+// group-major: unit u of a round runs on CTA u mod grid, group u / grid, so a partial last
+// round (2^21 envs: 16384 tiles = 27.7 rounds of 148 x 4) leaves every SM with 2-3 busy groups
+// instead of 100 SMs with 4 and 48 idle, and the fewer groups per SM run faster.
 static int grid_for(int64_t n)
 {
-    const int64_t g = (units_for(n) + kG - 1) / kG;
+    const int64_t u = units_for(n);
     const int sms = sm_count();
-    return (int)(g < sms ? (g < 1 ? 1 : g) : sms);
+    return (int)(u < sms ? (u < 1 ? 1 : u) : sms);
 }
 
 cudaError_t launch_rollout_mlp(const DevParams& P, const DevBufs& B, const PolicyDev& W, int32_t T, float* trace,
