@@ -474,7 +474,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     GroupCtx c = make_ctx(sbase);
     const int64_t N = P.n;
     const int r = threadIdx.x % kM;
-    uint4* const rscratch = reinterpret_cast<uint4*>(smem + OFF_STAT) + (threadIdx.x >> 5) * kResetScratch;
+    // (the warp index broadcast from lane 0: a uniform value, so the address lives in a uniform
+    // register instead of being rematerialised in the step loop)
+    const uint32_t wcta = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+    uint4* const rscratch = reinterpret_cast<uint4*>(smem + OFF_STAT) + wcta * kResetScratch;
     const float4* const rtab = reinterpret_cast<const float4*>(smem + OFF_RTAB);
     double* const wrow = reinterpret_cast<double*>(smem + OFF_WSTAT) + (threadIdx.x >> 5) * kStatsLen;
     if ((threadIdx.x & 31) < kStatsLen) wrow[threadIdx.x & 31] = 0.0;
