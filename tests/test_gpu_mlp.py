@@ -320,3 +320,30 @@ def test_traced_and_untraced_rollouts_bitwise_equal(pkg, which):
         assert np.array_equal(sa[k], sb[k]), k
     ta, tb = a.episode_stats().cpu().numpy(), b.episode_stats().cpu().numpy()
     assert np.array_equal(ta[[0, 1, 2, 3, 4, 7]], tb[[0, 1, 2, 3, 4, 7]])
+
+
+@pytest.mark.parametrize("n_units", [1, 149, 2 * 148 * 4 + 300])
+def test_mlp_rollout_unit_dealing_covers_every_env_once(pkg, n_units):
+    """The rollout deals 128-env units group-major over min(units, SMs) CTAs:
+    one unit, more units than SMs but fewer than one full round, and more than two rounds with a
+    partial last one.  Every env is processed exactly once (the env-step count is N T) and its
+    result does not depend on where its unit ran (the tail envs equal a separate small env over
+    the same global ids, bitwise)."""
+    cfg = inputs.config_c5()
+    n = max(1, n_units * 128 - 45)
+    T = 12
+    W = inputs.policy_weights(146, 64, seed=11, out_bias=inputs.hover_policy_bias())
+    pol = pkg.Policy(W)
+    big = pkg.Env(cfg, n)
+    big.reset()
+    big.episode_stats(reset=True)
+    big.rollout(T, policy=pol)
+    st = big.episode_stats().cpu().numpy()
+    assert st[7] == n * T
+    k = min(n, 300)
+    tail = pkg.Env(cfg, k, env_id_offset=n - k)
+    tail.reset()
+    tail.rollout(T, policy=pol)
+    sb, stl = snapshot(big), snapshot(tail)
+    for key in ("state", "dist", "hist", "ep_step", "ep_return"):
+        assert np.array_equal(sb[key][..., n - k:], stl[key]), key
