@@ -5,8 +5,9 @@
 //   a_t = tanh(W3 q16(relu(W2 q16(relu(W1 q16(o_t) + b1)) + b2)) + b3)        (Q21)
 //   then the same env transition as l2f_step (l2f_device.cuh).
 //
-// Design (DESIGN.md section 4.3):
-//  * persistent CTA per SM, 3 tiles x 128 envs; thread r of a tile owns env row r, which is
+// Design (DESIGN.md section 5.3):
+//  * persistent CTA per SM, 4 tiles x 128 envs (one 128-thread group per tile, units dealt
+//    group-major over the CTAs); thread r of a tile owns env row r, which is
 //    both row r of the MMA A operand and TMEM lane r of the accumulator (32x32b loads);
 //  * operands fp16 in shared memory (SWIZZLE_NONE canonical layouts), accumulators fp32 in
 //    TMEM (64 columns per tile reused by the three layers); biases enter the MMA through a
@@ -18,7 +19,7 @@
 //    history beyond the one 8-byte slot write per env-step;
 //  * one thread per tile and layer (lane 0 of warp l - 1 for layer l) issues the MMAs after a
 //    128-thread named barrier; MMA
-//    completion is signalled through tcgen05.commit -> mbarrier.  The other two tiles' warps
+//    completion is signalled through tcgen05.commit -> mbarrier.  The other three tiles' warps
 //    keep the FP32/INT pipes busy while one tile waits on the tensor core.
 #include <cstdio>
 
